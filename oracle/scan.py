@@ -1,0 +1,69 @@
+"""O-2 round driver -- TEST INFRASTRUCTURE (see oracle/__init__.py).
+
+Turns one round of generated token ids into the per-request segment records the
+device scan must publish (R5-R13), following SURVEY.md 8(c) O-2 steps 1-6:
+
+  1. bytes: S = T[y_1] || ... || T[y_N] over the round's generated ids (specials
+     map to the empty string; prompt/observation inputs are never scanned,
+     SPEC.md:102); e_t = sum_{s<=t} |T[y_s]|.
+  2./3. cuts from oracle.segment (plain definition).
+  4. round end (EOS, max_new_tokens, forced-stream end, cancel): one FINAL record
+     for the tail S[c_last, |S|), possibly empty.
+  token_index of a cut = min{t : e_t >= c_j} - 1 (0-based index of the generated
+  token holding the cut's last byte: "emit completed pieces ... immediately",
+  PAPER.md:144).  FINAL carries N-1 (0xFFFFFFFF when the round generated nothing).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import DELIM_NONE, FLAG_CANCELLED, FLAG_FINAL, segment
+
+NO_TOKEN = 0xFFFFFFFF
+
+
+@dataclass(frozen=True)
+class Record:
+    round: int
+    seq: int
+    token_index: int
+    byte_offset: int
+    byte_len: int
+    delim_id: int
+    flags: int
+    data: bytes
+
+
+def round_length(tokens, eos: int, max_new: int) -> int:
+    """Number of generated tokens in the round: up to and including the first EOS,
+    at most max_new (R12)."""
+    n = min(len(tokens), max_new)
+    for i in range(n):
+        if eos >= 0 and tokens[i] == eos:
+            return i + 1
+    return n
+
+
+def round_records(tokens, vocab_bytes, kind: int, delims: list[bytes], max_seg: int,
+                  round_idx: int = 0, seq_start: int = 0, cancelled: bool = False):
+    """Records for one round whose generated ids are exactly `tokens` (already cut at
+    the round end).  Returns (records, stream_bytes)."""
+    pieces = [vocab_bytes[t] for t in tokens]
+    S = b"".join(pieces)
+    ends = []
+    acc = 0
+    for p in pieces:
+        acc += len(p)
+        ends.append(acc)
+    recs = []
+    c_prev = 0
+    seq = seq_start
+    for (c, did, fl) in segment(kind, delims, max_seg, S):
+        t1 = next(t for t, e in enumerate(ends) if e >= c)  # min{t : e_t >= c} - 1 (0-based)
+        recs.append(Record(round_idx, seq, t1, c_prev, c - c_prev, did, fl, S[c_prev:c]))
+        seq += 1
+        c_prev = c
+    last = len(tokens) - 1 if tokens else NO_TOKEN
+    recs.append(Record(round_idx, seq, last, c_prev, len(S) - c_prev, DELIM_NONE,
+                       FLAG_FINAL | (FLAG_CANCELLED if cancelled else 0), S[c_prev:]))
+    return recs, S
