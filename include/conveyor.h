@@ -1,0 +1,270 @@
+/*
+ * conveyor.h -- C ABI of libconveyor, the B200-native decode hot path under Conveyor
+ * (Xu, Kong, Chen, Zhuo: "Conveyor: Efficient Tool-aware LLM Serving with Tool Partial
+ * Execution", arXiv 2406.00059).  One engine = one GPU = one continuous-batching decode
+ * replica with a fused, device-side tool-trigger scan.
+ *
+ * The five calls of the paper's problem statement:
+ *   cvy_register_tool      "select a parser ... register both the parser and the plugin"
+ *                          (sec 3.2; workflow steps (a),(b))
+ *   cvy_submit_request     a user request enters the scheduler (step (1))
+ *   cvy_step               one decoding iteration for every in-flight request (step (2);
+ *                          continuous batching); the trigger scan runs in
+ *                          the sampling epilogue of the same launch (steps (3)-(5))
+ *   cvy_poll_segments      the host "periodically polls" the completed partial-execution
+ *                          pieces while decoding continues (step (8))
+ *   cvy_inject_observation "concatenates the original prompt, plans, and observations ...
+ *                          feeds them back" (step (g)) -- appended to the
+ *                          resident KV cache of the request as forced inputs.
+ *
+ * Conventions
+ *   - Every call returns cvy_status (0 OK, < 0 error).  Nothing throws or aborts across
+ *     the ABI.  cvy_last_error() returns a thread-local message for the last failure.
+ *   - CVY_E_CUDA is sticky: after a CUDA error the engine is dead; only destroy is valid.
+ *   - Device pointers in cvy_weights are BORROWED (caller-owned, e.g. torch tensors) and
+ *     must outlive the engine.  Every host array passed in is copied before the call
+ *     returns.  Output buffers are caller-owned.
+ *   - Threading: submit / inject / cancel / release may be called from any thread (queued
+ *     under a mutex, applied at the next step boundary).  cvy_step is called from one
+ *     driver thread; cvy_poll_segments from exactly one consumer thread.
+ *   - Build: sm_100a only.  No CPU fallback: without a B200 every device call fails with
+ *     CVY_E_CUDA.
+ */
+#ifndef CONVEYOR_H
+#define CONVEYOR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVY_ABI_VERSION 1
+
+typedef enum {
+    CVY_OK = 0,
+    CVY_E_INVAL = -1,    /* bad argument                                              */
+    CVY_E_NOMEM = -2,    /* host or device allocation failed                          */
+    CVY_E_FULL = -3,     /* no free slot / pages / input capacity: retry later         */
+    CVY_E_AGAIN = -4,    /* nothing to poll                                            */
+    CVY_E_NOTFOUND = -5, /* unknown request id or tool                                 */
+    CVY_E_STATE = -6,    /* call not valid in the current lifecycle state              */
+    CVY_E_DUP = -7,      /* duplicate tool name                                        */
+    CVY_E_CUDA = -8,     /* CUDA error or no usable sm_100 device (sticky)             */
+    CVY_E_NCCL = -9      /* NCCL error                                                 */
+} cvy_status;
+
+typedef enum { CVY_DTYPE_BF16 = 0, CVY_DTYPE_FP32 = 1 } cvy_dtype;
+
+/* Parser kinds ("Conveyor offers a set of parsers"; R5-R11).
+ * LITERAL: a segment ends at the shortest prefix ending in a registered delimiter
+ *          (e.g. "\n" or ";" for a code interpreter).
+ * JSON_MEMBER: a ',' at depth 1 or the bracket closing depth 1 ends a segment
+ *          ("field complete", validator).
+ * JSON_OBJECT: the bracket returning depth to 0 ends a segment ("a complete stage of the
+ *          plan"). */
+typedef enum { CVY_PARSER_LITERAL = 0, CVY_PARSER_JSON_MEMBER = 1, CVY_PARSER_JSON_OBJECT = 2 } cvy_parser_kind;
+
+/* Host dispatch policy only; the device path is identical in both modes. */
+typedef enum { CVY_MODE_PARTIAL = 0, CVY_MODE_SEQUENTIAL = 1 } cvy_exec_mode;
+
+enum { CVY_SEG_FINAL = 1, CVY_SEG_OVERFLOW = 2, CVY_SEG_CANCELLED = 4 };
+#define CVY_DELIM_NONE 0xFFFFu
+#define CVY_NO_TOKEN 0xFFFFFFFFu
+
+/* Model shape.  Mistral/Llama family: RMSNorm, RoPE (rotate-half), GQA, SwiGLU, no bias,
+ * untied LM head (R1-R3).  Requirements: head_dim in {32,64,128};
+ * d_model, n_heads*head_dim, d_ff multiples of 128; n_heads % n_kv_heads == 0. */
+typedef struct {
+    int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
+    float rms_eps;
+    double rope_base;
+    int32_t eos_id; /* -1: no EOS (rounds end at max_new_tokens) */
+    cvy_dtype dtype; /* weights, activations at GEMM inputs, and KV cache */
+} cvy_model_config;
+
+enum {
+    CVY_ENGINE_NO_GRAPH = 1,     /* launch kernels directly instead of a CUDA graph          */
+    CVY_ENGINE_DEBUG_LOGITS = 2, /* keep the last step's fp32 logits for cvy_debug_logits   */
+    CVY_ENGINE_SCAN_OFF = 4,     /* trigger scan disabled for every slot (overhead A/B)      */
+    CVY_ENGINE_NO_PDL = 8        /* no programmatic dependent launch between kernels        */
+};
+
+typedef struct {
+    uint32_t max_slots;          /* max in-flight requests, 1..1024                         */
+    uint32_t n_pages;            /* pages in the KV pool (16 tokens each)                  */
+    uint32_t max_pages_per_slot; /* page-table width: max context = 16 * this              */
+    uint32_t ring_records;       /* segment ring capacity (power of two, >= 32*max_slots)  */
+    uint32_t round_bytes;        /* per-slot byte-log capacity per round                   */
+    uint32_t round_tokens;       /* per-slot generated-token log capacity per round        */
+    uint32_t input_cap;          /* per-slot forced-input (prompt/observation) capacity    */
+    uint32_t forced_cap;         /* per-slot teacher-forcing capacity per round            */
+    int32_t device;              /* CUDA device ordinal                                    */
+    uint32_t flags;              /* CVY_ENGINE_*                                           */
+} cvy_engine_config;
+
+/* Weights and KV pool: BORROWED device pointers, row-major, dtype = model dtype except
+ * the norm weights (fp32).  Layouts:
+ *   embed      [V][d]
+ *   lm_head    [V][d]
+ *   final_norm [d] fp32;  attn_norm, mlp_norm [L][d] fp32
+ *   wqkv       [L][(H + 2*Hkv)*hd][d]   rows: q heads, k heads, v heads
+ *   wo         [L][d][H*hd]
+ *   wgu        [L][2*d_ff][d]  gate/up interleaved in 64-row blocks: rows 128j..128j+63
+ *                              are gate rows 64j.., rows 128j+64..128j+127 up rows 64j..
+ *   wd         [L][d][d_ff]
+ *   kv_pool    [L][n_pages][2 (K,V)][Hkv][16][hd]  (written by the engine)            */
+typedef struct {
+    const void* embed;
+    const void* lm_head;
+    const float* final_norm;
+    const float* attn_norm;
+    const float* mlp_norm;
+    const void* wqkv;
+    const void* wo;
+    const void* wgu;
+    const void* wd;
+    void* kv_pool;
+} cvy_weights;
+
+typedef struct cvy_engine cvy_engine;
+
+/* Byte sizes of every weight buffer and of the KV pool for a config (host-only helper). */
+typedef struct {
+    size_t embed, lm_head, final_norm, attn_norm, mlp_norm, wqkv, wo, wgu, wd, kv_pool;
+} cvy_weight_sizes;
+cvy_status cvy_weight_sizes_for(const cvy_model_config* m, uint32_t n_pages, cvy_weight_sizes* out);
+
+/* Fill every weight buffer with the counter-hash random init of DESIGN.md "Input recipe"
+ * (uniform, std 0.02; norms 1.0) on the given device.  Synchronous.  Zeroes nothing else. */
+cvy_status cvy_init_synthetic_weights(const cvy_model_config* m, const cvy_weights* w,
+                                      uint64_t seed, int32_t device);
+
+/* Create / destroy.  vocab_bytes [V][16] and vocab_lens [V] give the byte string of every
+ * token id (<= 16 bytes; specials have length 0) and are copied. */
+cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config* e,
+                             const cvy_weights* w, const uint8_t* vocab_bytes,
+                             const uint8_t* vocab_lens, cvy_engine** out);
+void cvy_engine_destroy(cvy_engine* e);
+const char* cvy_last_error(void);
+int32_t cvy_abi_version(void);
+
+/* Tool registration (before the first submit).  LITERAL: 1..8 distinct delimiters of
+ * 1..8 bytes each.  JSON kinds take no delimiters.  max_segment_bytes 0 => 4096.
+ * Errors: E_DUP name clash, E_INVAL bad delimiters, E_STATE after the first submit,
+ * E_FULL more than 64 tools. */
+typedef struct {
+    const char* name;
+    cvy_parser_kind parser;
+    uint32_t n_delims;
+    const uint8_t* const* delims;
+    const uint32_t* delim_lens;
+    uint32_t max_segment_bytes;
+} cvy_tool_desc;
+cvy_status cvy_register_tool(cvy_engine* e, const cvy_tool_desc* t, int32_t* tool_id);
+
+/* A request: prompt tokens are fed as forced inputs (scan off); then up to max_new_tokens
+ * are generated (greedy argmax, lowest id on ties; "temperature to be 0").
+ * forced/forced_len: teacher forcing of the generated tokens of round 0 (parity/bench);
+ * when forced_len > 0 the round ends after forced_len tokens.  synth_prefix_len tokens of
+ * synthetic, already-RoPE'd KV (counter hash with synth_seed) precede the prompt.
+ * The engine assigns req_id.  E_FULL: no free slot or pages -- retry later. */
+typedef struct {
+    int32_t tool_id; /* -1: no tool; the scan is off for this request */
+    cvy_exec_mode mode;
+    const int32_t* prompt;
+    uint32_t prompt_len; /* >= 1 */
+    uint32_t synth_prefix_len;
+    uint64_t synth_seed;
+    uint32_t max_new_tokens;
+    const int32_t* forced;
+    uint32_t forced_len;
+    uint32_t reserve_tokens; /* extra KV tokens to reserve for later observation rounds */
+} cvy_request_desc;
+cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t* req_id);
+
+/* One decode step for all in-flight requests (one graph launch).  Non-blocking except
+ * that at most 2 steps are in flight and the ring must have worst-case space
+ * (max_slots * 17 records) -- otherwise it waits for the GPU / the poller.
+ * last_completed (optional) receives the stats of the most recently completed step. */
+typedef struct {
+    uint64_t step;
+    uint32_t n_active, n_generated, n_segments, n_finished;
+    float step_ms;
+} cvy_step_info;
+cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed);
+
+/* Wait until every launched step has completed. */
+cvy_status cvy_sync(cvy_engine* e);
+
+/* A completed partial-execution piece (or a round's FINAL tail) of one request.
+ * byte_offset/byte_len index the request's byte stream of that round; token_index is the
+ * 0-based index (within the round's generated tokens) of the token holding the segment's
+ * last byte (FINAL: the round's last token, CVY_NO_TOKEN if none). */
+typedef struct {
+    uint64_t req_id;
+    uint32_t round, seq;       /* seq: per request, from 0, no gaps, across rounds */
+    uint32_t step, token_index;
+    uint32_t byte_offset, byte_len;
+    uint16_t delim_id, flags;  /* delim_id: LITERAL index / JSON 0=',' 1=close / NONE  */
+    uint32_t slot;             /* engine slot that produced the record (diagnostic)   */
+} cvy_segment;
+
+/* Exactly one consumer thread.  Copies up to cap records (and their bytes, concatenated
+ * in record order, if bytes != NULL) and returns E_AGAIN when the ring is empty.
+ * A record is only returned if its bytes fit into bytes_cap. */
+cvy_status cvy_poll_segments(cvy_engine* e, cvy_segment* out, uint32_t cap, uint32_t* n,
+                             uint8_t* bytes, size_t bytes_cap, size_t* bytes_used);
+
+/* Start the next round of a request parked after FINAL: the round's last generated
+ * token followed by the observation tokens are fed as forced inputs (scan off), then
+ * round+1 generates (max_new_tokens; optional teacher forcing).  E_STATE if not parked. */
+cvy_status cvy_inject_observation(cvy_engine* e, uint64_t req_id, const int32_t* tokens,
+                                  uint32_t n, uint32_t max_new_tokens, const int32_t* forced,
+                                  uint32_t forced_len);
+
+/* Idempotent.  A running round ends with FINAL|CANCELLED at the next step. */
+cvy_status cvy_cancel_request(cvy_engine* e, uint64_t req_id);
+
+/* Frees the slot and its pages.  Only valid when the request is parked or cancelled. */
+cvy_status cvy_release_request(cvy_engine* e, uint64_t req_id);
+
+/* Generated token ids of the current/last round of a request (copied out). */
+cvy_status cvy_round_tokens(cvy_engine* e, uint64_t req_id, int32_t* out, uint32_t cap,
+                            uint32_t* n);
+
+/* Request state: 0 running, 1 parked (round finished), 2 cancelled, -1 unknown. */
+int32_t cvy_request_state(cvy_engine* e, uint64_t req_id);
+
+/* Parity only (requires CVY_ENGINE_DEBUG_LOGITS): last completed step's fp32 logits of
+ * the request's slot, [vocab]. */
+cvy_status cvy_debug_logits(cvy_engine* e, uint64_t req_id, float* out, uint32_t cap);
+
+/* Device-side timing of the engine's kernels for measurement: per-step CUDA-event time
+ * of the last step and the number of kernel launches per step. */
+typedef struct {
+    float last_step_ms;
+    uint32_t launches_per_step;
+    uint32_t slots_bucket; /* padded batch of the last launched step */
+} cvy_perf_info;
+cvy_status cvy_perf(cvy_engine* e, cvy_perf_info* out);
+
+/* Stream the engine launches on (cudaStream_t as void*), for external event timing. */
+void* cvy_stream(cvy_engine* e);
+
+/* Multi-GPU stats gather (NCCL all-gather over NVLink/NVSwitch of a 64-byte per-engine
+ * stats record; one engine per GPU, all owned by this process). out: [n][8] uint64. */
+cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n, uint64_t* out);
+
+/* Test / measurement hook: Y[b][n] = sum_k W[n][k] X[b][k] for b < B through the same
+ * tcgen05 stream-K GEMM kernel the decode step uses (bf16 W [N][K], X [B][K] device
+ * pointers, fp32 Y [B][N] device pointer; K % 64 == 0, B <= 512).  iters > 1 repeats the
+ * launch and returns the mean device time per launch in *ms (CUDA events). */
+cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int32_t N, int32_t K, int32_t B,
+                          int32_t iters, int32_t device, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONVEYOR_H */

@@ -1,0 +1,1327 @@
+// engine.cu -- host engine of libconveyor: device buffers, slot table, page allocator,
+// pinned segment ring, step-graph cache per batch bucket, and the C ABI of conveyor.h.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/conveyor.h"
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "gemm_sm100.cuh"
+#include "kernels.cuh"
+#include "step_params.h"
+
+using namespace cvy;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+cvy_status fail(cvy_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess) {                                                                \
+            return fail(CVY_E_CUDA, std::string(#expr ": ") + cudaGetErrorString(_e));          \
+        }                                                                                       \
+    } while (0)
+
+size_t dtype_size(cvy_dtype d) { return d == CVY_DTYPE_BF16 ? 2 : 4; }
+
+uint32_t pow2_at_least(uint32_t v) {
+    uint32_t p = 32;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2D bf16 tensor map: [rows][cols] row-major, box {64 cols, box_rows}, 128B swizzle.
+bool make_tmap(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
+               uint32_t box_rows) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t gdim[2] = {cols, rows};
+    cuuint64_t gstride[1] = {row_stride_elems * 2};
+    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estride,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+struct SlotHost {
+    bool used = false;
+    uint64_t req_id = 0;
+    int state = 3;  // 0 running, 1 parked (FINAL polled), 2 cancelled, 3 free
+    std::vector<int32_t> pages;
+    int32_t reserved = 0;  // KV positions reserved (pages * 16)
+    int32_t next_pos = 0;  // host's view of the position after the last fed/forced token
+    bool final_seen = false;
+    bool final_pending = false;  // round running (a FINAL will come)
+};
+
+struct Upload {
+    void* dst;
+    std::vector<uint8_t> data;
+};
+
+struct GemmPlan {
+    CUtensorMap tmW, tmX;
+    GemmTC g;
+    int grid;
+    size_t smem;
+    // SIMT path
+    const void* W;
+    const void* X;
+    int64_t w_row0;
+};
+
+struct Bucket {
+    int Bp = 0;
+    StepParams P;
+    int nsub = 2;
+    std::vector<GemmPlan> plans;  // per launch in order
+    cudaGraphExec_t graph = nullptr;
+    uint32_t launches = 0;
+};
+
+}  // namespace
+
+struct cvy_engine {
+    cvy_model_config m{};
+    cvy_engine_config c{};
+    cvy_weights w{};
+    int dev = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    bool dead = false;
+    bool bf16 = true;
+    int act_ld = 0;
+    // device buffers
+    SlotDev* d_slots = nullptr;
+    int32_t* d_page_table = nullptr;
+    int32_t* d_in_buf = nullptr;
+    int32_t* d_force_buf = nullptr;
+    float2* d_rope = nullptr;
+    int max_rope_pos = 0;
+    float* d_x = nullptr;
+    void* d_act = nullptr;
+    float* d_q = nullptr;
+    void* d_o = nullptr;
+    void* d_h = nullptr;
+    float* d_ssq = nullptr;
+    unsigned long long* d_am = nullptr;
+    float* d_dbg = nullptr;
+    int32_t* d_lm_done = nullptr;
+    float* d_attn_part = nullptr;
+    int attn_splits_max = 16;
+    uint8_t* d_vtab = nullptr;
+    uint8_t* d_vlen = nullptr;
+    ToolDev* d_tools = nullptr;
+    unsigned long long* d_ring_tail = nullptr;
+    unsigned long long* d_step = nullptr;
+    float* d_gemm_acc = nullptr;
+    int32_t* d_tile_cnt = nullptr;
+    Patch* d_patches = nullptr;
+    int max_patches = 0;
+    // pinned mapped host buffers
+    cvy_segment* h_ring = nullptr;
+    unsigned long long* h_ring_tail = nullptr;
+    uint8_t* h_byte_log = nullptr;
+    int32_t* h_tok_log = nullptr;
+    SlotStatus* h_status = nullptr;
+    StepStats* h_stats = nullptr;
+    void* dm_ring = nullptr;
+    void* dm_ring_tail = nullptr;
+    void* dm_byte_log = nullptr;
+    void* dm_tok_log = nullptr;
+    void* dm_status = nullptr;
+    void* dm_stats = nullptr;
+    // host state
+    std::mutex mu;
+    std::vector<Patch> pending;
+    std::vector<Upload> uploads;
+    std::vector<SlotHost> slots;
+    std::vector<int32_t> free_pages;
+    std::vector<ToolDev> tools;
+    std::vector<std::string> tool_names;
+    std::vector<uint32_t> tool_max_seg;
+    bool submitted_any = false;
+    uint64_t next_req = 1;
+    std::unordered_map<uint64_t, int> req_slot;
+    std::map<int, Bucket> buckets;
+    std::deque<std::pair<cudaEvent_t, cudaEvent_t>> inflight;  // (start, end)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
+    uint64_t steps_launched = 0;
+    uint64_t ring_head = 0;  // consumer position
+    float last_step_ms = 0.f;
+    int last_bucket = 0;
+    uint32_t last_launches = 0;
+    std::vector<uint8_t> vlen_host;
+};
+
+namespace {
+
+cvy_status check_cuda(cvy_engine* e, cudaError_t err, const char* what) {
+    if (err != cudaSuccess) {
+        e->dead = true;
+        return fail(CVY_E_CUDA, std::string(what) + ": " + cudaGetErrorString(err));
+    }
+    return CVY_OK;
+}
+
+bool model_ok(const cvy_model_config* m, std::string* why) {
+    if (!m) { *why = "null model config"; return false; }
+    if (m->n_layers < 0 || m->d_model <= 0 || m->n_heads <= 0 || m->n_kv_heads <= 0 || m->vocab <= 0 || m->d_ff <= 0) {
+        *why = "non-positive model dimension";
+        return false;
+    }
+    if (m->head_dim != 32 && m->head_dim != 64 && m->head_dim != 128) { *why = "head_dim must be 32, 64 or 128"; return false; }
+    if (m->d_model % 128 || (m->n_heads * m->head_dim) % 128 || m->d_ff % 64) { *why = "d_model, H*hd must be multiples of 128, d_ff of 64"; return false; }
+    if (m->n_heads % m->n_kv_heads || m->n_heads / m->n_kv_heads > kAttnMaxG) { *why = "n_heads / n_kv_heads must be an integer <= 8"; return false; }
+    if (m->dtype != CVY_DTYPE_BF16 && m->dtype != CVY_DTYPE_FP32) { *why = "bad dtype"; return false; }
+    if (m->dtype == CVY_DTYPE_FP32 && std::max(m->d_model, std::max(m->d_ff, m->n_heads * m->head_dim)) > 1024) {
+        *why = "fp32 parity path supports K <= 1024 only";
+        return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int32_t cvy_abi_version(void) { return CVY_ABI_VERSION; }
+const char* cvy_last_error(void) { return g_last_error.c_str(); }
+
+cvy_status cvy_weight_sizes_for(const cvy_model_config* m, uint32_t n_pages, cvy_weight_sizes* out) {
+    std::string why;
+    if (!model_ok(m, &why) || !out) return fail(CVY_E_INVAL, why.empty() ? "null output" : why);
+    const size_t es = dtype_size(m->dtype);
+    const size_t L = m->n_layers, d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim,
+                 dff = m->d_ff, V = m->vocab;
+    out->embed = V * d * es;
+    out->lm_head = V * d * es;
+    out->final_norm = d * 4;
+    out->attn_norm = L * d * 4;
+    out->mlp_norm = L * d * 4;
+    out->wqkv = L * (H + 2 * Hkv) * hd * d * es;
+    out->wo = L * d * H * hd * es;
+    out->wgu = L * 2 * dff * d * es;
+    out->wd = L * d * dff * es;
+    out->kv_pool = L * (size_t)n_pages * 2 * Hkv * kPageTokens * hd * es;
+    return CVY_OK;
+}
+
+cvy_status cvy_init_synthetic_weights(const cvy_model_config* m, const cvy_weights* w, uint64_t seed, int32_t device) {
+    std::string why;
+    if (!model_ok(m, &why) || !w) return fail(CVY_E_INVAL, why.empty() ? "null weights" : why);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CVY_E_CUDA, "no CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    const double a = 0.02 * std::sqrt(3.0);
+    const int64_t L = m->n_layers, d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim,
+                  dff = m->d_ff, V = m->vocab;
+    const bool bf = m->dtype == CVY_DTYPE_BF16;
+    const size_t es = dtype_size(m->dtype);
+    auto launch = [&](const void* dst, uint64_t tid, int64_t rows, int64_t cols, int inter, int which) {
+        dim3 grid(2048), block(256);
+        if (bf)
+            init_hash_kernel<__nv_bfloat16><<<grid, block>>>((__nv_bfloat16*)dst, seed, tid, rows, cols, a, inter, which);
+        else
+            init_hash_kernel<float><<<grid, block>>>((float*)dst, seed, tid, rows, cols, a, inter, which);
+    };
+    launch(w->embed, 0, V, d, 0, 0);
+    launch(w->lm_head, (uint64_t)(1 + 8 * L), V, d, 0, 0);
+    for (int64_t l = 0; l < L; ++l) {
+        const uint8_t* qkv = (const uint8_t*)w->wqkv + (size_t)l * (H + 2 * Hkv) * hd * d * es;
+        launch(qkv, 1 + 8 * l + 0, H * hd, d, 0, 0);
+        launch(qkv + (size_t)H * hd * d * es, 1 + 8 * l + 1, Hkv * hd, d, 0, 0);
+        launch(qkv + (size_t)(H + Hkv) * hd * d * es, 1 + 8 * l + 2, Hkv * hd, d, 0, 0);
+        launch((const uint8_t*)w->wo + (size_t)l * d * H * hd * es, 1 + 8 * l + 3, d, H * hd, 0, 0);
+        const uint8_t* gu = (const uint8_t*)w->wgu + (size_t)l * 2 * dff * d * es;
+        launch(gu, 1 + 8 * l + 4, dff, d, 1, 0);
+        launch(gu, 1 + 8 * l + 5, dff, d, 1, 1);
+        launch((const uint8_t*)w->wd + (size_t)l * d * dff * es, 1 + 8 * l + 6, d, dff, 0, 0);
+    }
+    fill_f32_kernel<<<64, 256>>>((float*)w->final_norm, d, 1.f);
+    fill_f32_kernel<<<256, 256>>>((float*)w->attn_norm, L * d, 1.f);
+    fill_f32_kernel<<<256, 256>>>((float*)w->mlp_norm, L * d, 1.f);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    return CVY_OK;
+}
+
+void cvy_engine_destroy(cvy_engine* e);
+
+cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config* ec, const cvy_weights* w,
+                             const uint8_t* vocab_bytes, const uint8_t* vocab_lens, cvy_engine** out) {
+    std::string why;
+    if (!out) return fail(CVY_E_INVAL, "null out");
+    *out = nullptr;
+    if (!model_ok(m, &why)) return fail(CVY_E_INVAL, why);
+    if (!ec || !w || !vocab_bytes || !vocab_lens) return fail(CVY_E_INVAL, "null argument");
+    if (ec->max_slots < 1 || ec->max_slots > (uint32_t)kMaxSlots) return fail(CVY_E_INVAL, "max_slots out of range");
+    if (ec->ring_records < 32u * ec->max_slots || (ec->ring_records & (ec->ring_records - 1)))
+        return fail(CVY_E_INVAL, "ring_records must be a power of two >= 32*max_slots");
+    if (ec->n_pages < 1 || ec->max_pages_per_slot < 1 || ec->round_bytes < 16 || ec->round_tokens < 1 ||
+        ec->input_cap < 1 || ec->forced_cap < 1)
+        return fail(CVY_E_INVAL, "capacity fields must be positive");
+    if (!w->embed || !w->lm_head || !w->final_norm || !w->attn_norm || !w->mlp_norm || !w->wqkv || !w->wo || !w->wgu ||
+        !w->wd || !w->kv_pool)
+        return fail(CVY_E_INVAL, "null weight pointer");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CVY_E_CUDA, "no CUDA device");
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, ec->device));
+    if (prop.major != 10) return fail(CVY_E_CUDA, "libconveyor is built for sm_100a (B200) only");
+    CUDA_TRY(cudaSetDevice(ec->device));
+
+    cvy_engine* e = new cvy_engine();
+    e->m = *m;
+    e->c = *ec;
+    e->w = *w;
+    e->dev = ec->device;
+    e->num_sms = prop.multiProcessorCount;
+    e->bf16 = m->dtype == CVY_DTYPE_BF16;
+    const int Bmax = (int)((ec->max_slots + 15) / 16 * 16);
+    const int d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim, dff = m->d_ff, V = m->vocab;
+    e->act_ld = std::max(d, std::max(H * hd, dff));
+    const size_t es = dtype_size(m->dtype);
+    auto dmalloc = [&](void** p, size_t bytes) -> cvy_status {
+        if (cudaMalloc(p, bytes) != cudaSuccess) return fail(CVY_E_NOMEM, "cudaMalloc failed");
+        if (cudaMemset(*p, 0, bytes) != cudaSuccess) return fail(CVY_E_CUDA, "cudaMemset failed");
+        return CVY_OK;
+    };
+    auto hmalloc = [&](void** hp, void** dp, size_t bytes) -> cvy_status {
+        if (cudaHostAlloc(hp, bytes, cudaHostAllocMapped) != cudaSuccess) return fail(CVY_E_NOMEM, "cudaHostAlloc failed");
+        std::memset(*hp, 0, bytes);
+        if (cudaHostGetDevicePointer(dp, *hp, 0) != cudaSuccess) return fail(CVY_E_CUDA, "cudaHostGetDevicePointer");
+        return CVY_OK;
+    };
+    cvy_status st = CVY_OK;
+#define ALLOC(ptr, bytes)                                          \
+    if ((st = dmalloc((void**)&(ptr), (bytes))) != CVY_OK) {       \
+        cvy_engine_destroy(e);                                     \
+        return st;                                                 \
+    }
+#define HALLOC(hptr, dptr, bytes)                                               \
+    if ((st = hmalloc((void**)&(hptr), (void**)&(dptr), (bytes))) != CVY_OK) {  \
+        cvy_engine_destroy(e);                                                  \
+        return st;                                                              \
+    }
+    ALLOC(e->d_slots, sizeof(SlotDev) * Bmax);
+    ALLOC(e->d_page_table, sizeof(int32_t) * Bmax * ec->max_pages_per_slot);
+    ALLOC(e->d_in_buf, sizeof(int32_t) * (size_t)Bmax * ec->input_cap);
+    ALLOC(e->d_force_buf, sizeof(int32_t) * (size_t)Bmax * ec->forced_cap);
+    e->max_rope_pos = (int)(ec->max_pages_per_slot * kPageTokens);
+    ALLOC(e->d_rope, sizeof(float2) * (size_t)e->max_rope_pos * (hd / 2));
+    ALLOC(e->d_x, sizeof(float) * (size_t)Bmax * d);
+    ALLOC(e->d_act, es * (size_t)Bmax * e->act_ld);
+    ALLOC(e->d_q, sizeof(float) * (size_t)Bmax * H * hd);
+    ALLOC(e->d_o, es * (size_t)Bmax * e->act_ld);
+    ALLOC(e->d_h, es * (size_t)Bmax * e->act_ld);
+    ALLOC(e->d_ssq, sizeof(float) * (size_t)(d / 128) * Bmax);
+    ALLOC(e->d_am, sizeof(unsigned long long) * Bmax);
+    if (ec->flags & CVY_ENGINE_DEBUG_LOGITS) ALLOC(e->d_dbg, sizeof(float) * (size_t)Bmax * V);
+    ALLOC(e->d_lm_done, sizeof(int32_t) * 4);
+    const int G = H / Hkv;
+    ALLOC(e->d_attn_part, sizeof(float) * (size_t)Bmax * Hkv * e->attn_splits_max * G * (hd + 2));
+    ALLOC(e->d_vtab, (size_t)V * kMaxTokenBytes);
+    ALLOC(e->d_vlen, (size_t)V);
+    ALLOC(e->d_tools, sizeof(ToolDev) * kMaxTools);
+    ALLOC(e->d_ring_tail, sizeof(unsigned long long) * 2);
+    ALLOC(e->d_step, sizeof(unsigned long long) * 2);
+    // stream-K accumulator workspace: rows padded to 256 per GEMM, Bmax columns
+    const size_t max_rows = (size_t)std::max({(size_t)V, (size_t)2 * dff, (size_t)(H + 2 * Hkv) * hd, (size_t)d}) + 256;
+    ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * Bmax);
+    ALLOC(e->d_tile_cnt, sizeof(int32_t) * 4096);
+    e->max_patches = 4 * Bmax + 64;
+    ALLOC(e->d_patches, sizeof(Patch) * e->max_patches);
+    HALLOC(e->h_ring, e->dm_ring, sizeof(cvy_segment) * ec->ring_records);
+    HALLOC(e->h_ring_tail, e->dm_ring_tail, sizeof(unsigned long long) * 8);
+    HALLOC(e->h_byte_log, e->dm_byte_log, (size_t)Bmax * ec->round_bytes);
+    HALLOC(e->h_tok_log, e->dm_tok_log, sizeof(int32_t) * (size_t)Bmax * ec->round_tokens);
+    HALLOC(e->h_status, e->dm_status, sizeof(SlotStatus) * Bmax);
+    HALLOC(e->h_stats, e->dm_stats, sizeof(StepStats) * 16);
+#undef ALLOC
+#undef HALLOC
+    for (int b = 0; b < Bmax; ++b) e->h_status[b].state = 3;
+    // RoPE table (fp64 angles -> fp32 cos/sin), theta_i = base^(-2i/hd)
+    {
+        std::vector<float2> rope((size_t)e->max_rope_pos * (hd / 2));
+        for (int p = 0; p < e->max_rope_pos; ++p)
+            for (int i = 0; i < hd / 2; ++i) {
+                double th = std::pow(m->rope_base, -2.0 * i / hd);
+                double ang = (double)p * th;
+                rope[(size_t)p * (hd / 2) + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+            }
+        if (cudaMemcpy(e->d_rope, rope.data(), rope.size() * sizeof(float2), cudaMemcpyHostToDevice) != cudaSuccess) {
+            cvy_engine_destroy(e);
+            return fail(CVY_E_CUDA, "rope upload");
+        }
+    }
+    if (cudaMemcpy(e->d_vtab, vocab_bytes, (size_t)V * kMaxTokenBytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy(e->d_vlen, vocab_lens, (size_t)V, cudaMemcpyHostToDevice) != cudaSuccess) {
+        cvy_engine_destroy(e);
+        return fail(CVY_E_CUDA, "vocab upload");
+    }
+    e->vlen_host.assign(vocab_lens, vocab_lens + V);
+    for (int i = 0; i < V; ++i)
+        if (vocab_lens[i] > kMaxTokenBytes) {
+            cvy_engine_destroy(e);
+            return fail(CVY_E_INVAL, "vocab entry longer than 16 bytes");
+        }
+    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cvy_engine_destroy(e);
+        return fail(CVY_E_CUDA, "stream create");
+    }
+    e->slots.resize(Bmax);
+    for (int p = (int)ec->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
+    // kernel attributes
+    cudaFuncSetAttribute(gemm_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(gemm_simt_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(gemm_simt_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (cudaDeviceSynchronize() != cudaSuccess) {
+        cvy_engine_destroy(e);
+        return fail(CVY_E_CUDA, "init sync");
+    }
+    *out = e;
+    return CVY_OK;
+}
+
+void cvy_engine_destroy(cvy_engine* e) {
+    if (!e) return;
+    cudaSetDevice(e->dev);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    for (auto& kv : e->buckets)
+        if (kv.second.graph) cudaGraphExecDestroy(kv.second.graph);
+    for (auto& pr : e->inflight) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    for (auto& pr : e->event_pool) {
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
+    }
+    void* dptrs[] = {e->d_slots, e->d_page_table, e->d_in_buf, e->d_force_buf, e->d_rope, e->d_x, e->d_act, e->d_q,
+                     e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
+                     e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches};
+    for (void* p : dptrs)
+        if (p) cudaFree(p);
+    void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats};
+    for (void* p : hptrs)
+        if (p) cudaFreeHost(p);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+}
+
+cvy_status cvy_register_tool(cvy_engine* e, const cvy_tool_desc* t, int32_t* tool_id) {
+    if (!e || !t || !tool_id) return fail(CVY_E_INVAL, "null argument");
+    if (e->dead) return fail(CVY_E_CUDA, "engine is dead");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (e->submitted_any) return fail(CVY_E_STATE, "tools must be registered before the first submit");
+    std::string name = t->name ? t->name : "";
+    if (name.empty()) return fail(CVY_E_INVAL, "empty tool name");
+    for (auto& n : e->tool_names)
+        if (n == name) return fail(CVY_E_DUP, "duplicate tool name: " + name);
+    if ((int)e->tools.size() >= kMaxTools) return fail(CVY_E_FULL, "too many tools");
+    ToolDev td;
+    std::memset(&td, 0, sizeof(td));
+    td.kind = (int32_t)t->parser;
+    td.max_seg = t->max_segment_bytes ? (int32_t)t->max_segment_bytes : 4096;
+    if (t->parser == CVY_PARSER_LITERAL) {
+        if (t->n_delims < 1 || t->n_delims > 8 || !t->delims || !t->delim_lens)
+            return fail(CVY_E_INVAL, "LITERAL needs 1..8 delimiters");
+        for (uint32_t i = 0; i < t->n_delims; ++i) {
+            uint32_t L = t->delim_lens[i];
+            if (L < 1 || L > 8 || !t->delims[i]) return fail(CVY_E_INVAL, "delimiter length must be 1..8");
+            uint64_t pack = 0;
+            for (uint32_t j = 0; j < L; ++j) pack = (pack << 8) | t->delims[i][j];
+            for (uint32_t k = 0; k < i; ++k)
+                if ((uint32_t)td.dlen[k] == L && td.dpack[k] == pack) return fail(CVY_E_INVAL, "duplicate delimiter");
+            td.dpack[i] = pack;
+            td.dmask[i] = L == 8 ? ~0ULL : ((1ULL << (8 * L)) - 1);
+            td.dlen[i] = (int32_t)L;
+        }
+        td.n_delims = (int32_t)t->n_delims;
+    } else if (t->parser == CVY_PARSER_JSON_MEMBER || t->parser == CVY_PARSER_JSON_OBJECT) {
+        if (t->n_delims != 0) return fail(CVY_E_INVAL, "JSON parsers take no delimiters");
+    } else {
+        return fail(CVY_E_INVAL, "unknown parser kind");
+    }
+    int id = (int)e->tools.size();
+    if (cudaMemcpy(e->d_tools + id, &td, sizeof(td), cudaMemcpyHostToDevice) != cudaSuccess)
+        return check_cuda(e, cudaErrorUnknown, "tool upload");
+    e->tools.push_back(td);
+    e->tool_names.push_back(name);
+    *tool_id = id;
+    return CVY_OK;
+}
+
+static bool reserve_pages(cvy_engine* e, SlotHost& sh, int32_t tokens_needed, int slot, std::vector<Upload>& ups) {
+    int need_pages = (tokens_needed + kPageTokens - 1) / kPageTokens;
+    if (need_pages > (int)e->c.max_pages_per_slot) return false;
+    int have = (int)sh.pages.size();
+    if (need_pages <= have) return true;
+    if ((int)e->free_pages.size() < need_pages - have) return false;
+    std::vector<int32_t> added;
+    for (int i = have; i < need_pages; ++i) {
+        sh.pages.push_back(e->free_pages.back());
+        added.push_back(e->free_pages.back());
+        e->free_pages.pop_back();
+    }
+    Upload u;
+    u.dst = e->d_page_table + (size_t)slot * e->c.max_pages_per_slot + have;
+    u.data.resize(added.size() * sizeof(int32_t));
+    std::memcpy(u.data.data(), added.data(), u.data.size());
+    ups.push_back(std::move(u));
+    sh.reserved = (int32_t)sh.pages.size() * kPageTokens;
+    return true;
+}
+
+cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t* req_id) {
+    if (!e || !r || !req_id) return fail(CVY_E_INVAL, "null argument");
+    if (e->dead) return fail(CVY_E_CUDA, "engine is dead");
+    if (r->prompt_len < 1 || !r->prompt) return fail(CVY_E_INVAL, "prompt_len must be >= 1");
+    if (r->prompt_len - 1 > e->c.input_cap) return fail(CVY_E_INVAL, "prompt longer than input_cap + 1");
+    if (r->forced_len > e->c.forced_cap || (r->forced_len && !r->forced)) return fail(CVY_E_INVAL, "bad forced stream");
+    if (r->max_new_tokens < 1) return fail(CVY_E_INVAL, "max_new_tokens must be >= 1");
+    for (uint32_t i = 0; i < r->prompt_len; ++i)
+        if (r->prompt[i] < 0 || r->prompt[i] >= e->m.vocab) return fail(CVY_E_INVAL, "prompt token out of range");
+    for (uint32_t i = 0; i < r->forced_len; ++i)
+        if (r->forced[i] < 0 || r->forced[i] >= e->m.vocab) return fail(CVY_E_INVAL, "forced token out of range");
+    std::lock_guard<std::mutex> lk(e->mu);
+    if (r->tool_id < -1 || r->tool_id >= (int)e->tools.size()) return fail(CVY_E_NOTFOUND, "unknown tool id");
+    int slot = -1;
+    for (int b = 0; b < (int)e->c.max_slots; ++b)
+        if (!e->slots[b].used) {
+            slot = b;
+            break;
+        }
+    if (slot < 0) return fail(CVY_E_FULL, "no free slot");
+    SlotHost sh;
+    const uint32_t gen = r->forced_len ? std::min(r->forced_len, r->max_new_tokens) : r->max_new_tokens;
+    const int32_t need = (int32_t)(r->synth_prefix_len + r->prompt_len + gen + 1 + r->reserve_tokens);
+    std::vector<Upload> ups;
+    if (!reserve_pages(e, sh, need, slot, ups)) {
+        for (int32_t p : sh.pages) e->free_pages.push_back(p);
+        return fail(CVY_E_FULL, "not enough KV pages");
+    }
+    // synthetic prefix is written at submit time (synchronously on the engine stream)
+    if (r->synth_prefix_len) {
+        int32_t* d_pages = e->d_page_table + (size_t)slot * e->c.max_pages_per_slot;
+        for (auto& u : ups) cudaMemcpyAsync(u.dst, u.data.data(), u.data.size(), cudaMemcpyHostToDevice, e->stream);
+        ups.clear();
+        const int64_t n = (int64_t)e->m.n_layers * r->synth_prefix_len * 2 * e->m.n_kv_heads * e->m.head_dim;
+        const int blocks = (int)std::min<int64_t>(4096, (n + 255) / 256);
+        if (e->bf16)
+            synth_prefix_kernel<__nv_bfloat16><<<blocks, 256, 0, e->stream>>>(
+                (__nv_bfloat16*)e->w.kv_pool, d_pages, (int)e->c.n_pages, e->m.n_layers, e->m.n_kv_heads,
+                e->m.head_dim, (int)r->synth_prefix_len, r->synth_seed);
+        else
+            synth_prefix_kernel<float><<<blocks, 256, 0, e->stream>>>(
+                (float*)e->w.kv_pool, d_pages, (int)e->c.n_pages, e->m.n_layers, e->m.n_kv_heads, e->m.head_dim,
+                (int)r->synth_prefix_len, r->synth_seed);
+        cvy_status cs = check_cuda(e, cudaGetLastError(), "synth prefix");
+        if (cs != CVY_OK) return cs;
+    }
+    for (auto& u : ups) e->uploads.push_back(std::move(u));
+    if (r->prompt_len > 1) {
+        Upload u;
+        u.dst = e->d_in_buf + (size_t)slot * e->c.input_cap;
+        u.data.resize((r->prompt_len - 1) * sizeof(int32_t));
+        std::memcpy(u.data.data(), r->prompt + 1, u.data.size());
+        e->uploads.push_back(std::move(u));
+    }
+    if (r->forced_len) {
+        Upload u;
+        u.dst = e->d_force_buf + (size_t)slot * e->c.forced_cap;
+        u.data.resize(r->forced_len * sizeof(int32_t));
+        std::memcpy(u.data.data(), r->forced, u.data.size());
+        e->uploads.push_back(std::move(u));
+    }
+    Patch p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = PATCH_SUBMIT;
+    p.slot = slot;
+    p.req_id = e->next_req++;
+    p.tool = (e->c.flags & CVY_ENGINE_SCAN_OFF) ? -1 : r->tool_id;
+    p.pos = (int32_t)r->synth_prefix_len;
+    p.cur_tok = r->prompt[0];
+    p.in_idx = 0;
+    p.in_len = (int32_t)r->prompt_len - 1;
+    p.max_new = (int32_t)r->max_new_tokens;
+    p.force_len = (int32_t)r->forced_len;
+    p.max_pos = sh.reserved;
+    e->pending.push_back(p);
+    sh.used = true;
+    sh.req_id = p.req_id;
+    sh.state = 0;
+    sh.final_pending = true;
+    sh.next_pos = (int32_t)(r->synth_prefix_len + r->prompt_len + gen);
+    e->slots[slot] = std::move(sh);
+    e->req_slot[p.req_id] = slot;
+    e->submitted_any = true;
+    *req_id = p.req_id;
+    return CVY_OK;
+}
+
+cvy_status cvy_inject_observation(cvy_engine* e, uint64_t req_id, const int32_t* tokens, uint32_t n,
+                                  uint32_t max_new_tokens, const int32_t* forced, uint32_t forced_len) {
+    if (!e || (n && !tokens) || (forced_len && !forced)) return fail(CVY_E_INVAL, "null argument");
+    if (e->dead) return fail(CVY_E_CUDA, "engine is dead");
+    if (n > e->c.input_cap || forced_len > e->c.forced_cap) return fail(CVY_E_INVAL, "observation too long");
+    if (max_new_tokens < 1) return fail(CVY_E_INVAL, "max_new_tokens must be >= 1");
+    for (uint32_t i = 0; i < n; ++i)
+        if (tokens[i] < 0 || tokens[i] >= e->m.vocab) return fail(CVY_E_INVAL, "token out of range");
+    for (uint32_t i = 0; i < forced_len; ++i)
+        if (forced[i] < 0 || forced[i] >= e->m.vocab) return fail(CVY_E_INVAL, "forced token out of range");
+    std::lock_guard<std::mutex> lk(e->mu);
+    auto it = e->req_slot.find(req_id);
+    if (it == e->req_slot.end()) return fail(CVY_E_NOTFOUND, "unknown request");
+    const int slot = it->second;
+    SlotHost& sh = e->slots[slot];
+    if (sh.state != 1) return fail(CVY_E_STATE, "request is not parked after a polled FINAL");
+    const uint32_t gen = forced_len ? std::min(forced_len, max_new_tokens) : max_new_tokens;
+    std::vector<Upload> ups;
+    const int32_t need = sh.next_pos + 1 + (int32_t)n + (int32_t)gen + 1;
+    if (!reserve_pages(e, sh, need, slot, ups)) return fail(CVY_E_FULL, "not enough KV pages for the next round");
+    for (auto& u : ups) e->uploads.push_back(std::move(u));
+    if (n) {
+        Upload u;
+        u.dst = e->d_in_buf + (size_t)slot * e->c.input_cap;
+        u.data.resize(n * sizeof(int32_t));
+        std::memcpy(u.data.data(), tokens, u.data.size());
+        e->uploads.push_back(std::move(u));
+    }
+    if (forced_len) {
+        Upload u;
+        u.dst = e->d_force_buf + (size_t)slot * e->c.forced_cap;
+        u.data.resize(forced_len * sizeof(int32_t));
+        std::memcpy(u.data.data(), forced, u.data.size());
+        e->uploads.push_back(std::move(u));
+    }
+    Patch p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = PATCH_INJECT;
+    p.slot = slot;
+    p.req_id = req_id;
+    p.in_len = (int32_t)n;
+    p.max_new = (int32_t)max_new_tokens;
+    p.force_len = (int32_t)forced_len;
+    p.max_pos = sh.reserved;
+    e->pending.push_back(p);
+    sh.state = 0;
+    sh.final_seen = false;
+    sh.final_pending = true;
+    sh.next_pos = sh.next_pos + 1 + (int32_t)n + (int32_t)gen;
+    return CVY_OK;
+}
+
+cvy_status cvy_cancel_request(cvy_engine* e, uint64_t req_id) {
+    if (!e) return fail(CVY_E_INVAL, "null engine");
+    std::lock_guard<std::mutex> lk(e->mu);
+    auto it = e->req_slot.find(req_id);
+    if (it == e->req_slot.end()) return fail(CVY_E_NOTFOUND, "unknown request");
+    SlotHost& sh = e->slots[it->second];
+    if (sh.state != 0) return CVY_OK;  // idempotent: parked or already cancelled
+    Patch p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = PATCH_CANCEL;
+    p.slot = it->second;
+    p.req_id = req_id;
+    e->pending.push_back(p);
+    return CVY_OK;
+}
+
+cvy_status cvy_release_request(cvy_engine* e, uint64_t req_id) {
+    if (!e) return fail(CVY_E_INVAL, "null engine");
+    std::lock_guard<std::mutex> lk(e->mu);
+    auto it = e->req_slot.find(req_id);
+    if (it == e->req_slot.end()) return fail(CVY_E_NOTFOUND, "unknown request");
+    const int slot = it->second;
+    SlotHost& sh = e->slots[slot];
+    if (sh.state == 0) return fail(CVY_E_STATE, "request still running (cancel it or wait for FINAL)");
+    Patch p;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = PATCH_RELEASE;
+    p.slot = slot;
+    p.req_id = req_id;
+    e->pending.push_back(p);
+    for (int32_t pg : sh.pages) e->free_pages.push_back(pg);
+    e->req_slot.erase(it);
+    e->slots[slot] = SlotHost();
+    return CVY_OK;
+}
+
+int32_t cvy_request_state(cvy_engine* e, uint64_t req_id) {
+    if (!e) return -1;
+    std::lock_guard<std::mutex> lk(e->mu);
+    auto it = e->req_slot.find(req_id);
+    if (it == e->req_slot.end()) return -1;
+    return e->slots[it->second].state;
+}
+
+}  // extern "C"
+
+// ============================================================================ step graph
+namespace {
+
+cvy_status launch_k(cvy_engine* e, const void* func, dim3 grid, dim3 block, size_t smem, void** args, bool pdl) {
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = e->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL)) ? 1 : 0;
+    cudaError_t err = cudaLaunchKernelExC(&cfg, func, args);
+    if (err != cudaSuccess) return fail(CVY_E_CUDA, std::string("launch: ") + cudaGetErrorString(err));
+    return CVY_OK;
+}
+
+StepParams base_params(cvy_engine* e, int Bp) {
+    StepParams P;
+    std::memset(&P, 0, sizeof(P));
+    const cvy_model_config& m = e->m;
+    P.L = m.n_layers;
+    P.d = m.d_model;
+    P.H = m.n_heads;
+    P.Hkv = m.n_kv_heads;
+    P.hd = m.head_dim;
+    P.dff = m.d_ff;
+    P.V = m.vocab;
+    P.eos = m.eos_id;
+    P.eps = m.rms_eps;
+    P.Bp = Bp;
+    P.Bmax = (int)e->slots.size();
+    P.n_pages = (int)e->c.n_pages;
+    P.max_pages = (int)e->c.max_pages_per_slot;
+    P.act_ld = e->act_ld;
+    P.slots = e->d_slots;
+    P.page_table = e->d_page_table;
+    P.in_buf = e->d_in_buf;
+    P.input_cap = (int)e->c.input_cap;
+    P.force_buf = e->d_force_buf;
+    P.forced_cap = (int)e->c.forced_cap;
+    P.rope = e->d_rope;
+    P.max_rope_pos = e->max_rope_pos;
+    P.embed = e->w.embed;
+    P.attn_norm = e->w.attn_norm;
+    P.mlp_norm = e->w.mlp_norm;
+    P.final_norm = e->w.final_norm;
+    P.kv_pool = e->w.kv_pool;
+    P.x = e->d_x;
+    P.act = e->d_act;
+    P.q = e->d_q;
+    P.o = e->d_o;
+    P.h = e->d_h;
+    P.ssq = e->d_ssq;
+    P.am_keys = e->d_am;
+    P.dbg_logits = e->d_dbg;
+    P.lm_done = e->d_lm_done;
+    P.attn_part = e->d_attn_part;
+    const int want = (2 * e->num_sms + m.n_kv_heads * Bp - 1) / (m.n_kv_heads * Bp);
+    P.attn_splits = std::max(1, std::min(e->attn_splits_max, want));
+    P.vtab = e->d_vtab;
+    P.vlen = e->d_vlen;
+    P.tools = e->d_tools;
+    P.ring = e->dm_ring;
+    P.ring_mask = e->c.ring_records - 1;
+    P.ring_tail_dev = e->d_ring_tail;
+    P.ring_tail_host = reinterpret_cast<unsigned long long*>(e->dm_ring_tail);
+    P.byte_log = reinterpret_cast<uint8_t*>(e->dm_byte_log);
+    P.round_bytes = e->c.round_bytes;
+    P.tok_log = reinterpret_cast<int32_t*>(e->dm_tok_log);
+    P.round_tokens = e->c.round_tokens;
+    P.status = reinterpret_cast<SlotStatus*>(e->dm_status);
+    P.stats = reinterpret_cast<StepStats*>(e->dm_stats);
+    P.step_ctr = e->d_step;
+    P.scan_off = (e->c.flags & CVY_ENGINE_SCAN_OFF) ? 1 : 0;
+    return P;
+}
+
+// plan one GEMM: W rows N per layer, K, epilogue
+bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int layer, int L_rows_total, const void* X,
+               EpiArgs epi, GemmPlan* out, std::string* why) {
+    GemmPlan gp;
+    std::memset(&gp, 0, sizeof(gp));
+    const int Bp = bk.Bp;
+    gp.W = Wbase;
+    gp.X = X;
+    gp.w_row0 = (int64_t)layer * N;
+    GemmTC& g = gp.g;
+    g.N = N;
+    g.K = K;
+    g.epi = epi;
+    if (e->bf16) {
+        g.nsub = bk.nsub;
+        g.mma_n = std::min(Bp, 256);
+        g.nbh = Bp / g.mma_n;
+        g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
+        g.kblocks = K / 64;
+        g.acc_stages = (2 * g.nsub * Bp <= 512) ? 2 : 1;
+        if (g.nsub * Bp > 512) {
+            *why = "nsub*Bp exceeds TMEM";
+            return false;
+        }
+        g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * Bp));
+        g.w_row0 = layer * N;
+        g.acc = e->d_gemm_acc;
+        g.tile_cnt = e->d_tile_cnt;
+        const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp);
+        const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
+        const uint32_t budget = 232448;
+        int stages = (int)((budget - fixed) / stage);
+        stages = std::min(stages, 12);
+        if (stages < 2) {
+            *why = "not enough shared memory for 2 stages";
+            return false;
+        }
+        g.stages = stages;
+        gp.smem = (size_t)stages * stage + fixed;
+        const long long T = (long long)g.tiles * g.kblocks;
+        gp.grid = (int)std::min<long long>(e->num_sms, T);
+        if (!make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub))) {
+            *why = "cuTensorMapEncodeTiled (weights) failed";
+            return false;
+        }
+        if (!make_tmap(&gp.tmX, X, (uint64_t)e->slots.size(), (uint64_t)K, (uint64_t)e->act_ld, (uint32_t)g.mma_n)) {
+            *why = "cuTensorMapEncodeTiled (activations) failed";
+            return false;
+        }
+    } else {
+        g.nsub = (epi.kind == EPI_SWIGLU) ? 2 : 1;
+        g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
+        gp.grid = g.tiles;
+        gp.smem = (size_t)(128 * kEsmLd + Bp + 32 * K) * sizeof(float);
+    }
+    *out = gp;
+    return true;
+}
+
+cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
+    auto it = e->buckets.find(Bp);
+    if (it != e->buckets.end()) {
+        *out = &it->second;
+        return CVY_OK;
+    }
+    Bucket bk;
+    bk.Bp = Bp;
+    bk.nsub = Bp <= 128 ? 2 : 1;
+    bk.P = base_params(e, Bp);
+    const cvy_model_config& m = e->m;
+    const int L = m.n_layers, d = m.d_model, H = m.n_heads, Hkv = m.n_kv_heads, hd = m.head_dim, dff = m.d_ff,
+              V = m.vocab;
+    const int Nqkv = (H + 2 * Hkv) * hd;
+    std::string why;
+    for (int l = 0; l < L; ++l) {
+        GemmPlan gp;
+        EpiArgs eq{EPI_QKV, l, Nqkv, nullptr};
+        if (!plan_gemm(e, bk, e->w.wqkv, Nqkv, d, l, L * Nqkv, e->d_act, eq, &gp, &why)) return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+        EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d};
+        if (!plan_gemm(e, bk, e->w.wo, d, H * hd, l, L * d, e->d_o, eo, &gp, &why)) return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+        EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr};
+        if (!plan_gemm(e, bk, e->w.wgu, 2 * dff, d, l, L * 2 * dff, e->d_act, eg, &gp, &why)) return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+        EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm};
+        if (!plan_gemm(e, bk, e->w.wd, d, dff, l, L * d, e->d_h, ed, &gp, &why)) return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+    }
+    {
+        GemmPlan gp;
+        EpiArgs el{EPI_LMHEAD, 0, V, nullptr};
+        if (!plan_gemm(e, bk, e->w.lm_head, V, d, 0, V, e->d_act, el, &gp, &why)) return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+    }
+    auto res = e->buckets.emplace(Bp, std::move(bk));
+    *out = &res.first->second;
+    return CVY_OK;
+}
+
+cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
+    if (e->bf16) {
+        void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g};
+        return launch_k(e, (const void*)gemm_tc_kernel<__nv_bfloat16>, dim3(gp.grid), dim3(kGemmThreads), gp.smem, args,
+                        true);
+    }
+    const float* W = (const float*)gp.W;
+    const float* X = (const float*)gp.X;
+    int64_t w_row0 = gp.w_row0;
+    int K = gp.g.K, nsub = gp.g.nsub, tiles = gp.g.tiles;
+    EpiArgs E = gp.g.epi;
+    void* args[] = {&bk.P, &W, &w_row0, &X, &K, &nsub, &tiles, &E};
+    return launch_k(e, (const void*)gemm_simt_kernel<float>, dim3(gp.grid), dim3(128), gp.smem, args, true);
+}
+
+cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
+    cvy_status st;
+    uint32_t launches = 0;
+    const int Bp = bk.Bp;
+    const cvy_model_config& m = e->m;
+    {
+        void* args[] = {&bk.P};
+        const void* f = e->bf16 ? (const void*)embed_kernel<__nv_bfloat16> : (const void*)embed_kernel<float>;
+        if ((st = launch_k(e, f, dim3(Bp), dim3(128), 0, args, true)) != CVY_OK) return st;
+        launches++;
+    }
+    const int G = m.n_heads / m.n_kv_heads;
+    const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
+    size_t pi = 0;
+    for (int l = 0; l < m.n_layers; ++l) {
+        if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
+        int layer = l;
+        void* aargs[] = {&bk.P, &layer};
+        const void* af = e->bf16 ? (const void*)attention_kernel<__nv_bfloat16> : (const void*)attention_kernel<float>;
+        if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAttnThreads), attn_smem, aargs, true)) !=
+            CVY_OK)
+            return st;
+        launches += 2;
+        if (bk.P.attn_splits > 1) {
+            void* margs[] = {&bk.P};
+            const void* mf =
+                e->bf16 ? (const void*)attention_merge_kernel<__nv_bfloat16> : (const void*)attention_merge_kernel<float>;
+            if ((st = launch_k(e, mf, dim3(m.n_kv_heads, Bp), dim3(128), 0, margs, true)) != CVY_OK) return st;
+            launches++;
+        }
+        for (int k = 0; k < 3; ++k) {
+            if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
+            launches++;
+        }
+    }
+    if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
+    launches++;
+    bk.launches = launches;
+    return CVY_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
+    if (!e) return fail(CVY_E_INVAL, "null engine");
+    if (e->dead) return fail(CVY_E_CUDA, "engine is dead");
+    cudaSetDevice(e->dev);
+    std::vector<Patch> patches;
+    std::vector<Upload> uploads;
+    int max_used = -1;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        patches.swap(e->pending);
+        uploads.swap(e->uploads);
+        for (int b = 0; b < (int)e->slots.size(); ++b)
+            if (e->slots[b].used) max_used = b;
+    }
+    // released slots still need their patch applied even if nothing is in use
+    int Bp = std::max(16, (max_used + 1 + 15) / 16 * 16);
+    if (Bp > (int)e->slots.size()) Bp = (int)e->slots.size();
+    // at most 2 steps in flight
+    while (e->inflight.size() >= 2) {
+        auto ev = e->inflight.front();
+        cvy_status st = check_cuda(e, cudaEventSynchronize(ev.second), "event sync");
+        if (st != CVY_OK) return st;
+        cudaEventElapsedTime(&e->last_step_ms, ev.first, ev.second);
+        e->inflight.pop_front();
+        e->event_pool.push_back(ev);
+    }
+    // ring back-pressure: worst case records of the steps in flight + this one
+    {
+        const uint64_t worst = (uint64_t)(e->inflight.size() + 1) * Bp * kMaxRecPerSlot;
+        auto t0 = std::chrono::steady_clock::now();
+        while (true) {
+            uint64_t tail = __atomic_load_n(e->h_ring_tail, __ATOMIC_ACQUIRE);
+            uint64_t head = __atomic_load_n(&e->ring_head, __ATOMIC_ACQUIRE);
+            if (tail - head + worst <= e->c.ring_records) break;
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+                return fail(CVY_E_FULL, "segment ring full: poll_segments is not draining it");
+            std::this_thread::yield();
+        }
+    }
+    for (auto& u : uploads) {
+        cvy_status st = check_cuda(e, cudaMemcpyAsync(u.dst, u.data.data(), u.data.size(), cudaMemcpyHostToDevice, e->stream),
+                                   "upload");
+        if (st != CVY_OK) return st;
+    }
+    if (!patches.empty()) {
+        if ((int)patches.size() > e->max_patches) return fail(CVY_E_FULL, "too many pending patches");
+        cvy_status st = check_cuda(e,
+                                   cudaMemcpyAsync(e->d_patches, patches.data(), patches.size() * sizeof(Patch),
+                                                   cudaMemcpyHostToDevice, e->stream),
+                                   "patch upload");
+        if (st != CVY_OK) return st;
+        apply_patches_kernel<<<1, 1, 0, e->stream>>>(e->d_slots, e->d_patches, (int)patches.size(),
+                                                     reinterpret_cast<SlotStatus*>(e->dm_status));
+        st = check_cuda(e, cudaGetLastError(), "apply patches");
+        if (st != CVY_OK) return st;
+    }
+    Bucket* bk = nullptr;
+    cvy_status st = build_bucket(e, Bp, &bk);
+    if (st != CVY_OK) return st;
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    if (!e->event_pool.empty()) {
+        ev = e->event_pool.back();
+        e->event_pool.pop_back();
+    } else {
+        cudaEventCreate(&ev.first);
+        cudaEventCreate(&ev.second);
+    }
+    cudaEventRecord(ev.first, e->stream);
+    if (e->c.flags & CVY_ENGINE_NO_GRAPH) {
+        if ((st = enqueue_step_kernels(e, *bk)) != CVY_OK) {
+            e->dead = true;
+            return st;
+        }
+    } else {
+        if (!bk->graph) {
+            cudaGraph_t g;
+            st = check_cuda(e, cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+            if (st != CVY_OK) return st;
+            cvy_status st2 = enqueue_step_kernels(e, *bk);
+            cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+            if (st2 != CVY_OK) {
+                e->dead = true;
+                return st2;
+            }
+            if ((st = check_cuda(e, ce, "end capture")) != CVY_OK) return st;
+            if ((st = check_cuda(e, cudaGraphInstantiate(&bk->graph, g, 0), "graph instantiate")) != CVY_OK) return st;
+            cudaGraphDestroy(g);
+        }
+        if ((st = check_cuda(e, cudaGraphLaunch(bk->graph, e->stream), "graph launch")) != CVY_OK) return st;
+    }
+    cudaEventRecord(ev.second, e->stream);
+    if ((st = check_cuda(e, cudaGetLastError(), "step launch")) != CVY_OK) return st;
+    e->inflight.push_back(ev);
+    e->steps_launched++;
+    e->last_bucket = Bp;
+    e->last_launches = bk->launches;
+    if (last_completed) {
+        std::memset(last_completed, 0, sizeof(*last_completed));
+        const uint64_t done = e->steps_launched - e->inflight.size();
+        if (done > 0) {
+            StepStats ss = e->h_stats[(done - 1) & 15];
+            last_completed->step = ss.step;
+            last_completed->n_active = ss.n_active;
+            last_completed->n_generated = ss.n_generated;
+            last_completed->n_segments = ss.n_segments;
+            last_completed->n_finished = ss.n_finished;
+            last_completed->step_ms = e->last_step_ms;
+        }
+    }
+    return CVY_OK;
+}
+
+cvy_status cvy_sync(cvy_engine* e) {
+    if (!e) return fail(CVY_E_INVAL, "null engine");
+    if (e->dead) return fail(CVY_E_CUDA, "engine is dead");
+    cudaSetDevice(e->dev);
+    cvy_status st = check_cuda(e, cudaStreamSynchronize(e->stream), "stream sync");
+    if (st != CVY_OK) return st;
+    while (!e->inflight.empty()) {
+        auto ev = e->inflight.front();
+        cudaEventElapsedTime(&e->last_step_ms, ev.first, ev.second);
+        e->inflight.pop_front();
+        e->event_pool.push_back(ev);
+    }
+    return CVY_OK;
+}
+
+cvy_status cvy_poll_segments(cvy_engine* e, cvy_segment* out, uint32_t cap, uint32_t* n, uint8_t* bytes,
+                             size_t bytes_cap, size_t* bytes_used) {
+    if (!e || !out || !n) return fail(CVY_E_INVAL, "null argument");
+    *n = 0;
+    if (bytes_used) *bytes_used = 0;
+    const uint64_t tail = __atomic_load_n(e->h_ring_tail, __ATOMIC_ACQUIRE);
+    uint64_t head = e->ring_head;
+    if (tail == head) return CVY_E_AGAIN;
+    size_t used = 0;
+    uint32_t k = 0;
+    std::vector<std::pair<uint32_t, uint64_t>> finals;
+    while (head < tail && k < cap) {
+        const cvy_segment& r = e->h_ring[head & (e->c.ring_records - 1)];
+        cvy_segment rec;
+        std::memcpy(&rec, (const void*)&r, sizeof(rec));
+        if (bytes) {
+            if (used + rec.byte_len > bytes_cap) break;
+            const uint32_t off = std::min(rec.byte_offset, e->c.round_bytes);
+            const uint32_t len = std::min(rec.byte_len, e->c.round_bytes - off);
+            std::memcpy(bytes + used, e->h_byte_log + (size_t)rec.slot * e->c.round_bytes + off, len);
+            if (len < rec.byte_len) std::memset(bytes + used + len, 0, rec.byte_len - len);
+            used += rec.byte_len;
+        }
+        out[k++] = rec;
+        if (rec.flags & CVY_SEG_FINAL) finals.push_back({rec.slot, rec.req_id});
+        ++head;
+    }
+    __atomic_store_n(&e->ring_head, head, __ATOMIC_RELEASE);
+    *n = k;
+    if (bytes_used) *bytes_used = used;
+    if (!finals.empty()) {
+        std::lock_guard<std::mutex> lk(e->mu);
+        for (auto& f : finals) {
+            SlotHost& sh = e->slots[f.first];
+            if (sh.used && sh.req_id == f.second) {
+                sh.final_seen = true;
+                sh.final_pending = false;
+                const cvy_segment* last = nullptr;
+                for (uint32_t i = 0; i < k; ++i)
+                    if (out[i].req_id == f.second && (out[i].flags & CVY_SEG_FINAL)) last = &out[i];
+                sh.state = (last && (last->flags & CVY_SEG_CANCELLED)) ? 2 : 1;
+            }
+        }
+    }
+    return k ? CVY_OK : CVY_E_AGAIN;
+}
+
+cvy_status cvy_round_tokens(cvy_engine* e, uint64_t req_id, int32_t* out, uint32_t cap, uint32_t* n) {
+    if (!e || !out || !n) return fail(CVY_E_INVAL, "null argument");
+    int slot;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto it = e->req_slot.find(req_id);
+        if (it == e->req_slot.end()) return fail(CVY_E_NOTFOUND, "unknown request");
+        slot = it->second;
+    }
+    const uint32_t gen_raw = ((volatile SlotStatus*)e->h_status)[slot].gen;
+    const uint32_t gen = std::min(gen_raw, e->c.round_tokens);
+    const uint32_t m = std::min(gen, cap);
+    std::memcpy(out, e->h_tok_log + (size_t)slot * e->c.round_tokens, m * sizeof(int32_t));
+    *n = m;
+    return CVY_OK;
+}
+
+cvy_status cvy_debug_logits(cvy_engine* e, uint64_t req_id, float* out, uint32_t cap) {
+    if (!e || !out) return fail(CVY_E_INVAL, "null argument");
+    if (!e->d_dbg) return fail(CVY_E_STATE, "engine created without CVY_ENGINE_DEBUG_LOGITS");
+    if (cap < (uint32_t)e->m.vocab) return fail(CVY_E_INVAL, "cap < vocab");
+    int slot;
+    {
+        std::lock_guard<std::mutex> lk(e->mu);
+        auto it = e->req_slot.find(req_id);
+        if (it == e->req_slot.end()) return fail(CVY_E_NOTFOUND, "unknown request");
+        slot = it->second;
+    }
+    cvy_status st = cvy_sync(e);
+    if (st != CVY_OK) return st;
+    return check_cuda(e,
+                      cudaMemcpy(out, e->d_dbg + (size_t)slot * e->m.vocab, sizeof(float) * e->m.vocab,
+                                 cudaMemcpyDeviceToHost),
+                      "logits copy");
+}
+
+cvy_status cvy_perf(cvy_engine* e, cvy_perf_info* out) {
+    if (!e || !out) return fail(CVY_E_INVAL, "null argument");
+    out->last_step_ms = e->last_step_ms;
+    out->launches_per_step = e->last_launches;
+    out->slots_bucket = (uint32_t)e->last_bucket;
+    return CVY_OK;
+}
+
+void* cvy_stream(cvy_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+}  // extern "C"
+
+// ============================================================================ multi-GPU stats
+// One decode replica per GPU (requests shard across replicas); the
+// only GPU<->GPU traffic is this all-gather of a 64-byte per-engine stats record over
+// NVLink / NVSwitch, on a side stream so it never sits on the decode critical path.
+#include <nccl.h>
+
+namespace {
+struct StatsComm {
+    std::vector<int> devs;
+    std::vector<ncclComm_t> comms;
+    std::vector<cudaStream_t> streams;
+    std::vector<uint64_t*> bufs;  // [n][8] recv + [8] send per device
+};
+std::mutex g_stats_mu;
+StatsComm g_stats;
+}  // namespace
+
+extern "C" cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n, uint64_t* out) {
+    if (!engines || n < 1 || !out) return fail(CVY_E_INVAL, "bad arguments");
+    std::lock_guard<std::mutex> lk(g_stats_mu);
+    std::vector<int> devs(n);
+    for (int i = 0; i < n; ++i) {
+        if (!engines[i]) return fail(CVY_E_INVAL, "null engine");
+        devs[i] = engines[i]->dev;
+    }
+    if (g_stats.devs != devs) {
+        for (size_t i = 0; i < g_stats.comms.size(); ++i) {
+            ncclCommDestroy(g_stats.comms[i]);
+            cudaSetDevice(g_stats.devs[i]);
+            cudaStreamDestroy(g_stats.streams[i]);
+            cudaFree(g_stats.bufs[i]);
+        }
+        g_stats = StatsComm();
+        g_stats.devs = devs;
+        g_stats.comms.resize(n);
+        if (ncclCommInitAll(g_stats.comms.data(), n, devs.data()) != ncclSuccess) {
+            g_stats = StatsComm();
+            return fail(CVY_E_NCCL, "ncclCommInitAll failed");
+        }
+        for (int i = 0; i < n; ++i) {
+            cudaSetDevice(devs[i]);
+            cudaStream_t s;
+            cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+            g_stats.streams.push_back(s);
+            uint64_t* b = nullptr;
+            CUDA_TRY(cudaMalloc(&b, sizeof(uint64_t) * 8 * (n + 1)));
+            g_stats.bufs.push_back(b);
+        }
+    }
+    std::vector<std::vector<uint64_t>> send(n, std::vector<uint64_t>(8, 0));
+    for (int i = 0; i < n; ++i) {
+        cvy_engine* e = engines[i];
+        const uint64_t done = e->steps_launched - e->inflight.size();
+        StepStats ss{};
+        if (done > 0) ss = e->h_stats[(done - 1) & 15];
+        send[i][0] = ss.step;
+        send[i][1] = ss.n_active;
+        send[i][2] = ss.n_generated;
+        send[i][3] = ss.n_segments;
+        send[i][4] = ss.n_finished;
+        uint32_t ms_bits;
+        std::memcpy(&ms_bits, &e->last_step_ms, 4);
+        send[i][5] = ms_bits;
+        send[i][6] = (uint64_t)e->dev;
+        send[i][7] = e->steps_launched;
+        cudaSetDevice(devs[i]);
+        CUDA_TRY(cudaMemcpyAsync(g_stats.bufs[i] + 8 * n, send[i].data(), 64, cudaMemcpyHostToDevice, g_stats.streams[i]));
+    }
+    if (ncclGroupStart() != ncclSuccess) return fail(CVY_E_NCCL, "ncclGroupStart");
+    for (int i = 0; i < n; ++i) {
+        if (ncclAllGather(g_stats.bufs[i] + 8 * n, g_stats.bufs[i], 8, ncclUint64, g_stats.comms[i], g_stats.streams[i]) !=
+            ncclSuccess) {
+            ncclGroupEnd();
+            return fail(CVY_E_NCCL, "ncclAllGather");
+        }
+    }
+    if (ncclGroupEnd() != ncclSuccess) return fail(CVY_E_NCCL, "ncclGroupEnd");
+    cudaSetDevice(devs[0]);
+    CUDA_TRY(cudaMemcpyAsync(out, g_stats.bufs[0], sizeof(uint64_t) * 8 * n, cudaMemcpyDeviceToHost, g_stats.streams[0]));
+    for (int i = 0; i < n; ++i) {
+        cudaSetDevice(devs[i]);
+        CUDA_TRY(cudaStreamSynchronize(g_stats.streams[i]));
+    }
+    return CVY_OK;
+}
+
+// ============================================================================ test hook
+extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int32_t N, int32_t K, int32_t B,
+                                     int32_t iters, int32_t device, float* ms) {
+    if (!W || !X || !Y || N < 1 || K < 64 || K % 64 || B < 1 || B > 512 || iters < 1)
+        return fail(CVY_E_INVAL, "bad GEMM arguments");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CVY_E_CUDA, "no CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(CVY_E_CUDA, "sm_100a only");
+    cudaFuncSetAttribute(gemm_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    const int Bp = (B + 15) / 16 * 16;
+    const int Bp2 = Bp > 256 ? 512 : (Bp > 128 ? 256 : Bp);
+    StepParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.Bp = Bp2;
+    P.Bmax = Bp2;
+    P.act_ld = K;
+    GemmTC g;
+    std::memset(&g, 0, sizeof(g));
+    g.N = N;
+    g.K = K;
+    g.nsub = Bp2 <= 128 ? 2 : 1;
+    g.mma_n = std::min(Bp2, 256);
+    g.nbh = Bp2 / g.mma_n;
+    g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
+    g.kblocks = K / 64;
+    g.acc_stages = (2 * g.nsub * Bp2 <= 512) ? 2 : 1;
+    g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * Bp2));
+    g.w_row0 = 0;
+    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp2);
+    const uint32_t fixed = GemmSmem::fixed_bytes(Bp2) + 1024;
+    g.stages = std::min(12, (int)((232448 - fixed) / stage));
+    g.epi.kind = EPI_STORE;
+    g.epi.N = N;
+    g.epi.store_out = nullptr;
+    float* Ytmp = nullptr;
+    CUDA_TRY(cudaMalloc(&Ytmp, sizeof(float) * (size_t)Bp2 * N));
+    g.epi.store_out = Ytmp;
+    CUDA_TRY(cudaMalloc(&g.acc, sizeof(float) * (size_t)(g.tiles * g.nsub * 128) * Bp2));
+    CUDA_TRY(cudaMemset(g.acc, 0, sizeof(float) * (size_t)(g.tiles * g.nsub * 128) * Bp2));
+    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (g.tiles + 1)));
+    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (g.tiles + 1)));
+    // X padded to Bp2 rows with zeros
+    void* Xp = nullptr;
+    CUDA_TRY(cudaMalloc(&Xp, (size_t)Bp2 * K * 2));
+    CUDA_TRY(cudaMemset(Xp, 0, (size_t)Bp2 * K * 2));
+    CUDA_TRY(cudaMemcpy(Xp, X, (size_t)B * K * 2, cudaMemcpyDeviceToDevice));
+    CUtensorMap tmW, tmX;
+    if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub)) ||
+        !make_tmap(&tmX, Xp, (uint64_t)Bp2, (uint64_t)K, (uint64_t)K, (uint32_t)g.mma_n))
+        return fail(CVY_E_CUDA, "tensor map encode failed");
+    int sms = prop.multiProcessorCount;
+    const long long T = (long long)g.tiles * g.kblocks;
+    const int grid = (int)std::min<long long>(sms, T);
+    const size_t smem = (size_t)g.stages * stage + fixed;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    gemm_tc_kernel<__nv_bfloat16><<<grid, kGemmThreads, smem>>>(tmW, tmX, P, g);  // warm-up
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaEventRecord(e0);
+    for (int i = 0; i < iters; ++i) gemm_tc_kernel<__nv_bfloat16><<<grid, kGemmThreads, smem>>>(tmW, tmX, P, g);
+    cudaEventRecord(e1);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    if (ms) *ms = t / iters;
+    CUDA_TRY(cudaMemcpy2D(Y, sizeof(float) * N, Ytmp, sizeof(float) * N, sizeof(float) * N, B, cudaMemcpyDeviceToDevice));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(Ytmp);
+    cudaFree(g.acc);
+    cudaFree(g.tile_cnt);
+    cudaFree(Xp);
+    return CVY_OK;
+}

@@ -1,0 +1,204 @@
+"""Thin Python binding over libconveyor's C ABI (include/conveyor.h), same call names.
+
+PyTorch is used only for device memory (weights, KV pool) -- every step of the decode
+path (embedding, projections, attention, sampling, trigger scan, compaction, publish) runs
+in the library's sm_100a kernels.  No CPU fallback: without the library or a B200 the
+calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+from .capi import check
+
+
+def model_config(shape, dtype: str = "bf16") -> capi.ModelConfig:
+    return capi.ModelConfig(shape.L, shape.d, shape.H, shape.Hkv, shape.hd, shape.dff, shape.V,
+                            float(shape.eps), float(shape.rope_base), int(shape.eos),
+                            capi.DTYPE_BF16 if dtype == "bf16" else capi.DTYPE_FP32)
+
+
+class DeviceModel:
+    """Weights + KV pool as torch CUDA tensors (borrowed by the engine)."""
+
+    def __init__(self, shape, dtype: str, n_pages: int, seed: int, device: int = 0):
+        import torch
+        self.shape = shape
+        self.n_pages = n_pages
+        self.dtype = dtype
+        self.cfg = model_config(shape, dtype)
+        sizes = capi.WeightSizes()
+        check(capi.lib().cvy_weight_sizes_for(ctypes.byref(self.cfg), n_pages, ctypes.byref(sizes)))
+        dev = torch.device("cuda", device)
+        self.tensors = {}
+        for name, _ in capi.WeightSizes._fields_:
+            nbytes = getattr(sizes, name)
+            self.tensors[name] = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        self.tensors["kv_pool"].zero_()
+        self.w = capi.Weights(*[self.tensors[n].data_ptr() for n, _ in capi.Weights._fields_])
+        check(capi.lib().cvy_init_synthetic_weights(ctypes.byref(self.cfg), ctypes.byref(self.w), seed, device))
+
+    def tensor(self, name):
+        return self.tensors[name]
+
+
+@dataclass
+class Record:
+    req_id: int
+    round: int
+    seq: int
+    step: int
+    token_index: int
+    byte_offset: int
+    byte_len: int
+    delim_id: int
+    flags: int
+    slot: int
+    data: bytes
+
+
+class Engine:
+    def __init__(self, model: DeviceModel, vocab: list[bytes], max_slots: int = 64, n_pages: int | None = None,
+                 max_pages_per_slot: int = 256, ring_records: int | None = None, round_bytes: int = 1 << 16,
+                 round_tokens: int = 4096, input_cap: int = 4096, forced_cap: int = 4096, device: int = 0,
+                 flags: int = 0):
+        from inputs.vocab import table
+        self.model = model
+        self.V = model.shape.V
+        tb, ln = table(vocab)
+        if ring_records is None:
+            ring_records = 1
+            while ring_records < 64 * max_slots:
+                ring_records <<= 1
+        self.ecfg = capi.EngineConfig(max_slots, n_pages if n_pages is not None else model.n_pages, max_pages_per_slot,
+                                      ring_records, round_bytes, round_tokens, input_cap, forced_cap, device, flags)
+        h = ctypes.c_void_p()
+        check(capi.lib().cvy_engine_create(ctypes.byref(model.cfg), ctypes.byref(self.ecfg), ctypes.byref(model.w),
+                                           tb, ln, ctypes.byref(h)))
+        self.h = h
+        self._seg_buf = (capi.Segment * 4096)()
+        self._byte_buf = ctypes.create_string_buffer(1 << 22)
+
+    def close(self):
+        if getattr(self, "h", None):
+            capi.lib().cvy_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- the five calls of the paper's problem statement (+ lifecycle helpers)
+    def register_tool(self, name: str, parser: int, delims=(), max_segment_bytes: int = 0) -> int:
+        n = len(delims)
+        bufs = [(ctypes.c_uint8 * len(d)).from_buffer_copy(d) for d in delims]
+        arr = (ctypes.POINTER(ctypes.c_uint8) * max(n, 1))(*[ctypes.cast(b, ctypes.POINTER(ctypes.c_uint8)) for b in bufs])
+        lens = (ctypes.c_uint32 * max(n, 1))(*[len(d) for d in delims])
+        desc = capi.ToolDesc(name.encode(), parser, n, arr if n else None, lens if n else None, max_segment_bytes)
+        tid = ctypes.c_int32()
+        check(capi.lib().cvy_register_tool(self.h, ctypes.byref(desc), ctypes.byref(tid)))
+        return tid.value
+
+    def submit_request(self, prompt, max_new_tokens: int, tool_id: int = -1, mode: int = capi.MODE_PARTIAL,
+                       forced=None, synth_prefix_len: int = 0, synth_seed: int = 0, reserve_tokens: int = 0,
+                       allow_full: bool = False):
+        p = np.ascontiguousarray(np.asarray(prompt, dtype=np.int32))
+        f = np.ascontiguousarray(np.asarray(forced if forced is not None else [], dtype=np.int32))
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        desc = capi.RequestDesc(tool_id, mode, p.ctypes.data_as(i32p), len(p), synth_prefix_len, synth_seed,
+                                max_new_tokens, f.ctypes.data_as(i32p) if len(f) else None, len(f), reserve_tokens)
+        rid = ctypes.c_uint64()
+        st = capi.lib().cvy_submit_request(self.h, ctypes.byref(desc), ctypes.byref(rid))
+        if allow_full and st == capi.CVY_E_FULL:
+            return None
+        check(st)
+        return rid.value
+
+    def step(self) -> capi.StepInfo:
+        info = capi.StepInfo()
+        check(capi.lib().cvy_step(self.h, ctypes.byref(info)))
+        return info
+
+    def sync(self):
+        check(capi.lib().cvy_sync(self.h))
+
+    def poll_segments(self, with_bytes: bool = True) -> list[Record]:
+        out = []
+        while True:
+            n = ctypes.c_uint32()
+            used = ctypes.c_size_t()
+            st = capi.lib().cvy_poll_segments(self.h, self._seg_buf, len(self._seg_buf), ctypes.byref(n),
+                                              self._byte_buf if with_bytes else None,
+                                              len(self._byte_buf) if with_bytes else 0, ctypes.byref(used))
+            if st == capi.CVY_E_AGAIN:
+                return out
+            check(st)
+            raw = self._byte_buf.raw[:used.value] if with_bytes else b""
+            off = 0
+            for i in range(n.value):
+                s = self._seg_buf[i]
+                data = raw[off:off + s.byte_len] if with_bytes else b""
+                off += s.byte_len if with_bytes else 0
+                out.append(Record(s.req_id, s.round, s.seq, s.step, s.token_index, s.byte_offset, s.byte_len,
+                                  s.delim_id, s.flags, s.slot, data))
+            if n.value < len(self._seg_buf):
+                return out
+
+    def inject_observation(self, req_id: int, tokens, max_new_tokens: int, forced=None):
+        t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))
+        f = np.ascontiguousarray(np.asarray(forced if forced is not None else [], dtype=np.int32))
+        i32p = ctypes.POINTER(ctypes.c_int32)
+        check(capi.lib().cvy_inject_observation(self.h, req_id, t.ctypes.data_as(i32p) if len(t) else None, len(t),
+                                                max_new_tokens, f.ctypes.data_as(i32p) if len(f) else None, len(f)))
+
+    def cancel_request(self, req_id: int):
+        check(capi.lib().cvy_cancel_request(self.h, req_id))
+
+    def release_request(self, req_id: int):
+        check(capi.lib().cvy_release_request(self.h, req_id))
+
+    def request_state(self, req_id: int) -> int:
+        return capi.lib().cvy_request_state(self.h, req_id)
+
+    def round_tokens(self, req_id: int, cap: int = 1 << 16) -> list[int]:
+        buf = (ctypes.c_int32 * cap)()
+        n = ctypes.c_uint32()
+        check(capi.lib().cvy_round_tokens(self.h, req_id, buf, cap, ctypes.byref(n)))
+        return list(buf[:n.value])
+
+    def debug_logits(self, req_id: int) -> np.ndarray:
+        out = np.empty(self.V, dtype=np.float32)
+        check(capi.lib().cvy_debug_logits(self.h, req_id, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), self.V))
+        return out
+
+    def perf(self) -> capi.PerfInfo:
+        p = capi.PerfInfo()
+        check(capi.lib().cvy_perf(self.h, ctypes.byref(p)))
+        return p
+
+    def stream_ptr(self) -> int:
+        return capi.lib().cvy_stream(self.h) or 0
+
+
+def stats_allgather(engines: list[Engine]) -> np.ndarray:
+    arr = (ctypes.c_void_p * len(engines))(*[e.h.value for e in engines])
+    out = np.zeros((len(engines), 8), dtype=np.uint64)
+    check(capi.lib().cvy_stats_allgather(arr, len(engines), out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))))
+    return out
+
+
+def debug_gemm(W, X, N: int, K: int, B: int, iters: int = 1, device: int = 0):
+    """Y = X W^T through the decode step's tcgen05 GEMM kernel (test/measurement hook).
+    W, X: bf16 CUDA tensors; returns (Y fp32 CUDA tensor [B][N], mean ms per launch)."""
+    import torch
+    Y = torch.empty((B, N), dtype=torch.float32, device=W.device)
+    ms = ctypes.c_float()
+    check(capi.lib().cvy_debug_gemm(W.data_ptr(), X.data_ptr(), Y.data_ptr(), N, K, B, iters, device,
+                                    ctypes.byref(ms)))
+    return Y, ms.value

@@ -1,0 +1,282 @@
+"""GPU parity (B200, via gpurun): libconveyor's CUDA path vs the CPU oracle, through the C ABI.
+
+Tolerances (BASELINE.json north_star): logits max-abs 1e-4 on the fp32 path and 2e-2 on the
+bf16 path; trigger positions and segment records bit-exact under teacher forcing.
+"""
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from gpu_harness import (as_tuples, ensure_built, expected_records, free_running_parity, group_records,
+                         make_engine)
+from inputs.configs import MISTRAL_7B, TINY, slice_of
+from inputs.vocab import Tokenizer, byte_level_vocab, synthetic_vocab
+from inputs.workloads import SINE_SCRIPT_13, codegen_script, plan_stages, validation_call
+from paper_2406_00059_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+BYTE_VOCAB = byte_level_vocab()
+
+
+def tiny_prompts(n):
+    return [list(f"# task {i}\n".encode()) for i in range(n)]
+
+
+# ------------------------------------------------------------------ the GEMM kernel alone
+@pytest.mark.parametrize("N,K,B", [(256, 128, 4), (384, 192, 16), (6144, 4096, 64), (4096, 4096, 64),
+                                   (28672, 4096, 64), (4096, 14336, 64), (32000, 4096, 64),
+                                   (4096, 4096, 128), (4096, 4096, 200), (4096, 4096, 512), (1000, 640, 33)])
+def test_tc_gemm_matches_fp64(N, K, B):
+    import torch
+    from paper_2406_00059_b200.engine import debug_gemm
+    ensure_built()
+    g = torch.Generator(device="cuda").manual_seed(N * 7 + K * 3 + B)
+    W = (torch.rand((N, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    X = (torch.rand((B, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    Y, _ = debug_gemm(W, X, N, K, B)
+    ref = X.double() @ W.double().T
+    err = (Y.double() - ref).abs().max().item()
+    assert err < 1e-3 * (K ** 0.5), err
+
+
+# ------------------------------------------------------------------ tiny config, free running
+def test_tiny_fp32_free_running_logits_1e4():
+    d, gens = free_running_parity(TINY, "fp32", BYTE_VOCAB, tiny_prompts(4), max_new=64, seed=1000, tol=1e-4)
+    assert d < 1e-4 and all(len(g) == 64 for g in gens)
+
+
+def test_tiny_bf16_free_running_logits_2e2():
+    d, gens = free_running_parity(TINY, "bf16", BYTE_VOCAB, tiny_prompts(4), max_new=64, seed=1000, tol=2e-2)
+    assert d < 2e-2
+
+
+def test_tiny_bf16_no_graph_matches_graph():
+    a, ga = free_running_parity(TINY, "bf16", BYTE_VOCAB, tiny_prompts(3), 16, seed=1001, tol=2e-2, graph=False)
+    b, gb = free_running_parity(TINY, "bf16", BYTE_VOCAB, tiny_prompts(3), 16, seed=1001, tol=2e-2, graph=True)
+    assert ga == gb
+
+
+def test_tiny_fp32_with_synthetic_prefix():
+    d, _ = free_running_parity(TINY, "fp32", BYTE_VOCAB, tiny_prompts(3), max_new=8, seed=1002, tol=1e-4,
+                               prefix=37, synth_seeds=[1, 2, 3])
+    assert d < 1e-4
+
+
+# ------------------------------------------------------------------ 7B shape
+def test_7b_two_layer_slice_bf16():
+    shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
+    vocab = synthetic_vocab(32000)
+    prompts = [[1, 300, 5000], [1, 77], [1, 31999, 2000, 12]]
+    d, _ = free_running_parity(shape, "bf16", vocab, prompts, max_new=3, seed=1003, tol=2e-2, prefix=40,
+                               synth_seeds=[11, 12, 13])
+    assert d < 2e-2
+
+
+@pytest.mark.slow
+def test_7b_full_32_layers_bf16_b2():
+    vocab = synthetic_vocab(32000)
+    d, _ = free_running_parity(MISTRAL_7B, "bf16", vocab, [[1, 523], [1, 9000]], max_new=2, seed=1004, tol=2e-2,
+                               prefix=16, synth_seeds=[5, 6])
+    assert d < 2e-2
+
+
+def test_7b_width_large_batch_sampled():
+    """B=512 (validation-config batch) on a 1-layer 7B-width slice: every GEMM runs at Bp=512
+    (two UMMA N=256 halves); sampled requests are checked against the oracle one by one."""
+    shape = slice_of(MISTRAL_7B, L=1, name="7b-L1")
+    vocab = synthetic_vocab(32000)
+    B = 512
+    seed = 1005
+    dm, eng = make_engine(shape, "bf16", vocab, B, seed, max_pages_per_slot=8)
+    rng = random.Random(3)
+    prompts = [[1, rng.randrange(3, 32000)] for _ in range(B)]
+    rids = [eng.submit_request(p, 2, synth_prefix_len=20 + (i % 50), synth_seed=i) for i, p in enumerate(prompts)]
+    sample = [0, 1, 137, 255, 256, 300, 511]
+    w = oracle.Weights(shape, seed, bf16=True, act_bf16=True)
+    oreqs = {}
+    for i in sample:
+        r = oracle.Request(w, 100)
+        r.synth_prefix(20 + (i % 50), i)
+        oreqs[i] = r
+    eng.step()
+    eng.sync()
+    ora = oracle.step([oreqs[i] for i in sample], [prompts[i][0] for i in sample])
+    for j, i in enumerate(sample):
+        gl = eng.debug_logits(rids[i])
+        assert np.max(np.abs(gl - ora[j])) < 2e-2, i
+    eng.poll_segments()
+    eng.close()
+
+
+# ------------------------------------------------------------------ trigger scan: bit-exact
+def run_forced(eng, reqs, steps_cap=10000):
+    """reqs: list of (prompt, forced, tool_id, max_new).  Steps until every FINAL is polled."""
+    rids = [eng.submit_request(p, mx, tool_id=t, forced=f) for (p, f, t, mx) in reqs]
+    got = []
+    finals = set()
+    for _ in range(steps_cap):
+        eng.step()
+        for r in eng.poll_segments():
+            got.append(r)
+            if r.flags & capi.SEG_FINAL:
+                finals.add(r.req_id)
+        if len(finals) == len(rids):
+            break
+    eng.sync()
+    for r in eng.poll_segments():
+        got.append(r)
+    return rids, group_records(got)
+
+
+def test_tiny_teacher_forced_newline_segments_bitexact():
+    dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, 4, 1006)
+    tool = eng.register_tool("python", capi.PARSER_LITERAL, [b"\n"])
+    rng = random.Random(5)
+    forced = [list(codegen_script(rng, n_lines=8).encode())[:64] for _ in range(4)]
+    reqs = [(list(b"# task\n"), f, tool, 64) for f in forced]
+    rids, got = run_forced(eng, reqs)
+    for rid, f in zip(rids, forced):
+        assert as_tuples(got[rid]) == expected_records(f, BYTE_VOCAB, oracle.PARSER_LITERAL, [b"\n"])
+    eng.close()
+
+
+def test_vocab32k_all_parsers_bitexact_b64():
+    """Synthetic 32k vocab (delimiters inside multi-byte tokens), three tools, 64 requests:
+    code lines with '\\n' and ';' (+ a short max_segment for OVERFLOW), 4-stage JSON plans
+    (object completion), validation calls (member completion)."""
+    shape = slice_of(TINY, L=2, V=32000, name="tiny-v32k")
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    dm, eng = make_engine(shape, "bf16", vocab, 64, 1007, max_pages_per_slot=48)
+    t_code = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n", b";", b"):\n"])
+    t_short = eng.register_tool("interp-short", capi.PARSER_LITERAL, [b"\n"], max_segment_bytes=24)
+    t_plan = eng.register_tool("planner", capi.PARSER_JSON_OBJECT)
+    t_val = eng.register_tool("validator", capi.PARSER_JSON_MEMBER)
+    rng = random.Random(9)
+    reqs, meta = [], []
+    for i in range(64):
+        k = i % 4
+        if k == 0:
+            text, tool, kind, dl, ms = codegen_script(rng, 30), t_code, oracle.PARSER_LITERAL, [b"\n", b";", b"):\n"], 4096
+        elif k == 1:
+            text, tool, kind, dl, ms = codegen_script(rng, 20), t_short, oracle.PARSER_LITERAL, [b"\n"], 24
+        elif k == 2:
+            text, tool, kind, dl, ms = plan_stages(rng), t_plan, oracle.PARSER_JSON_OBJECT, [], 4096
+        else:
+            text, tool, kind, dl, ms = validation_call(rng, rng.random() < 0.5), t_val, oracle.PARSER_JSON_MEMBER, [], 4096
+        f = tok.encode(text)[:500]
+        reqs.append(([1, rng.randrange(3, 32000)], f, tool, 600))
+        meta.append((f, kind, dl, ms))
+    rids, got = run_forced(eng, reqs)
+    for rid, (f, kind, dl, ms) in zip(rids, meta):
+        assert as_tuples(got[rid]) == expected_records(f, vocab, kind, dl, ms), rid
+    eng.close()
+
+
+def test_eos_ends_round_and_multi_round_inject():
+    """EOS (id 2, no bytes) ends round 0; the observation is injected and round 1 generates;
+    records and seq continue across rounds; logits stay in tolerance across the boundary."""
+    shape = slice_of(TINY, L=2, V=32000, name="tiny-v32k")
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    dm, eng = make_engine(shape, "fp32", vocab, 2, 1008, max_pages_per_slot=32)
+    tool = eng.register_tool("search", capi.PARSER_LITERAL, [b"\n"])
+    f0 = tok.encode('search("hello world in Go")\nsearch("x")\n') + [2, 77, 78]
+    obs = tok.encode("\n[OBSERVATION search]\nresult text\n")
+    f1 = tok.encode("answer: done\n") + [2]
+    rid = eng.submit_request([1, 500], 100, tool_id=tool, forced=f0, reserve_tokens=64)
+    recs = []
+    for _ in range(200):
+        eng.step()
+        recs += eng.poll_segments()
+        if any(r.flags & capi.SEG_FINAL for r in recs):
+            break
+    n0 = f0.index(2) + 1
+    exp0 = expected_records(f0[:n0], vocab, oracle.PARSER_LITERAL, [b"\n"])
+    assert as_tuples(recs) == exp0
+    assert eng.request_state(rid) == 1
+    eng.inject_observation(rid, obs, 50, forced=f1)
+    recs1 = []
+    for _ in range(200):
+        eng.step()
+        recs1 += eng.poll_segments()
+        if any(r.flags & capi.SEG_FINAL for r in recs1):
+            break
+    exp1 = expected_records(f1, vocab, oracle.PARSER_LITERAL, [b"\n"], round_idx=1, seq_start=len(exp0))
+    assert as_tuples(recs1) == exp1
+    assert eng.round_tokens(rid) == f1
+    eng.release_request(rid)
+    eng.close()
+
+
+def test_cancel_emits_final_cancelled_with_tail():
+    dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, 2, 1009)
+    tool = eng.register_tool("validator", capi.PARSER_JSON_MEMBER)
+    rng = random.Random(2)
+    f = list(validation_call(rng, True).encode())
+    rid = eng.submit_request(list(b"{"), 1000, tool_id=tool, forced=f)
+    recs = []
+    for _ in range(40):
+        eng.step()
+        recs += eng.poll_segments()
+    eng.cancel_request(rid)
+    eng.cancel_request(rid)  # idempotent
+    for _ in range(5):
+        eng.step()
+    eng.sync()
+    recs += eng.poll_segments()
+    fin = [r for r in recs if r.flags & capi.SEG_FINAL]
+    assert len(fin) == 1 and fin[0].flags == capi.SEG_FINAL | capi.SEG_CANCELLED
+    n = fin[0].token_index + 1
+    assert as_tuples(recs) == expected_records(f[:n], BYTE_VOCAB, oracle.PARSER_JSON_MEMBER, [], cancelled=True)
+    assert eng.request_state(rid) == 2
+    eng.release_request(rid)
+    eng.close()
+
+
+def test_paper_13_line_script_13_segments_on_gpu():
+    dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, 1, 1010, max_pages_per_slot=32)
+    tool = eng.register_tool("python", capi.PARSER_LITERAL, [b"\n"])
+    f = list(SINE_SCRIPT_13.encode())
+    rids, got = run_forced(eng, [(list(b"```python\n"), f, tool, 1000)])
+    recs = got[rids[0]]
+    assert len(recs) == 14 and recs[-1].flags == capi.SEG_FINAL and recs[-1].byte_len == 0
+    assert b"".join(r.data for r in recs) == SINE_SCRIPT_13.encode()
+    eng.close()
+
+
+def test_submit_errors_and_full():
+    dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, 2, 1011, n_pages=8, max_pages_per_slot=4)
+    with pytest.raises(capi.CvyError) as ei:
+        eng.submit_request([], 4)
+    assert ei.value.status == capi.CVY_E_INVAL
+    with pytest.raises(capi.CvyError) as ei:
+        eng.submit_request([1], 4, tool_id=5)
+    assert ei.value.status == capi.CVY_E_NOTFOUND
+    a = eng.submit_request([1], 4)
+    b = eng.submit_request([1], 4)
+    assert eng.submit_request([1], 4, allow_full=True) is None
+    with pytest.raises(capi.CvyError) as ei:
+        eng.register_tool("late", capi.PARSER_JSON_OBJECT)
+    assert ei.value.status == capi.CVY_E_STATE
+    with pytest.raises(capi.CvyError) as ei:
+        eng.release_request(a)
+    assert ei.value.status == capi.CVY_E_STATE
+    eng.close()
+
+
+def test_tool_registration_errors():
+    dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, 1, 1012)
+    eng.register_tool("a", capi.PARSER_LITERAL, [b"\n"])
+    for args, status in [(("a", capi.PARSER_JSON_OBJECT, []), capi.CVY_E_DUP),
+                         (("b", capi.PARSER_LITERAL, []), capi.CVY_E_INVAL),
+                         (("c", capi.PARSER_LITERAL, [b"123456789"]), capi.CVY_E_INVAL),
+                         (("d", capi.PARSER_LITERAL, [b";", b";"]), capi.CVY_E_INVAL),
+                         (("e", capi.PARSER_JSON_MEMBER, [b","]), capi.CVY_E_INVAL)]:
+        with pytest.raises(capi.CvyError) as ei:
+            eng.register_tool(*args)
+        assert ei.value.status == status
+    eng.close()
