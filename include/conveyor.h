@@ -92,7 +92,7 @@ enum {
 };
 
 typedef struct {
-    uint32_t max_slots;          /* max in-flight requests, 1..1024                         */
+    uint32_t max_slots;          /* max in-flight requests, 1..512                          */
     uint32_t n_pages;            /* pages in the KV pool (16 tokens each)                  */
     uint32_t max_pages_per_slot; /* page-table width: max context = 16 * this              */
     uint32_t ring_records;       /* segment ring capacity (power of two, >= 32*max_slots)  */
@@ -256,6 +256,12 @@ void* cvy_stream(cvy_engine* e);
 /* Multi-GPU stats gather (NCCL all-gather over NVLink/NVSwitch of a 64-byte per-engine
  * stats record; one engine per GPU, all owned by this process). out: [n][8] uint64. */
 cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n, uint64_t* out);
+
+/* Test hook: copy an internal device buffer of the last completed step to host memory.
+ * which: 0 x (fp32 [Bmax][d]), 1 act, 2 q (fp32 [Bmax][H*hd]), 3 o, 4 h (model dtype
+ * [Bmax][act_ld]), 5 ssq (fp32 [d/128][Bmax]).  *bytes receives the buffer size; if dst is
+ * NULL only the size is returned. */
+cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap, size_t* bytes);
 
 /* Test / measurement hook: Y[b][n] = sum_k W[n][k] X[b][k] for b < B through the same
  * tcgen05 stream-K GEMM kernel the decode step uses (bf16 W [N][K], X [B][K] device

@@ -103,6 +103,7 @@ PROTOTYPES = {
     "cvy_perf": (c_i32, [c_vp, ctypes.POINTER(PerfInfo)]),
     "cvy_stream": (c_vp, [c_vp]),
     "cvy_stats_allgather": (c_i32, [ctypes.POINTER(c_vp), c_i32, ctypes.POINTER(c_u64)]),
+    "cvy_debug_buffer": (c_i32, [c_vp, c_i32, c_vp, c_sz, ctypes.POINTER(c_sz)]),
     "cvy_debug_gemm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f32)]),
 }
 

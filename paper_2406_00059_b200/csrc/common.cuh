@@ -16,10 +16,18 @@ template <typename T> struct DT;
 template <> struct DT<__nv_bfloat16> {
     static CVY_DEV float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
     static CVY_DEV __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+    // GEMM-input activations are carried as a (hi, lo) bf16 pair: hi = bf16(v),
+    // lo = bf16(v - hi), planes `plane` elements apart.
+    static CVY_DEV void store_act(__nv_bfloat16* p, size_t plane, float v) {
+        __nv_bfloat16 hi = __float2bfloat16_rn(v);
+        p[0] = hi;
+        p[plane] = __float2bfloat16_rn(v - __bfloat162float(hi));
+    }
 };
 template <> struct DT<float> {
     static CVY_DEV float to_f(float v) { return v; }
     static CVY_DEV float from_f(float v) { return v; }
+    static CVY_DEV void store_act(float* p, size_t, float v) { p[0] = v; }
 };
 
 CVY_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -128,6 +136,16 @@ CVY_DEV uint64_t sdesc_kmajor_sw128(uint32_t smem_addr) {
     d |= (uint64_t)(1024u >> 4) << 32;    // SBO
     d |= (uint64_t)1u << 46;              // version
     d |= (uint64_t)2u << 61;              // SWIZZLE_128B
+    return d;
+}
+// Same for rows of 64 bytes (BLOCK_K = 32 bf16): 64B swizzle, 8-row groups 512 B apart.
+CVY_DEV uint64_t sdesc_kmajor_sw64(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(1u) << 16;
+    d |= (uint64_t)(512u >> 4) << 32;
+    d |= (uint64_t)1u << 46;
+    d |= (uint64_t)4u << 61;              // SWIZZLE_64B
     return d;
 }
 // TMEM -> registers: 32 lanes x 32 consecutive fp32 columns; lane = thread's warp quarter.

@@ -64,17 +64,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-// 2D bf16 tensor map: [rows][cols] row-major, box {64 cols, box_rows}, 128B swizzle.
+// 2D bf16 tensor map: [rows][cols] row-major, box {box_cols, box_rows}; box_cols 64 -> 128B
+// swizzle, 32 -> 64B swizzle (matches the UMMA shared-memory descriptors).
 bool make_tmap(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_elems,
-               uint32_t box_rows) {
+               uint32_t box_rows, uint32_t box_cols = 64) {
     auto fn = get_encode_fn();
     if (!fn) return false;
     cuuint64_t gdim[2] = {cols, rows};
     cuuint64_t gstride[1] = {row_stride_elems * 2};
-    cuuint32_t box[2] = {64, box_rows};
+    cuuint32_t box[2] = {box_cols, box_rows};
     cuuint32_t estride[2] = {1, 1};
     CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride, box, estride,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -315,7 +318,9 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     e->dev = ec->device;
     e->num_sms = prop.multiProcessorCount;
     e->bf16 = m->dtype == CVY_DTYPE_BF16;
-    const int Bmax = (int)((ec->max_slots + 15) / 16 * 16);
+    int Bmax = (int)((ec->max_slots + 31) / 32 * 32);
+    if (Bmax > 256) Bmax = 512 * ((Bmax + 511) / 512);
+    else if (Bmax > 128) Bmax = 256;
     const int d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim, dff = m->d_ff, V = m->vocab;
     e->act_ld = std::max(d, std::max(H * hd, dff));
     const size_t es = dtype_size(m->dtype);
@@ -348,10 +353,11 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     e->max_rope_pos = (int)(ec->max_pages_per_slot * kPageTokens);
     ALLOC(e->d_rope, sizeof(float2) * (size_t)e->max_rope_pos * (hd / 2));
     ALLOC(e->d_x, sizeof(float) * (size_t)Bmax * d);
-    ALLOC(e->d_act, es * (size_t)Bmax * e->act_ld);
+    const size_t planes = e->bf16 ? 2 : 1;  // bf16: (hi, lo) activation pair
+    ALLOC(e->d_act, planes * es * (size_t)Bmax * e->act_ld);
     ALLOC(e->d_q, sizeof(float) * (size_t)Bmax * H * hd);
-    ALLOC(e->d_o, es * (size_t)Bmax * e->act_ld);
-    ALLOC(e->d_h, es * (size_t)Bmax * e->act_ld);
+    ALLOC(e->d_o, planes * es * (size_t)Bmax * e->act_ld);
+    ALLOC(e->d_h, planes * es * (size_t)Bmax * e->act_ld);
     ALLOC(e->d_ssq, sizeof(float) * (size_t)(d / 128) * Bmax);
     ALLOC(e->d_am, sizeof(unsigned long long) * Bmax);
     if (ec->flags & CVY_ENGINE_DEBUG_LOGITS) ALLOC(e->d_dbg, sizeof(float) * (size_t)Bmax * V);
@@ -734,6 +740,7 @@ StepParams base_params(cvy_engine* e, int Bp) {
     P.n_pages = (int)e->c.n_pages;
     P.max_pages = (int)e->c.max_pages_per_slot;
     P.act_ld = e->act_ld;
+    P.act_plane = e->bf16 ? (int64_t)e->slots.size() * e->act_ld : 0;
     P.slots = e->d_slots;
     P.page_table = e->d_page_table;
     P.in_buf = e->d_in_buf;
@@ -795,7 +802,8 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         g.mma_n = std::min(Bp, 256);
         g.nbh = Bp / g.mma_n;
         g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
-        g.kblocks = K / 64;
+        g.bk = Bp >= 512 ? 32 : 64;  // keep >= 2 stages with the (hi, lo) X tiles at Bp=512
+        g.kblocks = K / g.bk;
         g.acc_stages = (2 * g.nsub * Bp <= 512) ? 2 : 1;
         if (g.nsub * Bp > 512) {
             *why = "nsub*Bp exceeds TMEM";
@@ -805,7 +813,9 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         g.w_row0 = layer * N;
         g.acc = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
-        const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp);
+        g.xplanes = 2;
+        g.x_plane_rows = (int32_t)e->slots.size();
+        const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp, g.xplanes, g.bk);
         const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
         const uint32_t budget = 232448;
         int stages = (int)((budget - fixed) / stage);
@@ -818,11 +828,13 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         gp.smem = (size_t)stages * stage + fixed;
         const long long T = (long long)g.tiles * g.kblocks;
         gp.grid = (int)std::min<long long>(e->num_sms, T);
-        if (!make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub))) {
+        if (!make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub),
+                       (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (weights) failed";
             return false;
         }
-        if (!make_tmap(&gp.tmX, X, (uint64_t)e->slots.size(), (uint64_t)K, (uint64_t)e->act_ld, (uint32_t)g.mma_n)) {
+        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * e->slots.size()), (uint64_t)K, (uint64_t)e->act_ld, (uint32_t)g.mma_n,
+                       (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (activations) failed";
             return false;
         }
@@ -952,7 +964,10 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
             if (e->slots[b].used) max_used = b;
     }
     // released slots still need their patch applied even if nothing is in use
-    int Bp = std::max(16, (max_used + 1 + 15) / 16 * 16);
+    // batch bucket: multiple of 32 (epilogue chunk), 256 and 512 above 128/256
+    int Bp = std::max(32, (max_used + 1 + 31) / 32 * 32);
+    if (Bp > 256) Bp = 512;
+    else if (Bp > 128) Bp = 256;
     if (Bp > (int)e->slots.size()) Bp = (int)e->slots.size();
     // at most 2 steps in flight
     while (e->inflight.size() >= 2) {
@@ -965,7 +980,7 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
     }
     // ring back-pressure: worst case records of the steps in flight + this one
     {
-        const uint64_t worst = (uint64_t)(e->inflight.size() + 1) * Bp * kMaxRecPerSlot;
+        const uint64_t worst = (uint64_t)(e->inflight.size() + 1) * (uint64_t)(max_used + 1) * kMaxRecPerSlot;
         auto t0 = std::chrono::steady_clock::now();
         while (true) {
             uint64_t tail = __atomic_load_n(e->h_ring_tail, __ATOMIC_ACQUIRE);
@@ -1157,15 +1172,67 @@ cvy_status cvy_perf(cvy_engine* e, cvy_perf_info* out) {
 
 void* cvy_stream(cvy_engine* e) { return e ? (void*)e->stream : nullptr; }
 
+cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap, size_t* bytes) {
+    if (!e || !bytes) return fail(CVY_E_INVAL, "null argument");
+    const size_t B = e->slots.size(), es = dtype_size(e->m.dtype);
+    const void* src = nullptr;
+    size_t n = 0;
+    switch (which) {
+        case 0: src = e->d_x; n = B * e->m.d_model * 4; break;
+        case 1: src = e->d_act; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
+        case 2: src = e->d_q; n = B * e->m.n_heads * e->m.head_dim * 4; break;
+        case 3: src = e->d_o; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
+        case 4: src = e->d_h; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
+        case 5: src = e->d_ssq; n = (size_t)(e->m.d_model / 128) * B * 4; break;
+        default: return fail(CVY_E_INVAL, "unknown buffer");
+    }
+    *bytes = n;
+    if (!dst) return CVY_OK;
+    if (cap < n) return fail(CVY_E_INVAL, "buffer too small");
+    cvy_status st = cvy_sync(e);
+    if (st != CVY_OK) return st;
+    return check_cuda(e, cudaMemcpy(dst, src, n, cudaMemcpyDeviceToHost), "debug copy");
+}
+
 }  // extern "C"
 
 // ============================================================================ multi-GPU stats
 // One decode replica per GPU (requests shard across replicas); the
 // only GPU<->GPU traffic is this all-gather of a 64-byte per-engine stats record over
 // NVLink / NVSwitch, on a side stream so it never sits on the decode critical path.
+#include <dlfcn.h>
 #include <nccl.h>
 
 namespace {
+// NCCL is resolved lazily (dlopen at first use) so that loading libconveyor never pins an
+// NCCL build ahead of the one PyTorch ships (same soname, different versions).
+struct NcclApi {
+    decltype(&ncclCommInitAll) CommInitAll = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllGather) AllGather = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    bool ok = false;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW);
+        if (h) {
+            api.CommInitAll = (decltype(api.CommInitAll))dlsym(h, "ncclCommInitAll");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.ok = api.CommInitAll && api.CommDestroy && api.AllGather && api.GroupStart && api.GroupEnd;
+        }
+    }
+    return api;
+}
 struct StatsComm {
     std::vector<int> devs;
     std::vector<ncclComm_t> comms;
@@ -1179,6 +1246,8 @@ StatsComm g_stats;
 extern "C" cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n, uint64_t* out) {
     if (!engines || n < 1 || !out) return fail(CVY_E_INVAL, "bad arguments");
     std::lock_guard<std::mutex> lk(g_stats_mu);
+    NcclApi& N = nccl();
+    if (!N.ok) return fail(CVY_E_NCCL, "libnccl.so.2 not found");
     std::vector<int> devs(n);
     for (int i = 0; i < n; ++i) {
         if (!engines[i]) return fail(CVY_E_INVAL, "null engine");
@@ -1186,7 +1255,7 @@ extern "C" cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n,
     }
     if (g_stats.devs != devs) {
         for (size_t i = 0; i < g_stats.comms.size(); ++i) {
-            ncclCommDestroy(g_stats.comms[i]);
+            N.CommDestroy(g_stats.comms[i]);
             cudaSetDevice(g_stats.devs[i]);
             cudaStreamDestroy(g_stats.streams[i]);
             cudaFree(g_stats.bufs[i]);
@@ -1194,7 +1263,7 @@ extern "C" cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n,
         g_stats = StatsComm();
         g_stats.devs = devs;
         g_stats.comms.resize(n);
-        if (ncclCommInitAll(g_stats.comms.data(), n, devs.data()) != ncclSuccess) {
+        if (N.CommInitAll(g_stats.comms.data(), n, devs.data()) != ncclSuccess) {
             g_stats = StatsComm();
             return fail(CVY_E_NCCL, "ncclCommInitAll failed");
         }
@@ -1227,15 +1296,15 @@ extern "C" cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n,
         cudaSetDevice(devs[i]);
         CUDA_TRY(cudaMemcpyAsync(g_stats.bufs[i] + 8 * n, send[i].data(), 64, cudaMemcpyHostToDevice, g_stats.streams[i]));
     }
-    if (ncclGroupStart() != ncclSuccess) return fail(CVY_E_NCCL, "ncclGroupStart");
+    if (N.GroupStart() != ncclSuccess) return fail(CVY_E_NCCL, "ncclGroupStart");
     for (int i = 0; i < n; ++i) {
-        if (ncclAllGather(g_stats.bufs[i] + 8 * n, g_stats.bufs[i], 8, ncclUint64, g_stats.comms[i], g_stats.streams[i]) !=
+        if (N.AllGather(g_stats.bufs[i] + 8 * n, g_stats.bufs[i], 8, ncclUint64, g_stats.comms[i], g_stats.streams[i]) !=
             ncclSuccess) {
-            ncclGroupEnd();
+            N.GroupEnd();
             return fail(CVY_E_NCCL, "ncclAllGather");
         }
     }
-    if (ncclGroupEnd() != ncclSuccess) return fail(CVY_E_NCCL, "ncclGroupEnd");
+    if (N.GroupEnd() != ncclSuccess) return fail(CVY_E_NCCL, "ncclGroupEnd");
     cudaSetDevice(devs[0]);
     CUDA_TRY(cudaMemcpyAsync(out, g_stats.bufs[0], sizeof(uint64_t) * 8 * n, cudaMemcpyDeviceToHost, g_stats.streams[0]));
     for (int i = 0; i < n; ++i) {
@@ -1257,7 +1326,7 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10) return fail(CVY_E_CUDA, "sm_100a only");
     cudaFuncSetAttribute(gemm_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    const int Bp = (B + 15) / 16 * 16;
+    const int Bp = (B + 31) / 32 * 32;
     const int Bp2 = Bp > 256 ? 512 : (Bp > 128 ? 256 : Bp);
     StepParams P;
     std::memset(&P, 0, sizeof(P));
@@ -1272,11 +1341,14 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     g.mma_n = std::min(Bp2, 256);
     g.nbh = Bp2 / g.mma_n;
     g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
-    g.kblocks = K / 64;
+    g.bk = Bp2 >= 512 ? 32 : 64;
+    g.kblocks = K / g.bk;
     g.acc_stages = (2 * g.nsub * Bp2 <= 512) ? 2 : 1;
     g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * Bp2));
     g.w_row0 = 0;
-    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp2);
+    g.xplanes = 1;
+    g.x_plane_rows = 0;
+    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp2, 1, g.bk);
     const uint32_t fixed = GemmSmem::fixed_bytes(Bp2) + 1024;
     g.stages = std::min(12, (int)((232448 - fixed) / stage));
     g.epi.kind = EPI_STORE;
@@ -1295,8 +1367,8 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     CUDA_TRY(cudaMemset(Xp, 0, (size_t)Bp2 * K * 2));
     CUDA_TRY(cudaMemcpy(Xp, X, (size_t)B * K * 2, cudaMemcpyDeviceToDevice));
     CUtensorMap tmW, tmX;
-    if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub)) ||
-        !make_tmap(&tmX, Xp, (uint64_t)Bp2, (uint64_t)K, (uint64_t)K, (uint32_t)g.mma_n))
+    if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub), (uint32_t)g.bk) ||
+        !make_tmap(&tmX, Xp, (uint64_t)Bp2, (uint64_t)K, (uint64_t)K, (uint32_t)g.mma_n, (uint32_t)g.bk))
         return fail(CVY_E_CUDA, "tensor map encode failed");
     int sms = prop.multiProcessorCount;
     const long long T = (long long)g.tiles * g.kblocks;

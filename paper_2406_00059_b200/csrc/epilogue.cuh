@@ -89,7 +89,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                     size_t xi = (size_t)(cb + i) * P.d + n;
                     xn = P.x[xi] + v[i];
                     P.x[xi] = xn;
-                    act[(size_t)(cb + i) * P.act_ld + n] = DT<T>::from_f(xn * w);
+                    DT<T>::store_act(act + (size_t)(cb + i) * P.act_ld + n, (size_t)P.act_plane, xn * w);
                 }
                 esm[et * kEsmLd + i] = xn * xn;
             }
@@ -115,7 +115,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                         float g = esm[et * kEsmLd + i];
                         float u = esm[(et + 64) * kEsmLd + i];
                         float a = g / (1.f + __expf(-g)) * u;
-                        hb[(size_t)(cb + i) * P.act_ld + j] = DT<T>::from_f(a);
+                        DT<T>::store_act(hb + (size_t)(cb + i) * P.act_ld + j, (size_t)P.act_plane, a);
                     }
                 }
             }

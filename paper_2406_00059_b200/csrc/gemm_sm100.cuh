@@ -24,24 +24,27 @@ struct GemmTC {
     int32_t mma_n;      // UMMA N (<= 256)
     int32_t nbh;        // Bp / mma_n (1 or 2)
     int32_t tiles;
-    int32_t kblocks;    // K / 64
+    int32_t kblocks;    // K / bk
+    int32_t bk;         // K elements per pipeline stage: 64 (128B swizzle) or 32 (64B swizzle)
     int32_t stages;
     int32_t acc_stages; // TMEM accumulator buffers (1 or 2)
     uint32_t tmem_cols;
     int32_t w_row0;     // first row of this layer's matrix in the weight tensor map
+    int32_t xplanes;    // activation planes (2: hi/lo bf16 pair, both multiplied into D)
+    int32_t x_plane_rows;  // row offset of the lo plane in the activation tensor map
     float* acc;         // [tiles][nsub*128][Bp] zeroed fp32 workspace
     int32_t* tile_cnt;  // [tiles] arrival tickets (zeroed)
     EpiArgs epi;
 };
 
 constexpr int kGemmThreads = 192;
-constexpr int kBlockK = 64;  // 64 bf16 = 128 B rows (one 128B swizzle atom)
-
-// shared-memory carve-up (host and device agree)
+// shared-memory carve-up (host and device agree); rows are bk*2 bytes (one swizzle atom)
 struct GemmSmem {
-    __host__ __device__ static constexpr uint32_t w_bytes(int nsub) { return (uint32_t)nsub * 128u * 128u; }
-    __host__ __device__ static constexpr uint32_t x_bytes(int Bp) { return (uint32_t)Bp * 128u; }
-    __host__ __device__ static constexpr uint32_t stage_bytes(int nsub, int Bp) { return w_bytes(nsub) + x_bytes(Bp); }
+    __host__ __device__ static constexpr uint32_t w_bytes(int nsub, int bk) { return (uint32_t)nsub * 128u * bk * 2u; }
+    __host__ __device__ static constexpr uint32_t x_bytes(int Bp, int bk) { return (uint32_t)Bp * bk * 2u; }
+    __host__ __device__ static constexpr uint32_t stage_bytes(int nsub, int Bp, int planes, int bk) {
+        return w_bytes(nsub, bk) + (uint32_t)planes * x_bytes(Bp, bk);
+    }
     __host__ __device__ static constexpr uint32_t fixed_bytes(int Bp) {
         return 128u * kEsmLd * 4u      // esm
                + (uint32_t)Bp * 4u      // s_scale
@@ -63,7 +66,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                    const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t stage_bytes = GemmSmem::stage_bytes(G.nsub, P.Bp);
+    const uint32_t stage_bytes = GemmSmem::stage_bytes(G.nsub, P.Bp, G.xplanes, G.bk);
+    const uint32_t row_bytes = (uint32_t)G.bk * 2u;
     uint8_t* fixed = smem + (size_t)G.stages * stage_bytes;
     float* esm = reinterpret_cast<float*>(fixed);
     float* s_scale = esm + 128 * kEsmLd;
@@ -106,7 +110,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first();
             const uint64_t pol_x = policy_evict_last();
-            const uint32_t wb = GemmSmem::w_bytes(G.nsub);
+            const uint32_t wb = GemmSmem::w_bytes(G.nsub, G.bk);
             const int rows_per_tile = 128 * G.nsub;
             // prologue: weights do not depend on the previous kernel -> issue them before
             // the grid-dependency wait so the weight stream starts under the previous tail
@@ -117,15 +121,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
                 uint8_t* sw = smem + (size_t)i * stage_bytes;
                 mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
-                tma_load_2d(sw, &tmW, &full_bar[i], kb * kBlockK, G.w_row0 + tile * rows_per_tile, pol_w);
+                tma_load_2d(sw, &tmW, &full_bar[i], kb * G.bk, G.w_row0 + tile * rows_per_tile, pol_w);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i) {
                 const long long it = it0 + i;
                 const int kb = (int)(it % G.kblocks);
                 uint8_t* sx = smem + (size_t)i * stage_bytes + wb;
-                for (int h = 0; h < G.nbh; ++h)
-                    tma_load_2d(sx + (size_t)h * G.mma_n * 128, &tmX, &full_bar[i], kb * kBlockK, h * G.mma_n, pol_x);
+                for (int pl = 0; pl < G.xplanes; ++pl)
+                    for (int h = 0; h < G.nbh; ++h)
+                        tma_load_2d(sx + (size_t)(pl * P.Bp + h * G.mma_n) * row_bytes, &tmX, &full_bar[i], kb * G.bk,
+                                    pl * G.x_plane_rows + h * G.mma_n, pol_x);
             }
             int stage = pre % G.stages;
             uint32_t phase = (pre == G.stages) ? 1u : 0u;
@@ -134,10 +140,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
                 uint8_t* sw = smem + (size_t)stage * stage_bytes;
                 mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
-                tma_load_2d(sw, &tmW, &full_bar[stage], kb * kBlockK, G.w_row0 + tile * rows_per_tile, pol_w);
-                for (int h = 0; h < G.nbh; ++h)
-                    tma_load_2d(sw + wb + (size_t)h * G.mma_n * 128, &tmX, &full_bar[stage], kb * kBlockK, h * G.mma_n,
-                                pol_x);
+                tma_load_2d(sw, &tmW, &full_bar[stage], kb * G.bk, G.w_row0 + tile * rows_per_tile, pol_w);
+                for (int pl = 0; pl < G.xplanes; ++pl)
+                    for (int h = 0; h < G.nbh; ++h)
+                        tma_load_2d(sw + wb + (size_t)(pl * P.Bp + h * G.mma_n) * row_bytes, &tmX, &full_bar[stage],
+                                    kb * G.bk, pl * G.x_plane_rows + h * G.mma_n, pol_x);
                 if (++stage == G.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -147,7 +154,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     } else if (warp == 5) {
         // ===================== MMA issuer =====================
         const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)G.mma_n);
-        const uint32_t wb = GemmSmem::w_bytes(G.nsub);
+        const uint32_t wb = GemmSmem::w_bytes(G.nsub, G.bk);
+        const bool sw128 = G.bk == 64;
         int stage = 0;
         uint32_t phase = 0;
         int as = 0;
@@ -166,16 +174,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     const uint32_t sw = smem_u32(smem + (size_t)stage * stage_bytes);
                     const uint32_t sx = sw + wb;
                     const bool first = (it == (long long)tile * G.kblocks) || (it == it0);
-#pragma unroll
-                    for (int k = 0; k < kBlockK / 16; ++k) {
+                    for (int k = 0; k < G.bk / 16; ++k) {
                         for (int s = 0; s < G.nsub; ++s) {
-                            const uint64_t ad = sdesc_kmajor_sw128(sw + (uint32_t)s * 16384u + (uint32_t)k * 32u);
-                            for (int h = 0; h < G.nbh; ++h) {
-                                const uint64_t bd =
-                                    sdesc_kmajor_sw128(sx + (uint32_t)h * (uint32_t)G.mma_n * 128u + (uint32_t)k * 32u);
-                                umma_bf16(dcol + (uint32_t)(s * P.Bp + h * G.mma_n), ad, bd, idesc,
-                                          (first && k == 0) ? 0u : 1u);
-                            }
+                            const uint32_t aaddr = sw + (uint32_t)s * 128u * row_bytes + (uint32_t)k * 32u;
+                            const uint64_t ad = sw128 ? sdesc_kmajor_sw128(aaddr) : sdesc_kmajor_sw64(aaddr);
+                            for (int h = 0; h < G.nbh; ++h)
+                                for (int pl = 0; pl < G.xplanes; ++pl) {
+                                    const uint32_t baddr =
+                                        sx + (uint32_t)(pl * P.Bp + h * G.mma_n) * row_bytes + (uint32_t)k * 32u;
+                                    const uint64_t bd = sw128 ? sdesc_kmajor_sw128(baddr) : sdesc_kmajor_sw64(baddr);
+                                    umma_bf16(dcol + (uint32_t)(s * P.Bp + h * G.mma_n), ad, bd, idesc,
+                                              (first && k == 0 && pl == 0) ? 0u : 1u);
+                                }
                         }
                     }
                     umma_commit(&empty_bar[stage]);

@@ -125,12 +125,13 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Step
     const int tok = s.active ? s.cur_tok : 0;
     const T* E = reinterpret_cast<const T*>(P.embed) + (size_t)tok * P.d;
     T* act = reinterpret_cast<T*>(P.act) + (size_t)b * P.act_ld;
+    const float* nw = P.L > 0 ? P.attn_norm : P.final_norm;  // L == 0: straight to the LM head
     __shared__ float red[4];
     for (int blk = 0; blk < P.d / 128; ++blk) {
         const int i = blk * 128 + threadIdx.x;
         float v = DT<T>::to_f(E[i]);
         P.x[(size_t)b * P.d + i] = v;
-        act[i] = DT<T>::from_f(v * P.attn_norm[i]);
+        DT<T>::store_act(act + i, (size_t)P.act_plane, v * nw[i]);
         float sq = v * v;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
@@ -279,7 +280,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
             if (idx >= G * hd) break;
             const int j = idx / hd;
             float l = lrow[j];
-            o[idx] = DT<T>::from_f(l > 0.f ? acc[u] / l : 0.f);
+            DT<T>::store_act(o + idx, (size_t)P.act_plane, l > 0.f ? acc[u] / l : 0.f);
         }
     } else {
         float* part = P.attn_part + (((size_t)b * P.Hkv + g) * nsplit + split) * (size_t)(G * (hd + 2));
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(128) attention_merge_kernel(const __grid_const
             num += w * ps[idx];
             den += w * ps[G * hd + G + j];
         }
-        o[idx] = DT<T>::from_f(den > 0.f ? num / den : 0.f);
+        DT<T>::store_act(o + idx, (size_t)P.act_plane, den > 0.f ? num / den : 0.f);
     }
 }
 

@@ -10,7 +10,7 @@ constexpr int kPageTokens = 16;
 constexpr int kMaxTokenBytes = 16;
 constexpr int kMaxRecPerSlot = kMaxTokenBytes + 1;  // cuts of one token + FINAL
 constexpr int kMaxTools = 64;
-constexpr int kMaxSlots = 1024;
+constexpr int kMaxSlots = 512;
 
 // Per-slot device state (one continuous-batching slot = one in-flight request).
 struct SlotDev {
@@ -74,6 +74,7 @@ struct StepParams {
     int32_t Bmax;      // leading dimension of per-slot buffers
     int32_t n_pages, max_pages;
     int32_t act_ld;    // row stride (elements) of act / o / h buffers = max(d, H*hd, dff)
+    int64_t act_plane; // elements between the hi and lo planes of act / o / h (bf16 model)
     // state
     SlotDev* slots;
     const int32_t* page_table;  // [Bmax][max_pages]
@@ -91,10 +92,10 @@ struct StepParams {
     void* kv_pool;
     // activations
     float* x;                   // [Bmax][d] fp32 residual
-    void* act;                  // [Bmax][act_ld] model dtype: GEMM input after RMSNorm
+    void* act;                  // [planes][Bmax][act_ld] model dtype: GEMM input after RMSNorm
     float* q;                   // [Bmax][H*hd] fp32 (RoPE applied)
-    void* o;                    // [Bmax][act_ld] attention output
-    void* h;                    // [Bmax][act_ld] SwiGLU output
+    void* o;                    // [planes][Bmax][act_ld] attention output
+    void* h;                    // [planes][Bmax][act_ld] SwiGLU output
     float* ssq;                 // [d/128][Bmax] sum of squares per 128-wide block of x
     unsigned long long* am_keys;  // [Bmax] argmax keys
     float* dbg_logits;          // [Bmax][V] or null

@@ -177,6 +177,13 @@ class Engine:
         check(capi.lib().cvy_debug_logits(self.h, req_id, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), self.V))
         return out
 
+    def debug_buffer(self, which: int) -> bytes:
+        n = ctypes.c_size_t()
+        check(capi.lib().cvy_debug_buffer(self.h, which, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(n.value)
+        check(capi.lib().cvy_debug_buffer(self.h, which, buf, n.value, ctypes.byref(n)))
+        return buf.raw
+
     def perf(self) -> capi.PerfInfo:
         p = capi.PerfInfo()
         check(capi.lib().cvy_perf(self.h, ctypes.byref(p)))

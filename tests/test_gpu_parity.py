@@ -39,7 +39,7 @@ def test_tc_gemm_matches_fp64(N, K, B):
     Y, _ = debug_gemm(W, X, N, K, B)
     ref = X.double() @ W.double().T
     err = (Y.double() - ref).abs().max().item()
-    assert err < 1e-3 * (K ** 0.5), err
+    assert err < 1e-6 * K + 1e-5, err  # fp32 accumulation of exact bf16 products
 
 
 # ------------------------------------------------------------------ tiny config, free running
@@ -95,7 +95,7 @@ def test_7b_width_large_batch_sampled():
     prompts = [[1, rng.randrange(3, 32000)] for _ in range(B)]
     rids = [eng.submit_request(p, 2, synth_prefix_len=20 + (i % 50), synth_seed=i) for i, p in enumerate(prompts)]
     sample = [0, 1, 137, 255, 256, 300, 511]
-    w = oracle.Weights(shape, seed, bf16=True, act_bf16=True)
+    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
     oreqs = {}
     for i in sample:
         r = oracle.Request(w, 100)
@@ -178,8 +178,9 @@ def test_vocab32k_all_parsers_bitexact_b64():
 
 def test_eos_ends_round_and_multi_round_inject():
     """EOS (id 2, no bytes) ends round 0; the observation is injected and round 1 generates;
-    records and seq continue across rounds; logits stay in tolerance across the boundary."""
-    shape = slice_of(TINY, L=2, V=32000, name="tiny-v32k")
+    records and seq continue across rounds."""
+    import dataclasses
+    shape = dataclasses.replace(slice_of(TINY, L=2, V=32000, name="tiny-v32k-eos"), eos=2)
     vocab = synthetic_vocab(32000)
     tok = Tokenizer(vocab)
     dm, eng = make_engine(shape, "fp32", vocab, 2, 1008, max_pages_per_slot=32)
