@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py -- decode throughput of the Conveyor hot path on B200 (BASELINE.json metric).
+
+One "step" = one continuous-batching decode step of the whole hot path (SURVEY.md 8(a)
+S1-S13: embed, 32 x [QKV+RoPE+KV append, paged GQA attention, O+residual, gate/up+SwiGLU,
+down+residual], LM head + greedy sample + fused trigger scan + compaction + publish) for
+the N=1 workload of BASELINE.json configs[1] ("codegen"): Mistral-7B-shape random-init
+bf16, 64 in-flight requests per GPU, synthetic KV prefix 128 + U(0,400) tokens, teacher-
+forced ~400-token Python-script streams through the code-interpreter tool ('\\n').
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  `value` = generated tokens/s of the whole job with inputs
+resident in HBM (device time, CUDA events on the engine stream, max over ranks).  Inputs
+are larger than L2 (14.2 GB of weights streamed every step), so no L2 flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s/GPU + HBM roofline %; request latency, partial vs sequential tool exec"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+# ------------------------------------------------------------------ workload
+def codegen_workload(B: int, gen_tokens: int, seed: int = 2001):
+    """Per request: synthetic prefix length, synth seed, forced token stream (teacher forcing
+    of codegen scripts)."""
+    from inputs.vocab import Tokenizer, synthetic_vocab
+    from inputs.workloads import codegen_script
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    rng = random.Random(seed)
+    reqs = []
+    for b in range(B):
+        prefix = 128 + rng.randrange(0, 400)
+        ids = []
+        while len(ids) < gen_tokens:
+            ids += tok.encode(codegen_script(rng, 40))
+        reqs.append({"prefix": prefix, "seed": b, "forced": ids[:gen_tokens]})
+    return vocab, reqs
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def gemm_launch_bytes(shape, kind: int, B: int) -> int:
+    """Algorithmic HBM bytes of one projection GEMM launch: the bf16
+    weight matrix streamed once + the bf16 activation rows read + the rows written."""
+    d, H, Hkv, hd, dff, V = shape.d, shape.H, shape.Hkv, shape.hd, shape.dff, shape.V
+    if kind == 1:
+        N, K, out = (H + 2 * Hkv) * hd, d, B * (H * hd * 4 + 2 * Hkv * hd * 2)
+    elif kind == 4:
+        N, K, out = d, H * hd, B * d * (4 + 4 + 2)  # residual read+write fp32, next-norm input
+    elif kind == 5:
+        N, K, out = 2 * dff, d, B * dff * 2
+    elif kind == 6:
+        N, K, out = d, dff, B * d * (4 + 4 + 2)
+    else:
+        N, K, out = V, d, B * 8
+    return N * K * 2 + B * K * 2 + out
+
+
+def step_alg_bytes(shape, ctx_lens):
+    """Per step: weights streamed once + KV read (ctx incl. the new token) + KV written."""
+    kv_tok = shape.kv_bytes_per_token
+    return 2 * shape.n_params_streamed + sum(c + 1 for c in ctx_lens) * kv_tok + len(ctx_lens) * kv_tok
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def time_oracle(shape, reqs, budget_s: float, seed: int, n_req: int | None = None, max_steps: int | None = None):
+    """Run the CPU oracle (as it stands, weights regenerated from the counter hash every step,
+    no caching) on a bounded sample of the same workload: decode steps for a sample of the
+    requests (their synthetic prefixes, first input token).  The sample size is calibrated
+    so the total lands near budget_s.  Returns (tokens, seconds, threads, n_req, steps)."""
+    import oracle
+    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False, cache=False)
+
+    def one_step(sample):
+        ors = []
+        for r in sample:
+            o = oracle.Request(w, r["prefix"] + 4)
+            o.synth_prefix(r["prefix"], r["seed"])
+            ors.append(o)
+        t0 = time.perf_counter()
+        oracle.step(ors, [1] * len(sample))
+        return time.perf_counter() - t0
+
+    if n_req is None:
+        t1 = one_step(reqs[:1])
+        n_req = max(1, min(len(reqs), int(budget_s / 3 / max(t1, 1e-3))))
+    t_total, toks, steps, i = 0.0, 0, 0, 0
+    while True:
+        sample = [reqs[(i + j) % len(reqs)] for j in range(n_req)]
+        t_total += one_step(sample)
+        toks += n_req
+        steps += 1
+        i += n_req
+        if t_total >= budget_s or (max_steps and steps >= max_steps):
+            break
+    return toks, t_total, oracle.num_threads(), n_req, steps
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from inputs.configs import MISTRAL_7B
+    B = 64
+    _, reqs = codegen_workload(B, 8)
+    # calibrate: size each step (a sample of the 64 requests) to ~1 s of CPU work
+    _, t1, cores, _, _ = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=1, max_steps=1)
+    n = max(1, min(B, int(1.0 / max(t1, 1e-3))))
+    _, _, _, _, _ = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=n, max_steps=args.warmup)
+    total_tok, total_t, cores, _, _ = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=n, max_steps=args.steps)
+    value = total_tok / total_t
+    sample = f"{n} of the 64 codegen requests per step (1 decode step each, full 32 layers, their synthetic prefixes)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(B, None),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(B, ctx_mean):
+    return {"workload": "codegen (BASELINE.json configs[1]): Mistral-7B-shape random-init, "
+                        "teacher-forced Python-script streams, code-interpreter tool '\\n' (partial mode)",
+            "batch_per_gpu": B, "kv_prefix": "128+U(0,400) synthetic tokens", "ctx_mean": ctx_mean,
+            "l2": "no flush: inputs > L2 (14.2 GB weights + KV streamed per step)"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+
+    from inputs.configs import MISTRAL_7B
+    from paper_2406_00059_b200 import build, capi
+    from paper_2406_00059_b200.engine import DeviceModel, Engine
+    build.build()
+    shape = MISTRAL_7B
+    B = args.batch
+    W, K = args.warmup, args.steps
+    gen = W + K + 8
+    vocab, reqs = codegen_workload(B, gen)
+    max_ctx = max(r["prefix"] for r in reqs) + gen + 64
+    pages_per_slot = (max_ctx + 15) // 16 + 1
+    n_pages = B * pages_per_slot + 64
+    dm = DeviceModel(shape, "bf16", n_pages, seed=1001, device=local)
+    eng = Engine(dm, vocab, max_slots=B, max_pages_per_slot=pages_per_slot, device=local,
+                 flags=capi.ENGINE_SCAN_OFF if args.scan_off else 0)
+    tool = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n"])
+    rids = [eng.submit_request([1], gen, tool_id=tool, forced=r["forced"], synth_prefix_len=r["prefix"],
+                               synth_seed=r["seed"]) for r in reqs]
+
+    # a poller thread drains the pinned segment ring while decoding continues
+    stop = threading.Event()
+    nseg = [0]
+
+    def poller():
+        while not stop.is_set():
+            recs = eng.poll_segments(with_bytes=True)
+            nseg[0] += len(recs)
+            if not recs:
+                time.sleep(0.0002)
+
+    th = threading.Thread(target=poller, daemon=True)
+    th.start()
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=local)
+    for _ in range(W):
+        eng.step()
+    eng.sync()
+    ctx_start = [r["prefix"] + 1 + W for r in reqs]  # positions at the first timed step
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(K):
+        eng.step()
+    ev1.record(stream)
+    ev1.synchronize()
+    wall = time.perf_counter() - wall0
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    perf = eng.perf()
+    t = torch.tensor([dev_ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    max_ms = float(t.item())
+    value = world * B * K / (max_ms / 1000.0)
+    ctx_mean = float(np.mean([c + K / 2 for c in ctx_start]))
+
+    # per-kernel probe (timed graph variant: event pair per launch, no PDL): kernel shares
+    eng.set_kernel_timing(True)
+    for _ in range(3):
+        eng.step()
+    kt = eng.kernel_times()
+    eng.set_kernel_timing(False)
+    eng.sync()
+    probe_ctx = [c + K + 2 for c in ctx_start]
+    by_kind = {}
+    gemm_ms, gemm_bytes = 0.0, 0
+    for kind, layer, ms in kt:
+        by_kind.setdefault(capi.KERNEL_KINDS[kind], [0.0, 0])
+        by_kind[capi.KERNEL_KINDS[kind]][0] += ms
+        by_kind[capi.KERNEL_KINDS[kind]][1] += 1
+        if kind in (1, 4, 5, 6, 7):
+            gemm_ms += ms
+            gemm_bytes += gemm_launch_bytes(shape, kind, B)
+    probe_ms = sum(ms for _, _, ms in kt)
+    attn_ms = by_kind.get("attention", [0, 0])[0] + by_kind.get("attention_merge", [0, 0])[0]
+    kv_bytes = sum(c + 1 for c in probe_ctx) * shape.kv_bytes_per_token
+    peaks, peaks_src = load_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    achieved = gemm_bytes / (gemm_ms / 1000.0) / 1e9
+    roofline = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 stream-K projections, all 129 launches/step)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "peak_source": f"{peaks_src} HBM copy bandwidth", "traffic": load_traffic(),
+                "share_of_step": gemm_ms / probe_ms,
+                "attention": {"achieved": kv_bytes / (attn_ms / 1000.0) / 1e9, "frac": kv_bytes / (attn_ms / 1000.0) / 1e9 / hbm,
+                              "ms_per_step": attn_ms},
+                "kernels_ms_per_step": {k: round(v[0], 4) for k, v in by_kind.items()},
+                "probe_step_ms": probe_ms}
+    step_bytes = step_alg_bytes(shape, [c + K / 2 for c in ctx_start])
+    step_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (max_ms / K / 1000.0) / 1e9,
+                 "frac": step_bytes / (max_ms / K / 1000.0) / 1e9 / hbm}
+
+    # end-to-end through the C ABI with host buffers: release, then a fresh batch whose
+    # prompts and forced streams come from host memory; timed until every FINAL is polled and
+    # every request's generated tokens are read back to the host.
+    stop.set()
+    th.join()
+    eng.sync()
+    eng.poll_segments()
+    for rid in rids:
+        if eng.request_state(rid) == 0:
+            eng.cancel_request(rid)
+    for _ in range(3):
+        eng.step()
+    eng.sync()
+    eng.poll_segments()
+    for rid in rids:
+        eng.release_request(rid)
+    e2e = run_e2e(eng, reqs, tool, B)
+    eng.close()
+
+    stats = torch.tensor([value, max_ms], device="cuda", dtype=torch.float64)
+    if world > 1:
+        allst = [torch.zeros_like(stats) for _ in range(world)]
+        dist.all_gather(allst, stats)  # NCCL over NVLink: per-rank completion stats
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            toks, secs, cores, n, steps = time_oracle(shape, reqs, args.cpu_budget, 1001)
+            cpu = {"value": toks / secs, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                   "sample": f"{steps} decode step(s) x {n} of the 64 codegen requests (full 32 layers, their "
+                             f"synthetic prefixes), {secs:.1f} s of CPU work"}
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "bf16", "data": "synthetic", "config": workload_config(B, ctx_mean),
+                "tokens_per_s_per_gpu": value / world, "roofline": roofline, "step_roofline": step_roof,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(perf.launches_per_step) * K,
+                "clocks": clk, "wall_s_timed": wall, "segments_polled": nseg[0]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(eng, reqs, tool, B):
+    import numpy as np
+    G = 64
+    prompt_len = 16
+    rng = random.Random(77)
+    prompts = [[1] + [rng.randrange(259, 32000) for _ in range(prompt_len - 1)] for _ in range(B)]
+    t0 = time.perf_counter()
+    ids = [eng.submit_request(prompts[b], G, tool_id=tool, forced=reqs[b]["forced"][:G],
+                              synth_prefix_len=reqs[b]["prefix"], synth_seed=reqs[b]["seed"]) for b in range(B)]
+    finals, nrec, nbytes, steps = set(), 0, 0, 0
+    while len(finals) < B:
+        eng.step()
+        steps += 1
+        for r in eng.poll_segments():
+            nrec += 1
+            nbytes += r.byte_len
+            if r.flags & 1:
+                finals.add(r.req_id)
+        if steps > 10 * (G + prompt_len):
+            break
+    toks = [eng.round_tokens(i) for i in ids]
+    dt = time.perf_counter() - t0
+    ntok = sum(len(t) for t in toks)
+    for i in ids:
+        eng.release_request(i)
+    h2d = B * (prompt_len + G) * 4 + B * 64 * 4  # prompt + forced tokens + page-table entries
+    d2h = nrec * 40 + nbytes + ntok * 4
+    return {"value": ntok / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d / steps,
+            "d2h_bytes_per_step": d2h / steps, "steps": steps, "requests": B, "generated_per_request": G,
+            "prompt_tokens": prompt_len, "includes": "submit (host prompts + forced streams), prefill-as-decode, "
+                                                     "decode, segment polling, token read-back"}
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--scan-off", action="store_true", help="trigger scan disabled (overhead A/B)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

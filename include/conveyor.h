@@ -250,6 +250,19 @@ typedef struct {
 } cvy_perf_info;
 cvy_status cvy_perf(cvy_engine* e, cvy_perf_info* out);
 
+/* Per-kernel timing (measurement only).  When on, subsequent steps run a second graph
+ * variant with a CUDA event pair around every kernel launch (programmatic dependent
+ * launch disabled in that variant); cvy_kernel_times then returns the device time of each
+ * launch of the most recently completed timed step, in launch order.
+ * kind: 0 embed, 1 QKV GEMM, 2 attention, 3 attention merge, 4 O GEMM, 5 gate/up GEMM,
+ *       6 down GEMM, 7 LM-head GEMM + sampling/scan epilogue. */
+typedef struct {
+    int32_t kind, layer;
+    float ms;
+} cvy_kernel_time;
+cvy_status cvy_set_kernel_timing(cvy_engine* e, int32_t on);
+cvy_status cvy_kernel_times(cvy_engine* e, cvy_kernel_time* out, uint32_t cap, uint32_t* n);
+
 /* Stream the engine launches on (cudaStream_t as void*), for external event timing. */
 void* cvy_stream(cvy_engine* e);
 

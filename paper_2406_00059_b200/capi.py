@@ -72,6 +72,14 @@ class Segment(ctypes.Structure):
                 ("slot", c_u32)]
 
 
+class KernelTime(ctypes.Structure):
+    _fields_ = [("kind", c_i32), ("layer", c_i32), ("ms", c_f32)]
+
+
+KERNEL_KINDS = {0: "embed", 1: "gemm_qkv", 2: "attention", 3: "attention_merge", 4: "gemm_o", 5: "gemm_gate_up",
+                6: "gemm_down", 7: "gemm_lm_head+sample_scan"}
+
+
 class PerfInfo(ctypes.Structure):
     _fields_ = [("last_step_ms", c_f32), ("launches_per_step", c_u32), ("slots_bucket", c_u32)]
 
@@ -102,6 +110,8 @@ PROTOTYPES = {
     "cvy_debug_logits": (c_i32, [c_vp, c_u64, ctypes.POINTER(c_f32), c_u32]),
     "cvy_perf": (c_i32, [c_vp, ctypes.POINTER(PerfInfo)]),
     "cvy_stream": (c_vp, [c_vp]),
+    "cvy_set_kernel_timing": (c_i32, [c_vp, c_i32]),
+    "cvy_kernel_times": (c_i32, [c_vp, ctypes.POINTER(KernelTime), c_u32, ctypes.POINTER(c_u32)]),
     "cvy_stats_allgather": (c_i32, [ctypes.POINTER(c_vp), c_i32, ctypes.POINTER(c_u64)]),
     "cvy_debug_buffer": (c_i32, [c_vp, c_i32, c_vp, c_sz, ctypes.POINTER(c_sz)]),
     "cvy_debug_gemm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f32)]),

@@ -23,6 +23,7 @@
 #include "epilogue.cuh"
 #include "gemm_sm100.cuh"
 #include "kernels.cuh"
+#include "attention_tc.cuh"
 #include "step_params.h"
 
 using namespace cvy;
@@ -82,6 +83,62 @@ bool make_tmap(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
     return r == CUDA_SUCCESS;
 }
 
+// Tile/pipeline configuration of the tcgen05 GEMM for a padded batch Bp.
+//   Bp <= 128: 2 sub-tiles (256 weight rows) per tile, hi/lo planes merged (MMA N = 2*Bp)
+//   Bp 160..256: 1 sub-tile, planes as two MMAs into one accumulator (N = Bp)
+//   Bp 512: 1 sub-tile, 2 batch halves of N = 256, 32-element K stages (64B swizzle)
+bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why) {
+    g.N = N;
+    g.K = K;
+    g.merge = Bp <= 128;
+    g.bk = Bp >= 512 ? 32 : 64;
+    // 256-row tiles halve the activation (L2) traffic for the wide GEMMs; the narrow ones
+    // (N < 8192) use 128-row tiles to keep the stream-K partials small
+    g.nsub = (g.merge && N >= 8192) ? 2 : 1;
+    if (const char* ns = getenv("CVY_GEMM_NSUB")) g.nsub = std::max(1, std::min(2, atoi(ns)));
+    if (g.merge) {
+        g.mma_n = 2 * Bp;
+        g.nbh = 1;
+        g.cols_per_sub = 2 * Bp;
+    } else {
+        g.mma_n = std::min(Bp, 256);
+        g.nbh = Bp / g.mma_n;
+        g.cols_per_sub = Bp;
+    }
+    if (g.bk == 32) g.nsub = 1;
+    if (g.nsub * g.cols_per_sub > 512) {
+        *why = "accumulator exceeds TMEM";
+        return false;
+    }
+    g.acc_stages = (2 * g.nsub * g.cols_per_sub <= 512) ? 2 : 1;
+    g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * g.cols_per_sub));
+    g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
+    g.kblocks = K / g.bk;
+    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp, 2, g.bk);
+    const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
+    int stages = std::min(12, (int)((232448 - fixed) / stage));
+    if (stages < 2) {
+        *why = "not enough shared memory for 2 stages";
+        return false;
+    }
+    g.stages = stages;
+    *smem = (size_t)stages * stage + fixed;
+    const long long T = (long long)g.tiles * g.kblocks;
+    *grid = (int)std::min<long long>(num_sms, T);
+    return true;
+}
+
+void set_gemm_smem_attrs() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    for (int nsub = 1; nsub <= 2; ++nsub)
+        for (int merge = 0; merge <= 1; ++merge)
+            for (int bk : {32, 64})
+                cudaFuncSetAttribute(gemm_tc_kernel_ptr<__nv_bfloat16>(nsub, merge != 0, bk),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+}
+
 struct SlotHost {
     bool used = false;
     uint64_t req_id = 0;
@@ -115,6 +172,9 @@ struct Bucket {
     int nsub = 2;
     std::vector<GemmPlan> plans;  // per launch in order
     cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph_timed = nullptr;  // event pair around every kernel, no PDL
+    std::vector<cudaEvent_t> kev;
+    std::vector<std::pair<int, int>> kinfo;  // (kind, layer) per launch
     uint32_t launches = 0;
 };
 
@@ -191,6 +251,11 @@ struct cvy_engine {
     int last_bucket = 0;
     uint32_t last_launches = 0;
     std::vector<uint8_t> vlen_host;
+    bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
+    CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd]
+    bool timing = false;        // launch the timed graph variant
+    bool capturing_timed = false;
+    Bucket* last_timed = nullptr;
 };
 
 namespace {
@@ -369,10 +434,9 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     ALLOC(e->d_tools, sizeof(ToolDev) * kMaxTools);
     ALLOC(e->d_ring_tail, sizeof(unsigned long long) * 2);
     ALLOC(e->d_step, sizeof(unsigned long long) * 2);
-    // stream-K accumulator workspace: rows padded to 256 per GEMM, Bmax columns
-    const size_t max_rows = (size_t)std::max({(size_t)V, (size_t)2 * dff, (size_t)(H + 2 * Hkv) * hd, (size_t)d}) + 256;
-    ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * Bmax);
-    ALLOC(e->d_tile_cnt, sizeof(int32_t) * 4096);
+    // stream-K partials: 2 slots per CTA (first / last segment) x 256 rows x Bmax columns
+    ALLOC(e->d_gemm_acc, sizeof(float) * 2 * (size_t)e->num_sms * 256 * Bmax);
+    ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
     e->max_patches = 4 * Bmax + 64;
     ALLOC(e->d_patches, sizeof(Patch) * e->max_patches);
     HALLOC(e->h_ring, e->dm_ring, sizeof(cvy_segment) * ec->ring_records);
@@ -415,8 +479,18 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     }
     e->slots.resize(Bmax);
     for (int p = (int)ec->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
+    e->attn_tc = e->bf16 && (hd == 64 || hd == 128) && (H / Hkv) <= 4;
+    if (e->attn_tc) {
+        const uint64_t rows = (uint64_t)m->n_layers * ec->n_pages * 2 * Hkv * kPageTokens;
+        if (!make_tmap(&e->tm_kv, w->kv_pool, rows, (uint64_t)hd, (uint64_t)hd, 16, 64)) {
+            cvy_engine_destroy(e);
+            return fail(CVY_E_CUDA, "KV tensor map encode failed");
+        }
+        cudaFuncSetAttribute(attention_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        cudaFuncSetAttribute(attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+    }
     // kernel attributes
-    cudaFuncSetAttribute(gemm_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    set_gemm_smem_attrs();
     cudaFuncSetAttribute(gemm_simt_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(gemm_simt_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (cudaDeviceSynchronize() != cudaSuccess) {
@@ -431,8 +505,11 @@ void cvy_engine_destroy(cvy_engine* e) {
     if (!e) return;
     cudaSetDevice(e->dev);
     if (e->stream) cudaStreamSynchronize(e->stream);
-    for (auto& kv : e->buckets)
+    for (auto& kv : e->buckets) {
         if (kv.second.graph) cudaGraphExecDestroy(kv.second.graph);
+        if (kv.second.graph_timed) cudaGraphExecDestroy(kv.second.graph_timed);
+        for (cudaEvent_t ev : kv.second.kev) cudaEventDestroy(ev);
+    }
     for (auto& pr : e->inflight) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
@@ -716,7 +793,7 @@ cvy_status launch_k(cvy_engine* e, const void* func, dim3 grid, dim3 block, size
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL)) ? 1 : 0;
+    cfg.numAttrs = (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL) && !e->capturing_timed) ? 1 : 0;
     cudaError_t err = cudaLaunchKernelExC(&cfg, func, args);
     if (err != cudaSuccess) return fail(CVY_E_CUDA, std::string("launch: ") + cudaGetErrorString(err));
     return CVY_OK;
@@ -764,7 +841,7 @@ StepParams base_params(cvy_engine* e, int Bp) {
     P.dbg_logits = e->d_dbg;
     P.lm_done = e->d_lm_done;
     P.attn_part = e->d_attn_part;
-    const int want = (2 * e->num_sms + m.n_kv_heads * Bp - 1) / (m.n_kv_heads * Bp);
+    const int want = (4 * e->num_sms + m.n_kv_heads * Bp - 1) / (m.n_kv_heads * Bp);
     P.attn_splits = std::max(1, std::min(e->attn_splits_max, want));
     P.vtab = e->d_vtab;
     P.vlen = e->d_vlen;
@@ -798,42 +875,18 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
     g.K = K;
     g.epi = epi;
     if (e->bf16) {
-        g.nsub = bk.nsub;
-        g.mma_n = std::min(Bp, 256);
-        g.nbh = Bp / g.mma_n;
-        g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
-        g.bk = Bp >= 512 ? 32 : 64;  // keep >= 2 stages with the (hi, lo) X tiles at Bp=512
-        g.kblocks = K / g.bk;
-        g.acc_stages = (2 * g.nsub * Bp <= 512) ? 2 : 1;
-        if (g.nsub * Bp > 512) {
-            *why = "nsub*Bp exceeds TMEM";
-            return false;
-        }
-        g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * Bp));
+        if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why)) return false;
         g.w_row0 = layer * N;
-        g.acc = e->d_gemm_acc;
+        g.part = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
-        g.xplanes = 2;
         g.x_plane_rows = (int32_t)e->slots.size();
-        const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp, g.xplanes, g.bk);
-        const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
-        const uint32_t budget = 232448;
-        int stages = (int)((budget - fixed) / stage);
-        stages = std::min(stages, 12);
-        if (stages < 2) {
-            *why = "not enough shared memory for 2 stages";
-            return false;
-        }
-        g.stages = stages;
-        gp.smem = (size_t)stages * stage + fixed;
-        const long long T = (long long)g.tiles * g.kblocks;
-        gp.grid = (int)std::min<long long>(e->num_sms, T);
         if (!make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub),
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (weights) failed";
             return false;
         }
-        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * e->slots.size()), (uint64_t)K, (uint64_t)e->act_ld, (uint32_t)g.mma_n,
+        const uint32_t xrows = g.merge ? (uint32_t)Bp : (uint32_t)g.mma_n;
+        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * e->slots.size()), (uint64_t)K, (uint64_t)e->act_ld, xrows,
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (activations) failed";
             return false;
@@ -842,7 +895,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         g.nsub = (epi.kind == EPI_SWIGLU) ? 2 : 1;
         g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
         gp.grid = g.tiles;
-        gp.smem = (size_t)(128 * kEsmLd + Bp + 32 * K) * sizeof(float);
+        gp.smem = (size_t)(128 * kEsmLd + 4 + 4 * Bp + 32 * K) * sizeof(float);
     }
     *out = gp;
     return true;
@@ -892,8 +945,8 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
 cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
     if (e->bf16) {
         void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g};
-        return launch_k(e, (const void*)gemm_tc_kernel<__nv_bfloat16>, dim3(gp.grid), dim3(kGemmThreads), gp.smem, args,
-                        true);
+        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk), dim3(gp.grid),
+                        dim3(kGemmThreads), gp.smem, args, true);
     }
     const float* W = (const float*)gp.W;
     const float* X = (const float*)gp.X;
@@ -904,42 +957,91 @@ cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
     return launch_k(e, (const void*)gemm_simt_kernel<float>, dim3(gp.grid), dim3(128), gp.smem, args, true);
 }
 
+// Event pair around a launch when building the timed graph variant.
+struct KTimer {
+    cvy_engine* e;
+    Bucket& bk;
+    size_t i = 0;
+    KTimer(cvy_engine* e_, Bucket& b) : e(e_), bk(b) {}
+    void begin(int kind, int layer) {
+        if (!e->capturing_timed) return;
+        if (bk.kev.size() < 2 * (i + 1)) {
+            cudaEvent_t a, b;
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            bk.kev.push_back(a);
+            bk.kev.push_back(b);
+            bk.kinfo.push_back({kind, layer});
+        }
+        cudaEventRecordWithFlags(bk.kev[2 * i], e->stream, cudaEventRecordExternal);
+    }
+    void end() {
+        if (!e->capturing_timed) return;
+        cudaEventRecordWithFlags(bk.kev[2 * i + 1], e->stream, cudaEventRecordExternal);
+        ++i;
+    }
+};
+
 cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
     cvy_status st;
     uint32_t launches = 0;
+    KTimer kt(e, bk);
     const int Bp = bk.Bp;
     const cvy_model_config& m = e->m;
     {
         void* args[] = {&bk.P};
         const void* f = e->bf16 ? (const void*)embed_kernel<__nv_bfloat16> : (const void*)embed_kernel<float>;
+        kt.begin(0, 0);
         if ((st = launch_k(e, f, dim3(Bp), dim3(128), 0, args, true)) != CVY_OK) return st;
+        kt.end();
         launches++;
     }
     const int G = m.n_heads / m.n_kv_heads;
     const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
     size_t pi = 0;
     for (int l = 0; l < m.n_layers; ++l) {
+        kt.begin(1, l);
         if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
+        kt.end();
         int layer = l;
         void* aargs[] = {&bk.P, &layer};
-        const void* af = e->bf16 ? (const void*)attention_kernel<__nv_bfloat16> : (const void*)attention_kernel<float>;
-        if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAttnThreads), attn_smem, aargs, true)) !=
-            CVY_OK)
-            return st;
+        kt.begin(2, l);
+        if (e->attn_tc) {
+            void* targs[] = {&e->tm_kv, &bk.P, &layer};
+            const void* tf = m.head_dim == 128 ? (const void*)attention_tc_kernel<128> : (const void*)attention_tc_kernel<64>;
+            const int blk = kPageTokens * m.head_dim * 2;
+            const size_t tsmem = 1024 + (size_t)kAtcStages * kAtcPagesPerStage * 2 * blk + kAtcWarps * 8 * 16 * 2 +
+                                 (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * kAtcStages * 8;
+            if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
+                CVY_OK)
+                return st;
+        } else {
+            const void* af = e->bf16 ? (const void*)attention_kernel<__nv_bfloat16> : (const void*)attention_kernel<float>;
+            if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAttnThreads), attn_smem, aargs,
+                               true)) != CVY_OK)
+                return st;
+        }
+        kt.end();
         launches += 2;
         if (bk.P.attn_splits > 1) {
             void* margs[] = {&bk.P};
             const void* mf =
                 e->bf16 ? (const void*)attention_merge_kernel<__nv_bfloat16> : (const void*)attention_merge_kernel<float>;
+            kt.begin(3, l);
             if ((st = launch_k(e, mf, dim3(m.n_kv_heads, Bp), dim3(128), 0, margs, true)) != CVY_OK) return st;
+            kt.end();
             launches++;
         }
         for (int k = 0; k < 3; ++k) {
+            kt.begin(4 + k, l);
             if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
+            kt.end();
             launches++;
         }
     }
+    kt.begin(7, 0);
     if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
+    kt.end();
     launches++;
     bk.launches = launches;
     return CVY_OK;
@@ -1026,21 +1128,25 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
             return st;
         }
     } else {
-        if (!bk->graph) {
+        cudaGraphExec_t* target = e->timing ? &bk->graph_timed : &bk->graph;
+        if (!*target) {
             cudaGraph_t g;
+            e->capturing_timed = e->timing;
             st = check_cuda(e, cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
             if (st != CVY_OK) return st;
             cvy_status st2 = enqueue_step_kernels(e, *bk);
             cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
+            e->capturing_timed = false;
             if (st2 != CVY_OK) {
                 e->dead = true;
                 return st2;
             }
             if ((st = check_cuda(e, ce, "end capture")) != CVY_OK) return st;
-            if ((st = check_cuda(e, cudaGraphInstantiate(&bk->graph, g, 0), "graph instantiate")) != CVY_OK) return st;
+            if ((st = check_cuda(e, cudaGraphInstantiate(target, g, 0), "graph instantiate")) != CVY_OK) return st;
             cudaGraphDestroy(g);
         }
-        if ((st = check_cuda(e, cudaGraphLaunch(bk->graph, e->stream), "graph launch")) != CVY_OK) return st;
+        if ((st = check_cuda(e, cudaGraphLaunch(*target, e->stream), "graph launch")) != CVY_OK) return st;
+        if (e->timing) e->last_timed = bk;
     }
     cudaEventRecord(ev.second, e->stream);
     if ((st = check_cuda(e, cudaGetLastError(), "step launch")) != CVY_OK) return st;
@@ -1171,6 +1277,32 @@ cvy_status cvy_perf(cvy_engine* e, cvy_perf_info* out) {
 }
 
 void* cvy_stream(cvy_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+cvy_status cvy_set_kernel_timing(cvy_engine* e, int32_t on) {
+    if (!e) return fail(CVY_E_INVAL, "null engine");
+    if (e->c.flags & CVY_ENGINE_NO_GRAPH) return fail(CVY_E_STATE, "kernel timing needs the graph path");
+    e->timing = on != 0;
+    return CVY_OK;
+}
+
+cvy_status cvy_kernel_times(cvy_engine* e, cvy_kernel_time* out, uint32_t cap, uint32_t* n) {
+    if (!e || !out || !n) return fail(CVY_E_INVAL, "null argument");
+    *n = 0;
+    if (!e->last_timed) return fail(CVY_E_STATE, "no timed step has run");
+    cvy_status st = cvy_sync(e);
+    if (st != CVY_OK) return st;
+    Bucket& bk = *e->last_timed;
+    const uint32_t m = std::min<uint32_t>(cap, (uint32_t)bk.kinfo.size());
+    for (uint32_t i = 0; i < m; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, bk.kev[2 * i], bk.kev[2 * i + 1]);
+        out[i].kind = bk.kinfo[i].first;
+        out[i].layer = bk.kinfo[i].second;
+        out[i].ms = ms;
+    }
+    *n = m;
+    return CVY_OK;
+}
 
 cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap, size_t* bytes) {
     if (!e || !bytes) return fail(CVY_E_INVAL, "null argument");
@@ -1325,63 +1457,51 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     cudaDeviceProp prop;
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10) return fail(CVY_E_CUDA, "sm_100a only");
-    cudaFuncSetAttribute(gemm_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    const int Bp = (B + 31) / 32 * 32;
-    const int Bp2 = Bp > 256 ? 512 : (Bp > 128 ? 256 : Bp);
+    set_gemm_smem_attrs();
+    const int Bp0 = (B + 31) / 32 * 32;
+    const int Bp = Bp0 > 256 ? 512 : (Bp0 > 128 ? 256 : Bp0);
     StepParams P;
     std::memset(&P, 0, sizeof(P));
-    P.Bp = Bp2;
-    P.Bmax = Bp2;
+    P.Bp = Bp;
+    P.Bmax = Bp;
     P.act_ld = K;
     GemmTC g;
     std::memset(&g, 0, sizeof(g));
-    g.N = N;
-    g.K = K;
-    g.nsub = Bp2 <= 128 ? 2 : 1;
-    g.mma_n = std::min(Bp2, 256);
-    g.nbh = Bp2 / g.mma_n;
-    g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
-    g.bk = Bp2 >= 512 ? 32 : 64;
-    g.kblocks = K / g.bk;
-    g.acc_stages = (2 * g.nsub * Bp2 <= 512) ? 2 : 1;
-    g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * Bp2));
+    int grid = 0;
+    size_t smem = 0;
+    std::string why;
+    if (!gemm_config(g, N, K, Bp, prop.multiProcessorCount, &grid, &smem, &why)) return fail(CVY_E_INVAL, why);
+    if (const char* gr = getenv("CVY_GEMM_GRID")) grid = std::min(grid, atoi(gr));
     g.w_row0 = 0;
-    g.xplanes = 1;
-    g.x_plane_rows = 0;
-    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp2, 1, g.bk);
-    const uint32_t fixed = GemmSmem::fixed_bytes(Bp2) + 1024;
-    g.stages = std::min(12, (int)((232448 - fixed) / stage));
+    g.x_plane_rows = Bp;
     g.epi.kind = EPI_STORE;
     g.epi.N = N;
-    g.epi.store_out = nullptr;
+    if (const char* dbg = getenv("CVY_GEMM_DEBUG")) g.dbg = atoi(dbg);
     float* Ytmp = nullptr;
-    CUDA_TRY(cudaMalloc(&Ytmp, sizeof(float) * (size_t)Bp2 * N));
+    CUDA_TRY(cudaMalloc(&Ytmp, sizeof(float) * (size_t)Bp * N));
     g.epi.store_out = Ytmp;
-    CUDA_TRY(cudaMalloc(&g.acc, sizeof(float) * (size_t)(g.tiles * g.nsub * 128) * Bp2));
-    CUDA_TRY(cudaMemset(g.acc, 0, sizeof(float) * (size_t)(g.tiles * g.nsub * 128) * Bp2));
-    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (g.tiles + 1)));
-    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (g.tiles + 1)));
-    // X padded to Bp2 rows with zeros
+    CUDA_TRY(cudaMalloc(&g.part, sizeof(float) * 2 * (size_t)grid * g.nsub * 128 * Bp));
+    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * 2 * (g.tiles + 1)));
+    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * 2 * (g.tiles + 1)));
+    // X as the (hi, lo) pair the engine uses: hi = X (exact bf16), lo = 0, padded to Bp rows
     void* Xp = nullptr;
-    CUDA_TRY(cudaMalloc(&Xp, (size_t)Bp2 * K * 2));
-    CUDA_TRY(cudaMemset(Xp, 0, (size_t)Bp2 * K * 2));
+    CUDA_TRY(cudaMalloc(&Xp, (size_t)2 * Bp * K * 2));
+    CUDA_TRY(cudaMemset(Xp, 0, (size_t)2 * Bp * K * 2));
     CUDA_TRY(cudaMemcpy(Xp, X, (size_t)B * K * 2, cudaMemcpyDeviceToDevice));
     CUtensorMap tmW, tmX;
+    const uint32_t xrows = g.merge ? (uint32_t)Bp : (uint32_t)g.mma_n;
     if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub), (uint32_t)g.bk) ||
-        !make_tmap(&tmX, Xp, (uint64_t)Bp2, (uint64_t)K, (uint64_t)K, (uint32_t)g.mma_n, (uint32_t)g.bk))
+        !make_tmap(&tmX, Xp, (uint64_t)(2 * Bp), (uint64_t)K, (uint64_t)K, xrows, (uint32_t)g.bk))
         return fail(CVY_E_CUDA, "tensor map encode failed");
-    int sms = prop.multiProcessorCount;
-    const long long T = (long long)g.tiles * g.kblocks;
-    const int grid = (int)std::min<long long>(sms, T);
-    const size_t smem = (size_t)g.stages * stage + fixed;
+    const void* kfn = gemm_tc_kernel_ptr<__nv_bfloat16>(g.nsub, g.merge != 0, g.bk);
+    void* args[] = {&tmW, &tmX, &P, &g};
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    gemm_tc_kernel<__nv_bfloat16><<<grid, kGemmThreads, smem>>>(tmW, tmX, P, g);  // warm-up
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaLaunchKernel(kfn, dim3(grid), dim3(kGemmThreads), args, smem, 0));  // warm-up
     CUDA_TRY(cudaDeviceSynchronize());
     cudaEventRecord(e0);
-    for (int i = 0; i < iters; ++i) gemm_tc_kernel<__nv_bfloat16><<<grid, kGemmThreads, smem>>>(tmW, tmX, P, g);
+    for (int i = 0; i < iters; ++i) cudaLaunchKernel(kfn, dim3(grid), dim3(kGemmThreads), args, smem, 0);
     cudaEventRecord(e1);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventSynchronize(e1));
@@ -1392,7 +1512,7 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaFree(Ytmp);
-    cudaFree(g.acc);
+    cudaFree(g.part);
     cudaFree(g.tile_cnt);
     cudaFree(Xp);
     return CVY_OK;

@@ -17,22 +17,49 @@ constexpr uint32_t kEpiBar = 1;
 
 CVY_DEV void epi_sync() { named_bar_sync(kEpiBar, kEpiThreads); }
 
-// s_b = 1/sqrt(mean(x_b^2) + eps) from the per-128-block partial sums (fixed order).
-CVY_DEV void compute_row_scales(const StepParams& P, float* s_scale, int et) {
+// Per-column (= per slot) metadata the epilogues need, gathered once per CTA into shared
+// memory so the per-element epilogue never chases global pointers:
+//   scale[b]  = 1/sqrt(mean(x_b^2) + eps) from the per-128-block partial sums (fixed order)
+//   pos[b]    = position of the slot's current token (RoPE angle)
+//   kvoff[b]  = element offset, inside one layer of the KV pool, of (page(pos), K, kv-head 0,
+//               row pos%16); -1 if the slot is idle or out of reserved positions.
+struct EpiMeta {
+    float* scale;
+    int* pos;
+    long long* kvoff;
+};
+CVY_DEV void epilogue_prepare(const StepParams& P, const EpiArgs& E, EpiMeta& m, int et) {
     const int nblk = P.d / 128;
-    for (int b = et; b < P.Bp; b += kEpiThreads) {
-        float acc = 0.f;
-        for (int t = 0; t < nblk; ++t) acc += P.ssq[(size_t)t * P.Bmax + b];
-        s_scale[b] = rsqrtf(acc / (float)P.d + P.eps);
+    if (E.kind == EPI_QKV || E.kind == EPI_SWIGLU || E.kind == EPI_LMHEAD) {
+        for (int b = et; b < P.Bp; b += kEpiThreads) {
+            float acc = 0.f;
+            for (int t = 0; t < nblk; ++t) acc += P.ssq[(size_t)t * P.Bmax + b];
+            m.scale[b] = rsqrtf(acc / (float)P.d + P.eps);
+        }
+    }
+    if (E.kind == EPI_QKV) {
+        const size_t page_elems = (size_t)2 * P.Hkv * kPageTokens * P.hd;
+        for (int b = et; b < P.Bp; b += kEpiThreads) {
+            const SlotDev& s = P.slots[b];
+            int pos = s.pos;
+            long long off = -1;
+            if (s.active && pos < s.max_pos) {
+                const int page = P.page_table[(size_t)b * P.max_pages + pos / kPageTokens];
+                off = (long long)((size_t)page * page_elems + (size_t)(pos % kPageTokens) * P.hd);
+            }
+            m.pos[b] = min(max(pos, 0), P.max_rope_pos - 1);
+            m.kvoff[b] = off;
+        }
     }
 }
 
 // One 32-column chunk of one 128-row sub-tile.  n0 = first global row of the sub-tile.
 template <typename T>
 CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int cb, float* v, float* esm,
-                            const float* s_scale, int et) {
+                            const EpiMeta& M, int et, int width = 32) {
+    const float* s_scale = M.scale;
     const int n = n0 + et;
-    const int ncols = min(32, P.Bp - cb);
+    const int ncols = min(width, P.Bp - cb);
     switch (E.kind) {
         case EPI_QKV: {
             const int hd = P.hd, half = hd >> 1;
@@ -52,9 +79,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                 float pv = esm[partner * kEsmLd + i];
                 float r = v[i];
                 if (rot && i < ncols) {
-                    int pos = P.slots[cb + i].pos;
-                    pos = pos < P.max_rope_pos ? pos : P.max_rope_pos - 1;
-                    float2 cs = P.rope[(size_t)pos * half + j];
+                    const float2 cs = P.rope[(size_t)M.pos[cb + i] * half + j];
                     r = dim < half ? (v[i] * cs.x - pv * cs.y) : (v[i] * cs.x + pv * cs.y);
                 }
                 out[i] = r;
@@ -66,14 +91,12 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                 const int c = n >= qk_rows ? 1 : 0;
                 const int rel = n - P.H * hd - c * P.Hkv * hd;
                 const int g = rel / hd, e = rel % hd;
-                T* kv = reinterpret_cast<T*>(P.kv_pool);
-                for (int i = 0; i < ncols; ++i) {
-                    const SlotDev& s = P.slots[cb + i];
-                    if (!s.active || s.pos >= s.max_pos) continue;
-                    const int page = P.page_table[(size_t)(cb + i) * P.max_pages + s.pos / kPageTokens];
-                    size_t off = ((((size_t)E.layer * P.n_pages + page) * 2 + c) * P.Hkv + g) * (size_t)(kPageTokens * hd) +
-                                 (size_t)(s.pos % kPageTokens) * hd + e;
-                    kv[off] = DT<T>::from_f(out[i]);
+                T* kv = reinterpret_cast<T*>(P.kv_pool) + (size_t)E.layer * P.n_pages * (size_t)(2 * P.Hkv * kPageTokens * hd) +
+                        (size_t)(c * P.Hkv + g) * (kPageTokens * hd) + e;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const long long off = (i < ncols) ? M.kvoff[cb + i] : -1;
+                    if (off >= 0) kv[off] = DT<T>::from_f(out[i]);
                 }
             }
             break;

@@ -1,15 +1,20 @@
 // gemm_sm100.cuh -- skinny decode GEMM on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
 //
 // Y^T[n][b] = sum_k W[n][k] * X[b][k]  (swap-AB: the weight rows are the UMMA M=128 side,
-// the padded batch Bp is the UMMA N side), bf16 inputs, fp32 accumulation in TMEM.
-// Work split: stream-K over (tile, k-block) iterations -- exactly one persistent CTA per
-// SM, each owning a contiguous range of iterations, so every SM streams the same number
-// of weight bytes (HBM-bound for Bp <= ~200).  A tile finished by one CTA is epilogued
-// straight from TMEM; a tile shared by several CTAs is reduced with fp32 vector atomics
-// in an L2-resident workspace and epilogued by the last contributor (arrival ticket).
+// the padded batch is the UMMA N side), bf16 inputs, fp32 accumulation in TMEM.  X is the
+// (hi, lo) bf16 pair of the activation: for Bp <= 128 both planes
+// form ONE B operand of N = 2*Bp rows (TMEM columns [0,Bp) = W.x_hi, [Bp,2Bp) = W.x_lo,
+// summed in the epilogue); above that the two planes are separate MMAs into the same D.
+//
+// Work split: stream-K over (tile, k-block) iterations -- one persistent CTA per SM, each
+// owning a contiguous iteration range, so every SM streams the same weight bytes (the
+// kernel is HBM-bound for Bp <= ~200).  A tile finished by one CTA is epilogued from TMEM;
+// a tile shared by several CTAs is reduced deterministically: every contributor stores its
+// fp32 partial (L2-resident workspace), takes an arrival ticket, and the last one sums the
+// partials in CTA order and runs the epilogue.
 //
 // Warp roles (192 threads): warps 0-3 epilogue (TMEM lanes 0-127), warp 4 TMA producer,
-// warp 5 MMA issuer (one elected lane) and TMEM owner.
+// warp 5 MMA issuer (one lane; descriptors precomputed, loops unrolled) and TMEM owner.
 #pragma once
 #include "common.cuh"
 #include "epilogue.cuh"
@@ -20,24 +25,27 @@ namespace cvy {
 struct GemmTC {
     int32_t N;          // weight rows of this GEMM (one layer)
     int32_t K;
-    int32_t nsub;       // 128-row sub-tiles per tile (1 or 2)
-    int32_t mma_n;      // UMMA N (<= 256)
-    int32_t nbh;        // Bp / mma_n (1 or 2)
+    int32_t nsub;       // 128-row sub-tiles per tile (must equal the kernel's NSUB)
+    int32_t mma_n;      // UMMA N of one MMA
+    int32_t nbh;        // batch halves (Bp / mma_n) when the planes are not merged
     int32_t tiles;
     int32_t kblocks;    // K / bk
     int32_t bk;         // K elements per pipeline stage: 64 (128B swizzle) or 32 (64B swizzle)
     int32_t stages;
     int32_t acc_stages; // TMEM accumulator buffers (1 or 2)
     uint32_t tmem_cols;
+    int32_t cols_per_sub;  // TMEM columns of one sub-tile accumulator (2*Bp merged, else Bp)
+    int32_t merge;      // 1: hi/lo planes merged into one N = 2*Bp MMA
     int32_t w_row0;     // first row of this layer's matrix in the weight tensor map
-    int32_t xplanes;    // activation planes (2: hi/lo bf16 pair, both multiplied into D)
     int32_t x_plane_rows;  // row offset of the lo plane in the activation tensor map
-    float* acc;         // [tiles][nsub*128][Bp] zeroed fp32 workspace
-    int32_t* tile_cnt;  // [tiles] arrival tickets (zeroed)
+    float* part;        // [2*gridDim][nsub*128][Bp] fp32 partials (stream-K workspace)
+    int32_t* tile_cnt;  // [2][tiles] arrival / done counters (zeroed; reset by the last finisher)
     EpiArgs epi;
+    int32_t dbg;        // measurement knobs (test hook only): 1 no epilogue work, 2 no MMA issue
 };
 
 constexpr int kGemmThreads = 192;
+
 // shared-memory carve-up (host and device agree); rows are bk*2 bytes (one swizzle atom)
 struct GemmSmem {
     __host__ __device__ static constexpr uint32_t w_bytes(int nsub, int bk) { return (uint32_t)nsub * 128u * bk * 2u; }
@@ -47,7 +55,8 @@ struct GemmSmem {
     }
     __host__ __device__ static constexpr uint32_t fixed_bytes(int Bp) {
         return 128u * kEsmLd * 4u      // esm
-               + (uint32_t)Bp * 4u      // s_scale
+               + 16u                    // alignment pad
+               + (uint32_t)Bp * 16u     // EpiMeta: scale, pos, kvoff
                + 64u * 8u               // barriers
                + 64u;                   // tmem addr + flags
     }
@@ -60,20 +69,29 @@ CVY_DEV int cta_of_iter(long long i, long long T, int G) {
     return (int)c;
 }
 
-template <typename T>
+// descriptor arithmetic: adding `bytes` (multiple of 16) to the start address field
+CVY_DEV uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
+
+template <typename T, int NSUB, bool MERGE, int BK>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G) {
+    constexpr uint32_t ROW = BK * 2;                  // bytes per smem row
+    constexpr uint32_t WB = NSUB * 128u * ROW;        // weight bytes per stage
+    constexpr int KSTEPS = BK / 16;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const uint32_t stage_bytes = GemmSmem::stage_bytes(G.nsub, P.Bp, G.xplanes, G.bk);
-    const uint32_t row_bytes = (uint32_t)G.bk * 2u;
+    const int Bp = P.Bp;
+    const uint32_t XB = (uint32_t)Bp * ROW;           // one activation plane per stage
+    const uint32_t stage_bytes = WB + 2u * XB;
     uint8_t* fixed = smem + (size_t)G.stages * stage_bytes;
     float* esm = reinterpret_cast<float*>(fixed);
-    float* s_scale = esm + 128 * kEsmLd;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_scale + P.Bp + ((P.Bp & 1) ? 1 : 0));
-    uint64_t* full_bar = bars;
-    uint64_t* empty_bar = bars + G.stages;
+    EpiMeta meta;
+    meta.kvoff = reinterpret_cast<long long*>(esm + 128 * kEsmLd + 4);
+    meta.scale = reinterpret_cast<float*>(meta.kvoff + Bp);
+    meta.pos = reinterpret_cast<int*>(meta.scale + Bp);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta.pos + Bp + 2);
+    uint64_t* empty_bar = full_bar + G.stages;
     uint64_t* tfull_bar = empty_bar + G.stages;
     uint64_t* tempty_bar = tfull_bar + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
@@ -110,28 +128,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (lane == 0) {
             const uint64_t pol_w = policy_evict_first();
             const uint64_t pol_x = policy_evict_last();
-            const uint32_t wb = GemmSmem::w_bytes(G.nsub, G.bk);
-            const int rows_per_tile = 128 * G.nsub;
-            // prologue: weights do not depend on the previous kernel -> issue them before
-            // the grid-dependency wait so the weight stream starts under the previous tail
+            const int rows_per_tile = 128 * NSUB;
+            const int xh = MERGE ? 1 : G.nbh;
+            const int xrows = MERGE ? Bp : G.mma_n;
+            // weights do not depend on the previous kernel: issue the first stages before the
+            // grid-dependency wait so the weight stream starts under the previous kernel's tail
             const long long n_it = it1 - it0;
             const int pre = (int)(n_it < G.stages ? n_it : G.stages);
             for (int i = 0; i < pre; ++i) {
                 const long long it = it0 + i;
                 const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
-                uint8_t* sw = smem + (size_t)i * stage_bytes;
                 mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
-                tma_load_2d(sw, &tmW, &full_bar[i], kb * G.bk, G.w_row0 + tile * rows_per_tile, pol_w);
+                tma_load_2d(smem + (size_t)i * stage_bytes, &tmW, &full_bar[i], kb * BK, G.w_row0 + tile * rows_per_tile,
+                            pol_w);
             }
             pdl_wait();
             for (int i = 0; i < pre; ++i) {
-                const long long it = it0 + i;
-                const int kb = (int)(it % G.kblocks);
-                uint8_t* sx = smem + (size_t)i * stage_bytes + wb;
-                for (int pl = 0; pl < G.xplanes; ++pl)
-                    for (int h = 0; h < G.nbh; ++h)
-                        tma_load_2d(sx + (size_t)(pl * P.Bp + h * G.mma_n) * row_bytes, &tmX, &full_bar[i], kb * G.bk,
-                                    pl * G.x_plane_rows + h * G.mma_n, pol_x);
+                const int kb = (int)((it0 + i) % G.kblocks);
+                uint8_t* sx = smem + (size_t)i * stage_bytes + WB;
+                for (int pl = 0; pl < 2; ++pl)
+                    for (int h = 0; h < xh; ++h)
+                        tma_load_2d(sx + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[i], kb * BK,
+                                    pl * G.x_plane_rows + h * xrows, pol_x);
             }
             int stage = pre % G.stages;
             uint32_t phase = (pre == G.stages) ? 1u : 0u;
@@ -140,11 +158,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
                 uint8_t* sw = smem + (size_t)stage * stage_bytes;
                 mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
-                tma_load_2d(sw, &tmW, &full_bar[stage], kb * G.bk, G.w_row0 + tile * rows_per_tile, pol_w);
-                for (int pl = 0; pl < G.xplanes; ++pl)
-                    for (int h = 0; h < G.nbh; ++h)
-                        tma_load_2d(sw + wb + (size_t)(pl * P.Bp + h * G.mma_n) * row_bytes, &tmX, &full_bar[stage],
-                                    kb * G.bk, pl * G.x_plane_rows + h * G.mma_n, pol_x);
+                tma_load_2d(sw, &tmW, &full_bar[stage], kb * BK, G.w_row0 + tile * rows_per_tile, pol_w);
+                for (int pl = 0; pl < 2; ++pl)
+                    for (int h = 0; h < xh; ++h)
+                        tma_load_2d(sw + WB + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[stage], kb * BK,
+                                    pl * G.x_plane_rows + h * xrows, pol_x);
                 if (++stage == G.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -154,8 +172,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     } else if (warp == 5) {
         // ===================== MMA issuer =====================
         const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)G.mma_n);
-        const uint32_t wb = GemmSmem::w_bytes(G.nsub, G.bk);
-        const bool sw128 = G.bk == 64;
+        const uint64_t d0 = (BK == 64) ? sdesc_kmajor_sw128(smem_u32(smem)) : sdesc_kmajor_sw64(smem_u32(smem));
         int stage = 0;
         uint32_t phase = 0;
         int as = 0;
@@ -166,31 +183,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const long long seg_end = min(it1, (long long)(tile + 1) * G.kblocks);
             mbar_wait(&tempty_bar[as], aphase ^ 1u);
             tc_fence_after();
-            const uint32_t dcol = tmem_base + (uint32_t)(as * G.nsub * P.Bp);
+            const uint32_t dcol = tmem_base + (uint32_t)(as * NSUB * G.cols_per_sub);
+            bool first = true;
             for (; it < seg_end; ++it) {
                 mbar_wait(&full_bar[stage], phase);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t sw = smem_u32(smem + (size_t)stage * stage_bytes);
-                    const uint32_t sx = sw + wb;
-                    const bool first = (it == (long long)tile * G.kblocks) || (it == it0);
-                    for (int k = 0; k < G.bk / 16; ++k) {
-                        for (int s = 0; s < G.nsub; ++s) {
-                            const uint32_t aaddr = sw + (uint32_t)s * 128u * row_bytes + (uint32_t)k * 32u;
-                            const uint64_t ad = sw128 ? sdesc_kmajor_sw128(aaddr) : sdesc_kmajor_sw64(aaddr);
-                            for (int h = 0; h < G.nbh; ++h)
-                                for (int pl = 0; pl < G.xplanes; ++pl) {
-                                    const uint32_t baddr =
-                                        sx + (uint32_t)(pl * P.Bp + h * G.mma_n) * row_bytes + (uint32_t)k * 32u;
-                                    const uint64_t bd = sw128 ? sdesc_kmajor_sw128(baddr) : sdesc_kmajor_sw64(baddr);
-                                    umma_bf16(dcol + (uint32_t)(s * P.Bp + h * G.mma_n), ad, bd, idesc,
-                                              (first && k == 0 && pl == 0) ? 0u : 1u);
-                                }
+                if (lane == 0 && !(G.dbg & 2)) {
+                    const uint64_t ws = desc_add(d0, (uint32_t)stage * stage_bytes);
+                    const uint64_t xs = desc_add(ws, WB);
+#pragma unroll
+                    for (int k = 0; k < KSTEPS; ++k) {
+#pragma unroll
+                        for (int s = 0; s < NSUB; ++s) {
+                            const uint64_t ad = desc_add(ws, (uint32_t)s * 128u * ROW + (uint32_t)k * 32u);
+                            if (MERGE) {
+                                umma_bf16(dcol + (uint32_t)(s * G.cols_per_sub), ad, desc_add(xs, (uint32_t)k * 32u),
+                                          idesc, (first && k == 0) ? 0u : 1u);
+                            } else {
+                                for (int h = 0; h < G.nbh; ++h)
+#pragma unroll
+                                    for (int pl = 0; pl < 2; ++pl)
+                                        umma_bf16(dcol + (uint32_t)(s * G.cols_per_sub + h * G.mma_n), ad,
+                                                  desc_add(xs, (uint32_t)(pl * Bp + h * G.mma_n) * ROW + (uint32_t)k * 32u),
+                                                  idesc, (first && k == 0 && pl == 0) ? 0u : 1u);
+                            }
                         }
                     }
-                    umma_commit(&empty_bar[stage]);
                 }
+                if (lane == 0) umma_commit(&empty_bar[stage]);
                 __syncwarp();
+                first = false;
                 if (++stage == G.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -207,84 +229,164 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // ===================== epilogue (warps 0-3) =====================
         const int et = threadIdx.x;  // 0..127 == TMEM lane == tile row
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-        bool scales_ready = false;
+        const int rows = NSUB * 128;
+        const int first_tile = (int)(it0 / G.kblocks);
+        bool prepared = false;
         int as = 0;
         uint32_t aphase = 0;
         long long it = it0;
         while (it < it1) {
             const int tile = (int)(it / G.kblocks);
             const long long tb = (long long)tile * G.kblocks, te = tb + G.kblocks;
-            const long long seg_end = min(it1, te);
-            const int ncontrib = cta_of_iter(te - 1, T_iters, Gc) - cta_of_iter(tb, T_iters, Gc) + 1;
-            it = seg_end;
-            if (!scales_ready) {
+            it = min(it1, te);
+            const int c_first = cta_of_iter(tb, T_iters, Gc);
+            const int c_last = cta_of_iter(te - 1, T_iters, Gc);
+            if (!prepared) {
                 pdl_wait();
-                if (G.epi.kind != EPI_RESID && G.epi.kind != EPI_STORE) compute_row_scales(P, s_scale, et);
+                epilogue_prepare(P, G.epi, meta, et);
                 epi_sync();
-                scales_ready = true;
+                prepared = true;
             }
             mbar_wait(&tfull_bar[as], aphase);
             tc_fence_after();
-            const uint32_t tacc = tmem_base + lane_off + (uint32_t)(as * G.nsub * P.Bp);
-            float* accw = G.acc + (size_t)tile * (G.nsub * 128) * P.Bp;
-            bool do_epi = true;
-            bool from_tmem = true;
-            if (ncontrib > 1) {
-                // contribute this CTA's partial sums (fp32 vector atomics, L2-resident)
-                for (int s = 0; s < G.nsub; ++s)
-                    for (int cb = 0; cb < P.Bp; cb += 32) {
+            if (G.dbg & 1) {
+                tc_fence_before();
+                mbar_arrive(&tempty_bar[as]);
+                if (++as == G.acc_stages) {
+                    as = 0;
+                    aphase ^= 1u;
+                }
+                continue;
+            }
+            const uint32_t tacc = tmem_base + lane_off + (uint32_t)(as * NSUB * G.cols_per_sub);
+            bool did_epi = false;
+            if (c_first == c_last) {
+                // sole contributor: epilogue straight from TMEM (hi + lo planes summed)
+                for (int s = 0; s < NSUB; ++s)
+                    for (int cb = 0; cb < Bp; cb += 32) {
                         float v[32];
-                        tmem_ld32(tacc + (uint32_t)(s * P.Bp + cb), v);
-                        float4* dst = reinterpret_cast<float4*>(accw + (size_t)(s * 128 + et) * P.Bp + cb);
+                        tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
+                        if (MERGE) {
+                            float w[32];
+                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), w);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            atomicAdd(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                            for (int i = 0; i < 32; ++i) v[i] += w[i];
+                        }
+                        epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
                     }
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
+                did_epi = true;
+            } else {
+                // Shared tile: store this CTA's partial, wait for every contributor, then each
+                // contributor reduces (in CTA order: deterministic) and epilogues its share of the
+                // tile's 16-column units.  Waits only point to lower tiles: no deadlock.
+                const int slot = 2 * blockIdx.x + (tile == first_tile ? 0 : 1);
+                float* mine = G.part + (size_t)slot * rows * Bp;
+                for (int s = 0; s < NSUB; ++s)
+                    for (int cb = 0; cb < Bp; cb += 32) {
+                        float v[32];
+                        tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
+                        if (MERGE) {
+                            float w[32];
+                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), w);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] += w[i];
+                        }
+                        float4* dst = reinterpret_cast<float4*>(mine + (size_t)(s * 128 + et) * Bp + cb);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            __stcg(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                    }
+                tc_fence_before();
+                mbar_arrive(&tempty_bar[as]);
+                const int nc = c_last - c_first + 1;
+                // participants: contributors whose LAST segment is this tile (they finish at the
+                // kernel end anyway); the tile's last contributor, when the tile is only its
+                // first segment, stores and moves on without waiting (no cross-CTA chains)
+                const long long last_it1 = ((long long)(c_last + 1) * T_iters) / Gc;
+                const int n_part = (last_it1 <= te) ? nc : nc - 1;
+                const bool participant = (blockIdx.x - c_first) < n_part;
+                int* arrive_cnt = G.tile_cnt + tile;
+                int* done_cnt = G.tile_cnt + G.tiles + tile;
                 __threadfence();
                 epi_sync();
-                if (et == 0) flags[0] = (atomicAdd(&G.tile_cnt[tile], 1) == ncontrib - 1);
+                if (et == 0) {
+                    atomicAdd(arrive_cnt, 1);
+                    if (participant)
+                        while (*reinterpret_cast<volatile int*>(arrive_cnt) < nc) __nanosleep(64);
+                }
                 epi_sync();
-                do_epi = flags[0] != 0;
-                from_tmem = false;
-                if (do_epi) __threadfence();
-            }
-            if (do_epi) {
-                for (int s = 0; s < G.nsub; ++s) {
-                    const int n0 = (tile * G.nsub + s) * 128;
-                    for (int cb = 0; cb < P.Bp; cb += 32) {
-                        float v[32];
-                        if (from_tmem) {
-                            tmem_ld32(tacc + (uint32_t)(s * P.Bp + cb), v);
-                        } else {
-                            float4* src = reinterpret_cast<float4*>(accw + (size_t)(s * 128 + et) * P.Bp + cb);
+                if (!participant) {
+                    did_epi = false;
+                } else {
+                __threadfence();
+                const int me = blockIdx.x - c_first;
+                const int units = NSUB * (Bp / 16);
+                for (int u = me; u < units; u += n_part) {
+                    const int s = u / (Bp / 16), cb = (u % (Bp / 16)) * 16;
+                    float4 acc4[4] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f),
+                                      make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+                    constexpr int MAXC = 4;  // contributors loaded per batch (MLP)
+                    for (int c0 = c_first; c0 <= c_last; c0 += MAXC) {
+                        float4 buf[MAXC][4];
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                float4 t4 = __ldcg(src + q);
-                                v[4 * q] = t4.x;
-                                v[4 * q + 1] = t4.y;
-                                v[4 * q + 2] = t4.z;
-                                v[4 * q + 3] = t4.w;
-                                __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));
+                        for (int j = 0; j < MAXC; ++j) {
+                            const int c = c0 + j;
+                            if (c <= c_last) {
+                                const long long cit0 = ((long long)c * T_iters) / Gc;
+                                const int cslot = 2 * c + (tile == (int)(cit0 / G.kblocks) ? 0 : 1);
+                                const float4* src = reinterpret_cast<const float4*>(
+                                    G.part + (size_t)cslot * rows * Bp + (size_t)(s * 128 + et) * Bp + cb);
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) buf[j][q] = __ldcg(src + q);
                             }
                         }
-                        epilogue_chunk<T>(P, G.epi, n0, cb, v, esm, s_scale, et);
+#pragma unroll
+                        for (int j = 0; j < MAXC; ++j) {
+                            if (c0 + j <= c_last) {
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    acc4[q].x += buf[j][q].x;
+                                    acc4[q].y += buf[j][q].y;
+                                    acc4[q].z += buf[j][q].z;
+                                    acc4[q].w += buf[j][q].w;
+                                }
+                            }
+                        }
+                    }
+                    float v[32];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        v[4 * q] = acc4[q].x;
+                        v[4 * q + 1] = acc4[q].y;
+                        v[4 * q + 2] = acc4[q].z;
+                        v[4 * q + 3] = acc4[q].w;
+                    }
+#pragma unroll
+                    for (int i = 16; i < 32; ++i) v[i] = 0.f;
+                    epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et, 16);
+                }
+                __threadfence();
+                epi_sync();
+                if (et == 0) {
+                    const int d = atomicAdd(done_cnt, 1);
+                    flags[0] = (d == n_part - 1);
+                    if (d == n_part - 1) {  // every participant has read the partials: reset for reuse
+                        *arrive_cnt = 0;
+                        *done_cnt = 0;
                     }
                 }
-                if (from_tmem) {
-                    tc_fence_before();
-                    mbar_arrive(&tempty_bar[as]);
-                } else if (et == 0) {
-                    G.tile_cnt[tile] = 0;
+                epi_sync();
+                did_epi = flags[0] != 0;  // the tile is complete (for the LM-head tile count)
                 }
-                if (G.epi.kind == EPI_LMHEAD) {
-                    __threadfence();
-                    epi_sync();
-                    if (et == 0) flags[1] = (atomicAdd(P.lm_done, 1) == G.tiles - 1);
-                    epi_sync();
-                    if (flags[1]) sample_scan_publish(P, et, reinterpret_cast<int*>(esm));
-                }
+            }
+            if (G.epi.kind == EPI_LMHEAD && did_epi) {
+                __threadfence();
+                epi_sync();
+                if (et == 0) flags[1] = (atomicAdd(P.lm_done, 1) == G.tiles - 1);
+                epi_sync();
+                if (flags[1]) sample_scan_publish(P, et, reinterpret_cast<int*>(esm));
             }
             if (++as == G.acc_stages) {
                 as = 0;
@@ -298,6 +400,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         tmem_dealloc(tmem_base, G.tmem_cols);
     }
+}
+
+// Host-side selection of the kernel instantiation for a plan.
+template <typename T>
+inline const void* gemm_tc_kernel_ptr(int nsub, bool merge, int bk) {
+    if (bk == 32) return (const void*)gemm_tc_kernel<T, 1, false, 32>;
+    if (merge) return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, true, 64> : (const void*)gemm_tc_kernel<T, 1, true, 64>;
+    return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, false, 64> : (const void*)gemm_tc_kernel<T, 1, false, 64>;
 }
 
 }  // namespace cvy

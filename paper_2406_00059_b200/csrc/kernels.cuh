@@ -331,12 +331,16 @@ __global__ void __launch_bounds__(128) gemm_simt_kernel(const __grid_constant__ 
     pdl_launch_dependents();
     extern __shared__ float gsm[];
     float* esm = gsm;                          // [128][33]
-    float* s_scale = esm + 128 * kEsmLd;       // [Bp]
-    float* xs = s_scale + P.Bp;                // [32][K]
+    EpiMeta meta;
+    meta.kvoff = reinterpret_cast<long long*>(esm + 128 * kEsmLd + 4);
+    meta.scale = reinterpret_cast<float*>(meta.kvoff + P.Bp);
+    meta.pos = reinterpret_cast<int*>(meta.scale + P.Bp);
+    float* xs = reinterpret_cast<float*>(meta.pos + P.Bp);  // [32][K]
     __shared__ int flag;
     pdl_wait();
     const int et = threadIdx.x;
-    if (E.kind != EPI_RESID) compute_row_scales(P, s_scale, et);
+    epilogue_prepare(P, E, meta, et);
+    __syncthreads();
     const int tile = blockIdx.x;
     for (int s = 0; s < nsub; ++s) {
         const int n0 = (tile * nsub + s) * 128;
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(128) gemm_simt_kernel(const __grid_constant__ 
                     for (int i = 0; i < 32; ++i) v[i] = fmaf(w, xs[i * K + k], v[i]);
                 }
             }
-            epilogue_chunk<T>(P, E, n0, cb, v, esm, s_scale, et);
+            epilogue_chunk<T>(P, E, n0, cb, v, esm, meta, et);
         }
     }
     if (E.kind == EPI_LMHEAD) {

@@ -189,6 +189,15 @@ class Engine:
         check(capi.lib().cvy_perf(self.h, ctypes.byref(p)))
         return p
 
+    def set_kernel_timing(self, on: bool):
+        check(capi.lib().cvy_set_kernel_timing(self.h, 1 if on else 0))
+
+    def kernel_times(self):
+        buf = (capi.KernelTime * 4096)()
+        n = ctypes.c_uint32()
+        check(capi.lib().cvy_kernel_times(self.h, buf, len(buf), ctypes.byref(n)))
+        return [(buf[i].kind, buf[i].layer, buf[i].ms) for i in range(n.value)]
+
     def stream_ptr(self) -> int:
         return capi.lib().cvy_stream(self.h) or 0
 

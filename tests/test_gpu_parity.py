@@ -75,6 +75,20 @@ def test_7b_two_layer_slice_bf16():
     assert d < 2e-2
 
 
+@pytest.mark.parametrize("H,Hkv,hd,prefix", [(8, 2, 64, 90), (4, 2, 128, 230), (4, 4, 128, 17), (8, 8, 64, 300)])
+def test_tensor_core_attention_shapes(H, Hkv, hd, prefix):
+    """The TMA + mma.sync attention kernel across head_dim 64/128 and GQA groups 1, 2, 4,
+    contexts spanning several 4-page pipeline stages and split-KV partitions."""
+    from inputs.configs import ModelShape
+    shape = ModelShape(f"att-{H}-{Hkv}-{hd}", L=2, d=512, H=H, Hkv=Hkv, hd=hd, dff=1024, V=512, eps=1e-5,
+                       rope_base=1e4, eos=-1)
+    vocab = [bytes([i % 256]) * (1 + i // 256) for i in range(512)]
+    prompts = [[5, 300], [7], [100, 200, 300]]
+    d, _ = free_running_parity(shape, "bf16", vocab, prompts, max_new=4, seed=1013, tol=2e-2, prefix=prefix,
+                               synth_seeds=[21, 22, 23])
+    assert d < 2e-3
+
+
 @pytest.mark.slow
 def test_7b_full_32_layers_bf16_b2():
     vocab = synthetic_vocab(32000)
