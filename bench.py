@@ -112,6 +112,26 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ------------------------------------------------------------------ multi-rank reduction
+def reduce_over_ranks(local_ms: float, local_tokens: int, stats: list, device=None):
+    """Max-over-ranks device time, whole-job tokens, and the per-rank completion stats
+    all-gathered (NCCL over NVLink/NVSwitch on GPUs, gloo in the CPU tests).  Returns
+    (max_ms, total_tokens, gathered_stats [world][len(stats)])."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    t = torch.tensor([local_ms], dtype=torch.float64, device=device)
+    n = torch.tensor([local_tokens], dtype=torch.float64, device=device)
+    st = torch.tensor(stats, dtype=torch.float64, device=device)
+    if world == 1:
+        return float(t.item()), int(n.item()), [list(map(float, st.tolist()))]
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(n, op=dist.ReduceOp.SUM)
+    gathered = [torch.zeros_like(st) for _ in range(world)]
+    dist.all_gather(gathered, st)
+    return float(t.item()), int(n.item()), [list(map(float, g.tolist())) for g in gathered]
+
+
 # ------------------------------------------------------------------ algorithmic bytes
 def gemm_launch_bytes(shape, kind: int, B: int) -> int:
     """Algorithmic HBM bytes of one projection GEMM launch: the bf16
@@ -269,12 +289,9 @@ def run_ours(args):
     clk = clocks.stop()
     dev_ms = ev0.elapsed_time(ev1)
     perf = eng.perf()
-    t = torch.tensor([dev_ms], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
-    max_ms = float(t.item())
-    value = world * B * K / (max_ms / 1000.0)
+    max_ms, total_tokens, rank_stats = reduce_over_ranks(dev_ms, B * K, [float(rank), dev_ms, float(B * K)],
+                                                         device="cuda")
+    value = total_tokens / (max_ms / 1000.0)
     ctx_mean = float(np.mean([c + K / 2 for c in ctx_start]))
 
     # per-kernel probe (timed graph variant: event pair per launch, no PDL): kernel shares
@@ -331,10 +348,6 @@ def run_ours(args):
     e2e = run_e2e(eng, reqs, tool, B)
     eng.close()
 
-    stats = torch.tensor([value, max_ms], device="cuda", dtype=torch.float64)
-    if world > 1:
-        allst = [torch.zeros_like(stats) for _ in range(world)]
-        dist.all_gather(allst, stats)  # NCCL over NVLink: per-rank completion stats
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -347,7 +360,8 @@ def run_ours(args):
                 "dtype": "bf16", "data": "synthetic", "config": workload_config(B, ctx_mean),
                 "tokens_per_s_per_gpu": value / world, "roofline": roofline, "step_roofline": step_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(perf.launches_per_step) * K,
-                "clocks": clk, "wall_s_timed": wall, "segments_polled": nseg[0]}
+                "clocks": clk, "wall_s_timed": wall, "segments_polled": nseg[0],
+                "rank_stats": rank_stats}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -405,7 +419,15 @@ def main():
     ap.add_argument("--scan-off", action="store_true", help="trigger scan disabled (overhead A/B)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--latency-only", default="", help="comma list of workloads: run only the latency A/B")
+    ap.add_argument("--latency-batch", type=int, default=0, help="override every workload's batch")
     args = ap.parse_args()
+    if args.latency_only:
+        ws = args.latency_only.split(",")
+        base = {"codegen": 64, "search": 128, "planning": 256, "validation": 512}
+        bs = {w: (args.latency_batch or base[w]) for w in ws}
+        print(json.dumps({"latency": run_latency(ws, bs, verbose=True)}), flush=True)
+        return
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
@@ -416,3 +438,47 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+# ------------------------------------------------------------------ latency: partial vs sequential
+def run_latency(workloads, batches, device=0, verbose=False):
+    """Request completion latency with tool partial execution vs sequential tool execution on
+    the four workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool
+    costs in both modes (the baseline is the same code with partial execution
+    disabled).  Returns {workload: {...}}."""
+    from inputs.configs import MISTRAL_7B
+    from inputs.tool_workloads import TOOLS, build
+    from paper_2406_00059_b200 import capi
+    from paper_2406_00059_b200.engine import DeviceModel, Engine
+    from paper_2406_00059_b200.runtime import Runtime, summarize
+    prefixes = {"codegen": 128, "search": 256, "planning": 512, "validation": 1792}
+    max_tokens = {"codegen": 440, "search": 260, "planning": 300, "validation": 320}
+    pages_per = {w: (prefixes[w] + max_tokens[w] + 31) // 16 + 1 for w in workloads}
+    need = max(batches[w] * pages_per[w] for w in workloads) + 64
+    dm = DeviceModel(MISTRAL_7B, "bf16", need, seed=1002, device=device)
+    Bmax = max(batches[w] for w in workloads)
+    from inputs.vocab import synthetic_vocab
+    eng = Engine(dm, synthetic_vocab(32000), max_slots=Bmax, max_pages_per_slot=max(pages_per.values()) + 2,
+                 device=device)
+    tool_ids = {name: eng.register_tool(name, getattr(capi, kind), delims) for name, (kind, delims) in TOOLS.items()}
+    out = {}
+    for w in workloads:
+        res = {}
+        for mode, label in ((capi.MODE_PARTIAL, "partial"), (capi.MODE_SEQUENTIAL, "sequential")):
+            _, specs = build(w, batches[w], tool_ids)
+            rt = Runtime(eng, mode)
+            logs = rt.run(specs)
+            res[label] = summarize(logs, mode)
+            res[label]["steps"] = rt.steps
+            if verbose:
+                print(w, label, res[label], flush=True)
+        p, s_ = res["partial"]["mean_ms"], res["sequential"]["mean_ms"]
+        res["improvement"] = s_ / p - 1.0        # the paper's metric, PAPER.md:171
+        res["reduction"] = 1.0 - p / s_           # the north star's wording
+        if "detection_ms_mean" in res["partial"]:
+            d_p, d_s = res["partial"]["detection_ms_mean"], res["sequential"]["detection_ms_mean"]
+            res["detection_speedup"] = d_s / d_p - 1.0  # PAPER.md:203 reports 376.4%
+        res["batch"] = batches[w]
+        out[w] = res
+    eng.close()
+    return out

@@ -1,0 +1,134 @@
+"""The four tool-using workload shapes of BASELINE.json configs[1..4] as multi-round requests
+with seeded tool-stub cost models (SURVEY.md 8(d) "Configs restated").
+
+The paper gives no per-line or per-call tool costs (its Fig. 3 blocks are "not to scale",
+PAPER.md:119); these distributions are calibration knobs, identical in both modes:
+  codegen   : Python-interpreter stub, one serial instance; a line costs U(50,300) ms if it
+              imports, U(300,600) ms for the final render line, U(1,20) ms otherwise; a `:`
+              block is buffered until its closing blank line.
+  search    : 3 `search("...")` lines, each its own instance, U(200,1000) ms; observations are
+              injected and a 100-token answer follows.
+  planning  : 4 JSON stage objects (JSON_OBJECT parser); searches U(200,1000) ms, calculator
+              1 ms after stages 1-2, formatter 1 ms after stage 3; answer 60 tok.
+  validation: one 12-member JSON call (JSON_MEMBER parser), validator 0.05 ms per member;
+              a `location` member without ", ST" aborts the request.
+No method arithmetic lives here.
+"""
+from __future__ import annotations
+
+import json
+import random
+
+from .vocab import Tokenizer, synthetic_vocab
+from .workloads import codegen_script, plan_stages, prose, search_calls, validation_call
+
+
+def _codegen_plan(rng):
+    state = {"pending": 0.0, "in_block": False}
+    costs = {}
+
+    def plan(j, data: bytes):
+        from paper_2406_00059_b200.runtime import SegmentWork
+        line = data.decode(errors="replace")
+        body = line.strip()
+        if j not in costs:
+            if body.startswith("import"):
+                costs[j] = rng.uniform(0.050, 0.300)
+            elif "savefig" in body or "plt.show" in body or "plt.plot" in body:
+                costs[j] = rng.uniform(0.300, 0.600)
+            elif body == "":
+                costs[j] = 0.0
+            else:
+                costs[j] = rng.uniform(0.001, 0.020)
+        c = costs[j]
+        if body.endswith(":"):
+            state["in_block"] = True
+            state["pending"] = c
+            return SegmentWork(0.0, 0)
+        if state["in_block"]:
+            if body == "":
+                c, state["pending"], state["in_block"] = state["pending"], 0.0, False
+                return SegmentWork(c, 0)
+            state["pending"] += c
+            return SegmentWork(0.0, 0)
+        return SegmentWork(c, 0)
+    return plan
+
+
+def _search_plan(rng):
+    costs = [rng.uniform(0.2, 1.0) for _ in range(16)]
+
+    def plan(j, data: bytes):
+        from paper_2406_00059_b200.runtime import SegmentWork
+        if not data.strip():
+            return None
+        return SegmentWork(costs[j % 16], instance=j)
+    return plan
+
+
+def _planning_plan(rng):
+    costs = [rng.uniform(0.2, 1.0), rng.uniform(0.2, 1.0)]
+
+    def plan(j, data: bytes):
+        from paper_2406_00059_b200.runtime import SegmentWork
+        try:
+            st = json.loads(data.decode().strip())
+        except Exception:
+            return None
+        deps = [d - 1 for d in st.get("deps", []) if 0 <= d - 1 < j]
+        tool = st.get("tool")
+        cost = costs[j] if tool == "search" and j < 2 else 0.001
+        return SegmentWork(cost, instance=j, deps=deps)
+    return plan
+
+
+def _validation_plan():
+    def plan(j, data: bytes):
+        from paper_2406_00059_b200.runtime import SegmentWork
+        txt = data.decode(errors="replace")
+        bad = False
+        if '"location"' in txt:
+            rest = txt.split('"location"', 1)[1].split('"')
+            value = rest[1] if len(rest) > 1 else ""
+            bad = ", " not in value  # "<City>, <ST>" required by the news API
+        return SegmentWork(0.00005, instance=0, abort=bad)
+    return plan
+
+
+def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
+    """Returns (vocab, [RequestSpec]) for one workload shape."""
+    from paper_2406_00059_b200.runtime import RequestSpec, Round
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    specs = []
+    for b in range(B):
+        rng = random.Random(seed * 100003 + b)
+        if workload == "codegen":
+            text = codegen_script(rng, 40)
+            rounds = [Round(tok.encode(text)[:420], tool_ids["interp"], _codegen_plan(rng))]
+            prefix = 128
+        elif workload == "search":
+            r0 = tok.encode(search_calls(rng, 3))
+            obs = tok.encode("\n[OBSERVATION search]\n" + prose(rng, 60) + "\n")[:96]
+            r1 = tok.encode("The answer: " + prose(rng, 80))[:100]
+            rounds = [Round(r0, tool_ids["search"], _search_plan(rng), obs), Round(r1, -1)]
+            prefix = 256
+        elif workload == "planning":
+            r0 = tok.encode(plan_stages(rng))
+            obs = tok.encode("\n[OBSERVATION plan]\n" + prose(rng, 30) + "\n")[:48]
+            r1 = tok.encode("Result: " + prose(rng, 50))[:60]
+            rounds = [Round(r0, tool_ids["planner"], _planning_plan(rng), obs), Round(r1, -1)]
+            prefix = 512
+        elif workload == "validation":
+            bad = rng.random() < 0.5
+            r0 = tok.encode(validation_call(rng, bad))[:300]
+            rounds = [Round(r0, tool_ids["validator"], _validation_plan())]
+            prefix = 1792
+        else:
+            raise ValueError(workload)
+        specs.append(RequestSpec([1, rng.randrange(259, 32000)], rounds, synth_prefix=prefix, synth_seed=b))
+    return vocab, specs
+
+
+TOOLS = {"interp": ("PARSER_LITERAL", [b"\n"]), "search": ("PARSER_LITERAL", [b"\n"]),
+         "planner": ("PARSER_JSON_OBJECT", []), "validator": ("PARSER_JSON_MEMBER", [])}

@@ -1,0 +1,279 @@
+"""Host runtime above the C ABI: segment poller, tool executors, Partial vs Sequential dispatch.
+
+PAPER.md:146 (Fig. 4): the scheduler (1) takes requests, (2) runs decoding iterations, and
+(8) polls tool status; tools (6)/(7) run beside decoding and their outputs become the next
+round's input (step (g)).  Here:
+  * a driver thread calls cvy_step back to back (continuous batching);
+  * a poller thread drains the pinned segment ring (cvy_poll_segments) while decoding
+    continues -- Partial mode dispatches every segment the moment it is polled (tool partial
+    execution), Sequential mode holds a round's segments until its FINAL record
+    ("tool invocation always happens after decoding to the EOS", reading R15);
+  * tool executors are event-driven stubs with seeded costs: segments of one tool instance
+    run serially, instances run in parallel, DAG dependencies are honoured (planning) --
+    the same rules as the O-3 schedule in oracle/latency.py, so measured latencies can be
+    checked against the DES recomputed from the logged availability times;
+  * when a round's FINAL is in and all its tool work is done, the observation is injected
+    (cvy_inject_observation) and the next round decodes; the request completes after its
+    last round (plus its tools, if any).  A validator may abort (cvy_cancel_request).
+"""
+from __future__ import annotations
+
+import heapq
+import threading
+import time
+from dataclasses import dataclass, field
+
+from . import capi
+
+
+@dataclass
+class SegmentWork:
+    cost_s: float
+    instance: int = 0
+    deps: list = field(default_factory=list)   # indices of earlier segments of the round
+    abort: bool = False                        # validator verdict: abort the request
+
+
+@dataclass
+class Round:
+    forced: list                 # teacher-forced generated tokens of the round
+    tool_id: int                 # -1: no tool
+    plan: object = None          # callable(seg_index, seg_bytes) -> SegmentWork
+    observation: list = field(default_factory=list)  # tokens injected before the next round
+
+
+@dataclass
+class RequestSpec:
+    prompt: list
+    rounds: list
+    synth_prefix: int = 0
+    synth_seed: int = 0
+
+
+@dataclass
+class RequestLog:
+    spec: RequestSpec
+    rid: int = 0
+    t_submit: float = 0.0
+    t_done: float = 0.0
+    t_abort: float | None = None
+    round: int = 0
+    round_start: list = field(default_factory=list)
+    round_final: list = field(default_factory=list)
+    seg_avail: list = field(default_factory=list)    # per round: [t]
+    seg_work: list = field(default_factory=list)     # per round: [SegmentWork]
+    seg_end: list = field(default_factory=list)      # per round: [t]
+    held: list = field(default_factory=list)         # Sequential: segments waiting for FINAL
+    pending_tools: int = 0
+    final_seen: bool = False
+    done: bool = False
+
+
+class Runtime:
+    """Drives one engine through a batch of multi-round tool-using requests."""
+
+    def __init__(self, eng, mode: int):
+        self.eng = eng
+        self.mode = mode
+        self.lock = threading.Lock()
+        self.cv = threading.Condition(self.lock)
+        self.events = []           # heap of (t, seq, callback)
+        self.seq = 0
+        self.inst_free = {}        # (req, round, instance) -> t
+        self.by_rid = {}
+        self.active = 0
+        self.stop = False
+        self.steps = 0
+
+    # ---------------------------------------------------------------- tool clock
+    def _schedule(self, t, cb):
+        heapq.heappush(self.events, (t, self.seq, cb))
+        self.seq += 1
+        self.cv.notify_all()
+
+    def _dispatch(self, log: RequestLog, rnd: int, j: int, t_avail: float):
+        """Start segment j of round rnd at max(avail, instance free, deps done)."""
+        work = log.seg_work[rnd][j]
+        dep_ends = [log.seg_end[rnd][d] for d in work.deps]
+        if any(e is None for e in dep_ends):
+            return False  # retried when a dependency finishes
+        key = (log.rid, rnd, work.instance)
+        start = max(t_avail, self.inst_free.get(key, 0.0), max(dep_ends, default=0.0))
+        end = start + work.cost_s
+        self.inst_free[key] = end
+        log.seg_end[rnd][j] = end
+        log.pending_tools += 1
+        self._schedule(end, lambda lg=log, r=rnd, jj=j: self._tool_done(lg, r, jj))
+        return True
+
+    def _tool_done(self, log: RequestLog, rnd: int, j: int):
+        log.pending_tools -= 1
+        now = time.perf_counter()
+        if log.seg_work[rnd][j].abort and log.t_abort is None and not log.done:
+            log.t_abort = now
+            self.eng.cancel_request(log.rid)
+        # dependants waiting for this segment
+        for k, w in enumerate(log.seg_work[rnd]):
+            if log.seg_end[rnd][k] is None and j in w.deps and log.seg_avail[rnd][k] is not None:
+                if self.mode == capi.MODE_PARTIAL or log.final_seen:
+                    self._dispatch(log, rnd, k, max(now, log.seg_avail[rnd][k]))
+        self._maybe_advance(log, now)
+
+    def _maybe_advance(self, log: RequestLog, now: float):
+        if log.done or not log.final_seen or log.pending_tools > 0:
+            return
+        if any(e is None for e in log.seg_end[log.round]):
+            return
+        rnd = log.round
+        spec = log.spec
+        if log.t_abort is not None or rnd + 1 >= len(spec.rounds):
+            log.done = True
+            log.t_done = now
+            self.active -= 1
+            self.cv.notify_all()
+            return
+        nxt = spec.rounds[rnd + 1]
+        log.round = rnd + 1
+        log.final_seen = False
+        self._open_round(log, now)
+        self.eng.inject_observation(log.rid, spec.rounds[rnd].observation, len(nxt.forced), forced=nxt.forced)
+
+    def _open_round(self, log: RequestLog, now: float):
+        log.round_start.append(now)
+        log.round_final.append(None)
+        log.seg_avail.append([])
+        log.seg_work.append([])
+        log.seg_end.append([])
+        log.held = []
+
+    # ---------------------------------------------------------------- poller
+    def _on_record(self, r, now):
+        log = self.by_rid.get(r.req_id)
+        if log is None or log.done:
+            return
+        rnd = log.round
+        spec_round = log.spec.rounds[rnd]
+        is_final = bool(r.flags & capi.SEG_FINAL)
+        if not is_final or r.byte_len > 0:
+            if spec_round.tool_id >= 0 and spec_round.plan is not None:
+                j = len(log.seg_work[rnd])
+                work = spec_round.plan(j, r.data)
+                if work is not None:
+                    log.seg_work[rnd].append(work)
+                    log.seg_avail[rnd].append(now)
+                    log.seg_end[rnd].append(None)
+                    if self.mode == capi.MODE_PARTIAL:
+                        self._dispatch(log, rnd, j, now)
+                    else:
+                        log.held.append(j)
+        if is_final:
+            log.round_final[rnd] = now
+            log.final_seen = True
+            if r.flags & capi.SEG_CANCELLED:
+                log.done = True
+                log.t_done = now if log.t_abort is None else log.t_abort
+                self.active -= 1
+                self.cv.notify_all()
+                return
+            if self.mode == capi.MODE_SEQUENTIAL:
+                for j in log.held:
+                    self._dispatch(log, rnd, j, now)
+                log.held = []
+            # segments whose deps were not ready at dispatch time
+            for k in range(len(log.seg_work[rnd])):
+                if log.seg_end[rnd][k] is None:
+                    self._dispatch(log, rnd, k, now)
+            self._maybe_advance(log, now)
+
+    def _poller(self):
+        while True:
+            with self.lock:
+                if self.stop:
+                    return
+            recs = self.eng.poll_segments(with_bytes=True)
+            now = time.perf_counter()
+            with self.lock:
+                for r in recs:
+                    self._on_record(r, now)
+                # fire due tool completions
+                while self.events and self.events[0][0] <= now:
+                    _, _, cb = heapq.heappop(self.events)
+                    cb()
+            if not recs:
+                time.sleep(0.00005)
+
+    # ---------------------------------------------------------------- driver
+    def run(self, specs: list[RequestSpec], timeout_s: float = 600.0):
+        logs = []
+        t0 = time.perf_counter()
+        with self.lock:
+            for spec in specs:
+                lg = RequestLog(spec)
+                r0 = spec.rounds[0]
+                lg.t_submit = time.perf_counter()
+                lg.rid = self.eng.submit_request(spec.prompt, len(r0.forced), tool_id=r0.tool_id, mode=self.mode,
+                                                 forced=r0.forced, synth_prefix_len=spec.synth_prefix,
+                                                 synth_seed=spec.synth_seed,
+                                                 reserve_tokens=sum(len(rr.forced) + len(rr.observation) + 2
+                                                                    for rr in spec.rounds[1:]) +
+                                                 len(r0.observation))
+                self._open_round(lg, lg.t_submit)
+                self.by_rid[lg.rid] = lg
+                logs.append(lg)
+            self.active = len(logs)
+        th = threading.Thread(target=self._poller, daemon=True)
+        th.start()
+        try:
+            while True:
+                with self.lock:
+                    if self.active <= 0:
+                        break
+                    busy = any(not lg.done and (lg.round_final[lg.round] is None) for lg in logs)
+                if busy:
+                    self.eng.step()
+                    self.steps += 1
+                else:
+                    # every live request waits on tools: idle until an injection is queued
+                    with self.lock:
+                        self.cv.wait(timeout=0.0005)
+                if time.perf_counter() - t0 > timeout_s:
+                    raise TimeoutError("latency run did not finish")
+        finally:
+            self.eng.sync()
+            with self.lock:
+                self.stop = True
+            th.join()
+        for lg in logs:
+            self.eng.release_request(lg.rid)
+        return logs
+
+
+def summarize(logs, mode: int, des_check: bool = True):
+    """Per-request latency (submit -> completion) stats and the DES recomputation."""
+    import numpy as np
+    from oracle.latency import Segment, request_latency  # test/measurement infrastructure only
+    lat = np.array([(lg.t_done - lg.t_submit) * 1e3 for lg in logs])
+    out = {"n": len(logs), "mean_ms": float(lat.mean()), "std_ms": float(lat.std()),
+           "p50_ms": float(np.percentile(lat, 50)), "p95_ms": float(np.percentile(lat, 95))}
+    det = [((lg.t_abort - lg.t_submit) * 1e3) for lg in logs if lg.t_abort is not None]
+    if det:
+        out["detection_ms_mean"] = float(np.mean(det))
+        out["aborted"] = len(det)
+    if des_check:
+        errs = []
+        for lg in logs:
+            if lg.t_abort is not None:
+                continue
+            rounds = []
+            for i in range(len(lg.round_start)):
+                g = (lg.round_final[i] - lg.round_start[i]) if lg.round_final[i] else 0.0
+                segs = [Segment(a - lg.round_start[i], w.cost_s, w.instance, list(w.deps))
+                        for a, w in zip(lg.seg_avail[i], lg.seg_work[i])]
+                rounds.append({"g": g, "segs": segs})
+            # the DES recomputes the request from the logged availability times and costs
+            # (oracle/latency.py, O-3); it must agree within one poll quantum + one step
+            des, _ = request_latency(rounds, partial=(mode == capi.MODE_PARTIAL))
+            errs.append(abs(des - (lg.t_done - lg.t_submit)))
+        if errs:
+            out["des_max_abs_err_ms"] = float(max(errs) * 1e3)
+    return out
