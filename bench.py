@@ -436,9 +436,6 @@ def main():
         run_ours(args)
 
 
-if __name__ == "__main__":
-    main()
-
 
 # ------------------------------------------------------------------ latency: partial vs sequential
 def run_latency(workloads, batches, device=0, verbose=False):
@@ -452,7 +449,7 @@ def run_latency(workloads, batches, device=0, verbose=False):
     from paper_2406_00059_b200.engine import DeviceModel, Engine
     from paper_2406_00059_b200.runtime import Runtime, summarize
     prefixes = {"codegen": 128, "search": 256, "planning": 512, "validation": 1792}
-    max_tokens = {"codegen": 440, "search": 260, "planning": 300, "validation": 320}
+    max_tokens = {"codegen": 440, "search": 560, "planning": 400, "validation": 320}
     pages_per = {w: (prefixes[w] + max_tokens[w] + 31) // 16 + 1 for w in workloads}
     need = max(batches[w] * pages_per[w] for w in workloads) + 64
     dm = DeviceModel(MISTRAL_7B, "bf16", need, seed=1002, device=device)
@@ -482,3 +479,7 @@ def run_latency(workloads, batches, device=0, verbose=False):
         out[w] = res
     eng.close()
     return out
+
+
+if __name__ == "__main__":
+    main()

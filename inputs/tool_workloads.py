@@ -6,10 +6,12 @@ PAPER.md:119); these distributions are calibration knobs, identical in both mode
   codegen   : Python-interpreter stub, one serial instance; a line costs U(50,300) ms if it
               imports, U(300,600) ms for the final render line, U(1,20) ms otherwise; a `:`
               block is buffered until its closing blank line.
-  search    : 3 `search("...")` lines, each its own instance, U(200,1000) ms; observations are
-              injected and a 100-token answer follows.
-  planning  : 4 JSON stage objects (JSON_OBJECT parser); searches U(200,1000) ms, calculator
-              1 ms after stages 1-2, formatter 1 ms after stage 3; answer 60 tok.
+  search    : 3 `search("...")` lines, each followed by the code drafted for that language
+              ("the LLM decoding for the next search"), each search its own
+              instance, U(200,1000) ms; observations are injected and a 100-token answer follows.
+  planning  : 4 JSON stage objects (JSON_OBJECT parser), each after a short thought;
+              searches U(200,1000) ms, calculator 1 ms after stages 1-2, formatter 1 ms after
+              stage 3; answer 60 tokens.
   validation: one 12-member JSON call (JSON_MEMBER parser), validator 0.05 ms per member;
               a `location` member without ", ST" aborts the request.
 No method arithmetic lives here.
@@ -20,7 +22,7 @@ import json
 import random
 
 from .vocab import Tokenizer, synthetic_vocab
-from .workloads import codegen_script, plan_stages, prose, search_calls, validation_call
+from .workloads import codegen_script, plan_with_thoughts, prose, search_session, validation_call
 
 
 def _codegen_plan(rng):
@@ -57,12 +59,15 @@ def _codegen_plan(rng):
 
 def _search_plan(rng):
     costs = [rng.uniform(0.2, 1.0) for _ in range(16)]
+    seen = [0]
 
     def plan(j, data: bytes):
         from paper_2406_00059_b200.runtime import SegmentWork
-        if not data.strip():
-            return None
-        return SegmentWork(costs[j % 16], instance=j)
+        if not data.strip().startswith(b"search("):
+            return None  # drafted code lines are not tool input
+        k = seen[0]
+        seen[0] += 1
+        return SegmentWork(costs[k % 16], instance=k)
     return plan
 
 
@@ -71,13 +76,15 @@ def _planning_plan(rng):
 
     def plan(j, data: bytes):
         from paper_2406_00059_b200.runtime import SegmentWork
+        txt = data.decode(errors="replace")
         try:
-            st = json.loads(data.decode().strip())
+            st = json.loads(txt[txt.index("{"):].strip())
         except Exception:
             return None
+        sid = int(st.get("id", j + 1)) - 1
         deps = [d - 1 for d in st.get("deps", []) if 0 <= d - 1 < j]
         tool = st.get("tool")
-        cost = costs[j] if tool == "search" and j < 2 else 0.001
+        cost = costs[sid] if tool == "search" and sid < 2 else 0.001
         return SegmentWork(cost, instance=j, deps=deps)
     return plan
 
@@ -108,13 +115,13 @@ def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
             rounds = [Round(tok.encode(text)[:420], tool_ids["interp"], _codegen_plan(rng))]
             prefix = 128
         elif workload == "search":
-            r0 = tok.encode(search_calls(rng, 3))
+            r0 = tok.encode(search_session(rng, 3))
             obs = tok.encode("\n[OBSERVATION search]\n" + prose(rng, 60) + "\n")[:96]
             r1 = tok.encode("The answer: " + prose(rng, 80))[:100]
             rounds = [Round(r0, tool_ids["search"], _search_plan(rng), obs), Round(r1, -1)]
             prefix = 256
         elif workload == "planning":
-            r0 = tok.encode(plan_stages(rng))
+            r0 = tok.encode(plan_with_thoughts(rng))
             obs = tok.encode("\n[OBSERVATION plan]\n" + prose(rng, 30) + "\n")[:48]
             r1 = tok.encode("Result: " + prose(rng, 50))[:60]
             rounds = [Round(r0, tool_ids["planner"], _planning_plan(rng), obs), Round(r1, -1)]

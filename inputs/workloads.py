@@ -90,6 +90,31 @@ def search_calls(rng: random.Random, n: int = 3) -> str:
     return "\n".join(out) + "\n"
 
 
+def search_session(rng: random.Random, n: int = 3, code_lines: int = 12) -> str:
+    """Search workload round: the model writes a Hello World program in
+    several languages "consecutively, using tools to search online"; each `search(...)` line is
+    followed by the code it drafts, so a search runs while the next part is decoded."""
+    langs = ["Python", "C++", "Java", "Rust", "Go", "Ruby"]
+    out = []
+    for lang in rng.sample(langs, n):
+        out.append(f'search("hello world program in {lang} site:stackoverflow.com")')
+        out.append(f"# {lang} version, drafted while the search runs")
+        for _ in range(code_lines):
+            out.append(f"{rng.choice(_VARS)} = {_expr(rng)}")
+    return "\n".join(out) + "\n"
+
+
+def plan_with_thoughts(rng: random.Random, words: int = 30) -> str:
+    """LLMCompiler/ReWOO-style plan: a short thought before each stage object (prose holds no
+    brackets, so only the stage objects are JSON)."""
+    stages = plan_stages(rng).strip().split("\n")
+    out = []
+    for st in stages:
+        out.append("Thought: " + prose(rng, words))
+        out.append(st)
+    return "\n".join(out) + "\n"
+
+
 def prose(rng: random.Random, n_words: int) -> str:
     return " ".join(rng.choice(_WORDS) for _ in range(n_words)) + "."
 
