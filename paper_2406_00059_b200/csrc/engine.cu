@@ -434,8 +434,9 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     ALLOC(e->d_tools, sizeof(ToolDev) * kMaxTools);
     ALLOC(e->d_ring_tail, sizeof(unsigned long long) * 2);
     ALLOC(e->d_step, sizeof(unsigned long long) * 2);
-    // stream-K partials: 2 slots per CTA (first / last segment) x 256 rows x Bmax columns
-    ALLOC(e->d_gemm_acc, sizeof(float) * 2 * (size_t)e->num_sms * 256 * Bmax);
+    // stream-K accumulators of shared tiles: rows padded to 256 per GEMM, Bmax columns
+    const size_t max_rows = (size_t)std::max({(size_t)V, (size_t)2 * dff, (size_t)(H + 2 * Hkv) * hd, (size_t)d}) + 256;
+    ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * Bmax);
     ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
     e->max_patches = 4 * Bmax + 64;
     ALLOC(e->d_patches, sizeof(Patch) * e->max_patches);
@@ -1480,9 +1481,10 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     float* Ytmp = nullptr;
     CUDA_TRY(cudaMalloc(&Ytmp, sizeof(float) * (size_t)Bp * N));
     g.epi.store_out = Ytmp;
-    CUDA_TRY(cudaMalloc(&g.part, sizeof(float) * 2 * (size_t)grid * g.nsub * 128 * Bp));
-    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * 2 * (g.tiles + 1)));
-    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * 2 * (g.tiles + 1)));
+    CUDA_TRY(cudaMalloc(&g.part, sizeof(float) * (size_t)g.tiles * g.nsub * 128 * Bp));
+    CUDA_TRY(cudaMemset(g.part, 0, sizeof(float) * (size_t)g.tiles * g.nsub * 128 * Bp));
+    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (g.tiles + 1)));
+    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (g.tiles + 1)));
     // X as the (hi, lo) pair the engine uses: hi = X (exact bf16), lo = 0, padded to Bp rows
     void* Xp = nullptr;
     CUDA_TRY(cudaMalloc(&Xp, (size_t)2 * Bp * K * 2));

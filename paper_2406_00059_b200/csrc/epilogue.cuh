@@ -64,29 +64,32 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
         case EPI_QKV: {
             const int hd = P.hd, half = hd >> 1;
             const int qk_rows = (P.H + P.Hkv) * hd;
+            const int dim = n % hd;
+            const int j = dim & (half - 1);
+            const bool rot = n < qk_rows;
+            // all global inputs first (RoPE cos/sin of every column), then compute, then store:
+            // interleaving loads with stores would serialise them (possible aliasing)
+            float2 cs[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                cs[i] = (rot && i < ncols) ? __ldg(&P.rope[(size_t)M.pos[cb + i] * half + j]) : make_float2(1.f, 0.f);
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] *= s_scale[cb + i];
 #pragma unroll
             for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = v[i];
             epi_sync();
             const int partner = et ^ half;
-            const int dim = n % hd;
-            const int j = dim & (half - 1);
-            const bool rot = n < qk_rows;
             float out[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                float pv = esm[partner * kEsmLd + i];
-                float r = v[i];
-                if (rot && i < ncols) {
-                    const float2 cs = P.rope[(size_t)M.pos[cb + i] * half + j];
-                    r = dim < half ? (v[i] * cs.x - pv * cs.y) : (v[i] * cs.x + pv * cs.y);
-                }
-                out[i] = r;
+                const float pv = esm[partner * kEsmLd + i];
+                out[i] = dim < half ? (v[i] * cs[i].x - pv * cs[i].y) : (v[i] * cs[i].x + pv * cs[i].y);
             }
             epi_sync();
             if (n < P.H * hd) {
-                for (int i = 0; i < ncols; ++i) P.q[(size_t)(cb + i) * (P.H * hd) + n] = out[i];
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < ncols) P.q[(size_t)(cb + i) * (P.H * hd) + n] = out[i];
             } else if (n < E.N) {
                 const int c = n >= qk_rows ? 1 : 0;
                 const int rel = n - P.H * hd - c * P.Hkv * hd;
@@ -105,16 +108,21 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
             T* act = reinterpret_cast<T*>(P.act);
             const bool valid = n < E.N;
             const float w = valid ? E.norm_w[n] : 0.f;
+            float xv[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) xv[i] = (valid && i < ncols) ? P.x[(size_t)(cb + i) * P.d + n] : 0.f;
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
-                float xn = 0.f;
+                const float xn = xv[i] + v[i];
+                xv[i] = xn;
+                esm[et * kEsmLd + i] = (valid && i < ncols) ? xn * xn : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
                 if (valid && i < ncols) {
-                    size_t xi = (size_t)(cb + i) * P.d + n;
-                    xn = P.x[xi] + v[i];
-                    P.x[xi] = xn;
-                    DT<T>::store_act(act + (size_t)(cb + i) * P.act_ld + n, (size_t)P.act_plane, xn * w);
+                    P.x[(size_t)(cb + i) * P.d + n] = xv[i];
+                    DT<T>::store_act(act + (size_t)(cb + i) * P.act_ld + n, (size_t)P.act_plane, xv[i] * w);
                 }
-                esm[et * kEsmLd + i] = xn * xn;
             }
             epi_sync();
             if (et < 32 && et < ncols) {

@@ -9,9 +9,10 @@
 // Work split: stream-K over (tile, k-block) iterations -- one persistent CTA per SM, each
 // owning a contiguous iteration range, so every SM streams the same weight bytes (the
 // kernel is HBM-bound for Bp <= ~200).  A tile finished by one CTA is epilogued from TMEM;
-// a tile shared by several CTAs is reduced deterministically: every contributor stores its
-// fp32 partial (L2-resident workspace), takes an arrival ticket, and the last one sums the
-// partials in CTA order and runs the epilogue.
+// a tile shared by several CTAs is reduced with fp32 vector reductions into an L2-resident
+// accumulator; an arrival ticket elects the last contributor, which reads the sum, re-zeroes
+// it and runs the epilogue.  No CTA ever waits on another (fp32 summation order -- and thus
+// the last bits of the result -- varies run to run).
 //
 // Warp roles (192 threads): warps 0-3 epilogue (TMEM lanes 0-127), warp 4 TMA producer,
 // warp 5 MMA issuer (one lane; descriptors precomputed, loops unrolled) and TMEM owner.
@@ -38,10 +39,11 @@ struct GemmTC {
     int32_t merge;      // 1: hi/lo planes merged into one N = 2*Bp MMA
     int32_t w_row0;     // first row of this layer's matrix in the weight tensor map
     int32_t x_plane_rows;  // row offset of the lo plane in the activation tensor map
-    float* part;        // [2*gridDim][nsub*128][Bp] fp32 partials (stream-K workspace)
-    int32_t* tile_cnt;  // [2][tiles] arrival / done counters (zeroed; reset by the last finisher)
+    float* part;        // [tiles][nsub*128][Bp] fp32 accumulators of shared tiles (zero between uses)
+    int32_t* tile_cnt;  // [tiles] arrival tickets (zero between uses; reset by the last arriver)
     EpiArgs epi;
-    int32_t dbg;        // measurement knobs (test hook only): 1 no epilogue work, 2 no MMA issue
+    int32_t dbg;        // measurement knobs (test hook only): 1 no epilogue work, 2 no MMA issue,
+                        // 4 shared tiles: store partial only, 8 skip the epilogue functor
 };
 
 constexpr int kGemmThreads = 192;
@@ -67,6 +69,11 @@ CVY_DEV int cta_of_iter(long long i, long long T, int G) {
     while (c + 1 < G && ((c + 1) * T) / G <= i) ++c;
     while (c > 0 && (c * T) / G > i) --c;
     return (int)c;
+}
+
+// fp32 x4 reduction into global memory at L2, no return value
+CVY_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
 // descriptor arithmetic: adding `bytes` (multiple of 16) to the start address field
@@ -272,17 +279,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
                         }
-                        epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
+                        if (!(G.dbg & 8)) epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
                     }
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
                 did_epi = true;
             } else {
-                // Shared tile: store this CTA's partial, wait for every contributor, then each
-                // contributor reduces (in CTA order: deterministic) and epilogues its share of the
-                // tile's 16-column units.  Waits only point to lower tiles: no deadlock.
-                const int slot = 2 * blockIdx.x + (tile == first_tile ? 0 : 1);
-                float* mine = G.part + (size_t)slot * rows * Bp;
+                // Shared tile: add this CTA's partial into the tile's fp32 accumulator with L2
+                // vector reductions (no return, nobody waits), take an arrival ticket; the last
+                // arriver reads the completed sum, re-zeroes it, and runs the epilogue.
+                float* acc = G.part + (size_t)tile * rows * Bp;
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
                         float v[32];
@@ -293,92 +299,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
                         }
-                        float4* dst = reinterpret_cast<float4*>(mine + (size_t)(s * 128 + et) * Bp + cb);
+                        float* dst = acc + (size_t)(s * 128 + et) * Bp + cb;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            __stcg(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                        for (int q = 0; q < 8; ++q) red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                     }
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
-                const int nc = c_last - c_first + 1;
-                // participants: contributors whose LAST segment is this tile (they finish at the
-                // kernel end anyway); the tile's last contributor, when the tile is only its
-                // first segment, stores and moves on without waiting (no cross-CTA chains)
-                const long long last_it1 = ((long long)(c_last + 1) * T_iters) / Gc;
-                const int n_part = (last_it1 <= te) ? nc : nc - 1;
-                const bool participant = (blockIdx.x - c_first) < n_part;
-                int* arrive_cnt = G.tile_cnt + tile;
-                int* done_cnt = G.tile_cnt + G.tiles + tile;
                 __threadfence();
                 epi_sync();
-                if (et == 0) {
-                    atomicAdd(arrive_cnt, 1);
-                    if (participant)
-                        while (*reinterpret_cast<volatile int*>(arrive_cnt) < nc) __nanosleep(64);
-                }
+                if (et == 0) flags[0] = (atomicAdd(&G.tile_cnt[tile], 1) == c_last - c_first) && !(G.dbg & 4);
                 epi_sync();
-                if (!participant) {
-                    did_epi = false;
-                } else {
-                __threadfence();
-                const int me = blockIdx.x - c_first;
-                const int units = NSUB * (Bp / 16);
-                for (int u = me; u < units; u += n_part) {
-                    const int s = u / (Bp / 16), cb = (u % (Bp / 16)) * 16;
-                    float4 acc4[4] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f),
-                                      make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-                    constexpr int MAXC = 4;  // contributors loaded per batch (MLP)
-                    for (int c0 = c_first; c0 <= c_last; c0 += MAXC) {
-                        float4 buf[MAXC][4];
+                if (flags[0]) {
+                    __threadfence();
+                    for (int s = 0; s < NSUB; ++s)
+                        for (int cb = 0; cb < Bp; cb += 32) {
+                            float v[32];
+                            float4* src = reinterpret_cast<float4*>(acc + (size_t)(s * 128 + et) * Bp + cb);
 #pragma unroll
-                        for (int j = 0; j < MAXC; ++j) {
-                            const int c = c0 + j;
-                            if (c <= c_last) {
-                                const long long cit0 = ((long long)c * T_iters) / Gc;
-                                const int cslot = 2 * c + (tile == (int)(cit0 / G.kblocks) ? 0 : 1);
-                                const float4* src = reinterpret_cast<const float4*>(
-                                    G.part + (size_t)cslot * rows * Bp + (size_t)(s * 128 + et) * Bp + cb);
-#pragma unroll
-                                for (int q = 0; q < 4; ++q) buf[j][q] = __ldcg(src + q);
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 t4 = __ldcg(src + q);
+                                v[4 * q] = t4.x;
+                                v[4 * q + 1] = t4.y;
+                                v[4 * q + 2] = t4.z;
+                                v[4 * q + 3] = t4.w;
                             }
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));
+                            if (!(G.dbg & 8)) epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
                         }
-#pragma unroll
-                        for (int j = 0; j < MAXC; ++j) {
-                            if (c0 + j <= c_last) {
-#pragma unroll
-                                for (int q = 0; q < 4; ++q) {
-                                    acc4[q].x += buf[j][q].x;
-                                    acc4[q].y += buf[j][q].y;
-                                    acc4[q].z += buf[j][q].z;
-                                    acc4[q].w += buf[j][q].w;
-                                }
-                            }
-                        }
-                    }
-                    float v[32];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        v[4 * q] = acc4[q].x;
-                        v[4 * q + 1] = acc4[q].y;
-                        v[4 * q + 2] = acc4[q].z;
-                        v[4 * q + 3] = acc4[q].w;
-                    }
-#pragma unroll
-                    for (int i = 16; i < 32; ++i) v[i] = 0.f;
-                    epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et, 16);
-                }
-                __threadfence();
-                epi_sync();
-                if (et == 0) {
-                    const int d = atomicAdd(done_cnt, 1);
-                    flags[0] = (d == n_part - 1);
-                    if (d == n_part - 1) {  // every participant has read the partials: reset for reuse
-                        *arrive_cnt = 0;
-                        *done_cnt = 0;
-                    }
-                }
-                epi_sync();
-                did_epi = flags[0] != 0;  // the tile is complete (for the LM-head tile count)
+                    if (et == 0) G.tile_cnt[tile] = 0;
+                    did_epi = true;
                 }
             }
             if (G.epi.kind == EPI_LMHEAD && did_epi) {

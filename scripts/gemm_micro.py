@@ -11,8 +11,8 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     _, ms = debug_gemm(W, X, N, K, B, iters=50)
     print(json.dumps({"N": N, "K": K, "B": B, "us": ms * 1e3, "GBps": N * K * 2 / ms / 1e6}))
     sys.exit(0)
-cases = [(128*148, 4096, 64), (256, 4096, 64), (4096, 4096, 64), (6144, 4096, 64), (28672, 4096, 64), (4096, 14336, 64), (32000, 4096, 64), (4096, 4096, 256), (28672, 4096, 512)]
-envs = [{}, {"CVY_GEMM_DEBUG": "1"}, {"CVY_GEMM_NSUB": "2"}]
+cases = [(4096, 4096, 64), (6144, 4096, 64), (28672, 4096, 64), (4096, 14336, 64), (32000, 4096, 64)]
+envs = [{}, {"CVY_GEMM_DEBUG": "4"}, {"CVY_GEMM_DEBUG": "1"}]
 for env in envs:
     for (N, K, B) in cases:
         e = dict(os.environ); e.update(env)
