@@ -87,13 +87,14 @@ bool make_tmap(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
 //   Bp <= 128: 2 sub-tiles (256 weight rows) per tile, hi/lo planes merged (MMA N = 2*Bp)
 //   Bp 160..256: 1 sub-tile, planes as two MMAs into one accumulator (N = Bp)
 //   Bp 512: 1 sub-tile, 2 batch halves of N = 256, 32-element K stages (64B swizzle)
-bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why) {
+bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why,
+                 bool allow_kernel_split = true) {
     g.N = N;
     g.K = K;
     g.merge = Bp <= 128;
     g.bk = Bp >= 512 ? 32 : 64;
-    // 256-row tiles halve the activation (L2) traffic for the wide GEMMs; the narrow ones
-    // (N < 8192) use 128-row tiles to keep the stream-K partials small
+    // wide GEMMs (gate/up, LM head): 256-row tiles, one per CTA, no reduction; narrow ones
+    // (QKV, O, down): 128-row tiles with K split over a 2..4-CTA cluster (DSMEM reduction)
     g.nsub = (g.merge && N >= 8192) ? 2 : 1;
     if (const char* ns = getenv("CVY_GEMM_NSUB")) g.nsub = std::max(1, std::min(2, atoi(ns)));
     if (g.merge) {
@@ -105,7 +106,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         g.nbh = Bp / g.mma_n;
         g.cols_per_sub = Bp;
     }
-    if (g.bk == 32) g.nsub = 1;
+    if (g.bk == 32 || !g.merge) g.nsub = 1;
     if (g.nsub * g.cols_per_sub > 512) {
         *why = "accumulator exceeds TMEM";
         return false;
@@ -123,8 +124,23 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     }
     g.stages = stages;
     *smem = (size_t)stages * stage + fixed;
-    const long long T = (long long)g.tiles * g.kblocks;
-    *grid = (int)std::min<long long>(num_sms, T);
+    // split mode: tiles <= SMs (one tile, or one cluster of S CTAs per tile)
+    g.split = 0;
+    if (g.merge && !getenv("CVY_GEMM_STREAMK")) {
+        int S = 1;
+        // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
+        while (allow_kernel_split && S < 4 && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
+        if (S == 3) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
+        if (g.tiles <= num_sms) g.split = S;
+        // the DSMEM staging of the partial must fit in the pipeline smem
+        if (g.split > 1 && (size_t)g.nsub * Bp * 512 > (size_t)stages * stage) g.split = 0;
+    }
+    if (g.split > 0) {
+        *grid = g.tiles * g.split;
+    } else {
+        const long long T = (long long)g.tiles * g.kblocks;
+        *grid = (int)std::min<long long>(num_sms, T);
+    }
     return true;
 }
 
@@ -132,11 +148,12 @@ void set_gemm_smem_attrs() {
     static bool done = false;
     if (done) return;
     done = true;
-    for (int nsub = 1; nsub <= 2; ++nsub)
-        for (int merge = 0; merge <= 1; ++merge)
-            for (int bk : {32, 64})
-                cudaFuncSetAttribute(gemm_tc_kernel_ptr<__nv_bfloat16>(nsub, merge != 0, bk),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    for (int epi = 0; epi <= EPI_STORE; ++epi)
+        for (int nsub = 1; nsub <= 2; ++nsub)
+            for (int merge = 0; merge <= 1; ++merge)
+                for (int bk : {32, 64})
+                    cudaFuncSetAttribute(gemm_tc_kernel_ptr<__nv_bfloat16>(nsub, merge != 0, bk, epi),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
 }
 
 struct SlotHost {
@@ -180,6 +197,8 @@ struct Bucket {
 
 }  // namespace
 
+struct cvy_engine;
+int m_d(const cvy_engine* e);
 struct cvy_engine {
     cvy_model_config m{};
     cvy_engine_config c{};
@@ -253,10 +272,14 @@ struct cvy_engine {
     std::vector<uint8_t> vlen_host;
     bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
     CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd]
+    unsigned long long* d_trace = nullptr;  // test hook: GEMM CTA timestamps of one layer
+    int trace_layer = -1;
     bool timing = false;        // launch the timed graph variant
     bool capturing_timed = false;
     Bucket* last_timed = nullptr;
 };
+
+int m_d(const cvy_engine* e) { return e->m.d_model; }
 
 namespace {
 
@@ -480,6 +503,14 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     }
     e->slots.resize(Bmax);
     for (int p = (int)ec->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
+    if (const char* tl = getenv("CVY_GEMM_TRACE_LAYER")) {
+        e->trace_layer = atoi(tl);
+        if (cudaMalloc(&e->d_trace, sizeof(unsigned long long) * 8 * 4 * e->num_sms) != cudaSuccess) {
+            cvy_engine_destroy(e);
+            return fail(CVY_E_NOMEM, "trace buffer");
+        }
+        cudaMemset(e->d_trace, 0, sizeof(unsigned long long) * 8 * 4 * e->num_sms);
+    }
     e->attn_tc = e->bf16 && (hd == 64 || hd == 128) && (H / Hkv) <= 4;
     if (e->attn_tc) {
         const uint64_t rows = (uint64_t)m->n_layers * ec->n_pages * 2 * Hkv * kPageTokens;
@@ -519,7 +550,7 @@ void cvy_engine_destroy(cvy_engine* e) {
         cudaEventDestroy(pr.first);
         cudaEventDestroy(pr.second);
     }
-    void* dptrs[] = {e->d_slots, e->d_page_table, e->d_in_buf, e->d_force_buf, e->d_rope, e->d_x, e->d_act, e->d_q,
+    void* dptrs[] = {e->d_trace, e->d_slots, e->d_page_table, e->d_in_buf, e->d_force_buf, e->d_rope, e->d_x, e->d_act, e->d_q,
                      e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches};
     for (void* p : dptrs)
@@ -783,18 +814,30 @@ int32_t cvy_request_state(cvy_engine* e, uint64_t req_id) {
 // ============================================================================ step graph
 namespace {
 
-cvy_status launch_k(cvy_engine* e, const void* func, dim3 grid, dim3 block, size_t smem, void** args, bool pdl) {
+cvy_status launch_k(cvy_engine* e, const void* func, dim3 grid, dim3 block, size_t smem, void** args, bool pdl,
+                    int cluster = 1) {
     cudaLaunchConfig_t cfg;
     std::memset(&cfg, 0, sizeof(cfg));
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = e->stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL) && !e->capturing_timed) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)cluster;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL) && !e->capturing_timed) ? 1 : 0;
+    cfg.numAttrs = na;
     cudaError_t err = cudaLaunchKernelExC(&cfg, func, args);
     if (err != cudaSuccess) return fail(CVY_E_CUDA, std::string("launch: ") + cudaGetErrorString(err));
     return CVY_OK;
@@ -876,8 +919,12 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
     g.K = K;
     g.epi = epi;
     if (e->bf16) {
-        if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why)) return false;
+        if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD)) return false;
         g.w_row0 = layer * N;
+        if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD) {
+            const int k = epi.kind == EPI_QKV ? 0 : epi.kind == EPI_SWIGLU ? 2 : (K == ::m_d(e) ? 1 : 3);
+            g.trace = e->d_trace + (size_t)k * 8 * e->num_sms;
+        }
         g.part = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
         g.x_plane_rows = (int32_t)e->slots.size();
@@ -946,8 +993,8 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
 cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
     if (e->bf16) {
         void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g};
-        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk), dim3(gp.grid),
-                        dim3(kGemmThreads), gp.smem, args, true);
+        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind), dim3(gp.grid),
+                        dim3(kGemmThreads), gp.smem, args, true, gp.g.split > 1 ? gp.g.split : 1);
     }
     const float* W = (const float*)gp.W;
     const float* X = (const float*)gp.X;
@@ -1317,6 +1364,11 @@ cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap,
         case 3: src = e->d_o; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
         case 4: src = e->d_h; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
         case 5: src = e->d_ssq; n = (size_t)(e->m.d_model / 128) * B * 4; break;
+        case 10: case 11: case 12: case 13:
+            if (!e->d_trace) return fail(CVY_E_STATE, "set CVY_GEMM_TRACE_LAYER before engine create");
+            src = e->d_trace + (size_t)(which - 10) * 8 * e->num_sms;
+            n = sizeof(unsigned long long) * 8 * e->num_sms;
+            break;
         default: return fail(CVY_E_INVAL, "unknown buffer");
     }
     *bytes = n;
@@ -1472,7 +1524,6 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     size_t smem = 0;
     std::string why;
     if (!gemm_config(g, N, K, Bp, prop.multiProcessorCount, &grid, &smem, &why)) return fail(CVY_E_INVAL, why);
-    if (const char* gr = getenv("CVY_GEMM_GRID")) grid = std::min(grid, atoi(gr));
     g.w_row0 = 0;
     g.x_plane_rows = Bp;
     g.epi.kind = EPI_STORE;
@@ -1495,21 +1546,62 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub), (uint32_t)g.bk) ||
         !make_tmap(&tmX, Xp, (uint64_t)(2 * Bp), (uint64_t)K, (uint64_t)K, xrows, (uint32_t)g.bk))
         return fail(CVY_E_CUDA, "tensor map encode failed");
-    const void* kfn = gemm_tc_kernel_ptr<__nv_bfloat16>(g.nsub, g.merge != 0, g.bk);
+    const void* kfn = gemm_tc_kernel_ptr<__nv_bfloat16>(g.nsub, g.merge != 0, g.bk, EPI_STORE);
     void* args[] = {&tmW, &tmX, &P, &g};
+    cudaLaunchConfig_t lc;
+    std::memset(&lc, 0, sizeof(lc));
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kGemmThreads);
+    lc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = (unsigned)(g.split > 1 ? g.split : 1);
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    lc.attrs = la;
+    lc.numAttrs = 1;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    CUDA_TRY(cudaLaunchKernel(kfn, dim3(grid), dim3(kGemmThreads), args, smem, 0));  // warm-up
+    CUDA_TRY(cudaLaunchKernelExC(&lc, kfn, args));  // warm-up
     CUDA_TRY(cudaDeviceSynchronize());
     cudaEventRecord(e0);
-    for (int i = 0; i < iters; ++i) cudaLaunchKernel(kfn, dim3(grid), dim3(kGemmThreads), args, smem, 0);
+    for (int i = 0; i < iters; ++i) cudaLaunchKernelExC(&lc, kfn, args);
     cudaEventRecord(e1);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventSynchronize(e1));
     float t = 0.f;
     cudaEventElapsedTime(&t, e0, e1);
     if (ms) *ms = t / iters;
+    if (getenv("CVY_GEMM_TRACE")) {
+        // one traced launch: per-CTA globaltimer stamps relative to the earliest CTA start
+        unsigned long long* tr = nullptr;
+        CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * grid));
+        CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * grid));
+        g.trace = tr;
+        void* targs[] = {&tmW, &tmX, &P, &g};
+        CUDA_TRY(cudaLaunchKernelExC(&lc, kfn, targs));
+        CUDA_TRY(cudaDeviceSynchronize());
+        std::vector<unsigned long long> h(8 * (size_t)grid);
+        CUDA_TRY(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
+        cudaFree(tr);
+        g.trace = nullptr;
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[8 * c]);
+        double mx[6] = {0}, mn[6], sum[6] = {0};
+        for (int k = 0; k < 6; ++k) mn[k] = 1e30;
+        for (int c = 0; c < grid; ++c)
+            for (int k = 0; k < 6; ++k) {
+                double v = h[8 * c + k] ? (h[8 * c + k] - t0) * 1e-3 : -1;
+                mx[k] = std::max(mx[k], v);
+                mn[k] = std::min(mn[k], v);
+                sum[k] += v;
+            }
+        const char* names[6] = {"start", "producer done", "first seg MMA done", "last seg MMA done", "epilogue done",
+                                "exit"};
+        for (int k = 0; k < 6; ++k)
+            fprintf(stderr, "trace %-20s min %8.2f avg %8.2f max %8.2f us\n", names[k], mn[k], sum[k] / grid, mx[k]);
+    }
     CUDA_TRY(cudaMemcpy2D(Y, sizeof(float) * N, Ytmp, sizeof(float) * N, sizeof(float) * N, B, cudaMemcpyDeviceToDevice));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

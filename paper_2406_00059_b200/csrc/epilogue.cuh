@@ -54,13 +54,13 @@ CVY_DEV void epilogue_prepare(const StepParams& P, const EpiArgs& E, EpiMeta& m,
 }
 
 // One 32-column chunk of one 128-row sub-tile.  n0 = first global row of the sub-tile.
-template <typename T>
+template <typename T, int KIND = -1>
 CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int cb, float* v, float* esm,
                             const EpiMeta& M, int et, int width = 32) {
     const float* s_scale = M.scale;
     const int n = n0 + et;
     const int ncols = min(width, P.Bp - cb);
-    switch (E.kind) {
+    switch (KIND >= 0 ? KIND : E.kind) {
         case EPI_QKV: {
             const int hd = P.hd, half = hd >> 1;
             const int qk_rows = (P.H + P.Hkv) * hd;
@@ -154,8 +154,9 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
             break;
         }
         case EPI_STORE: {
-            if (n < E.N)
-                for (int i = 0; i < ncols; ++i) E.store_out[(size_t)(cb + i) * E.N + n] = v[i];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (n < E.N && i < ncols) E.store_out[(size_t)(cb + i) * E.N + n] = v[i];
             break;
         }
         case EPI_LMHEAD: {

@@ -37,6 +37,8 @@ struct GemmTC {
     uint32_t tmem_cols;
     int32_t cols_per_sub;  // TMEM columns of one sub-tile accumulator (2*Bp merged, else Bp)
     int32_t merge;      // 1: hi/lo planes merged into one N = 2*Bp MMA
+    int32_t split;      // 0: stream-K over all CTAs; S >= 1: tile = blockIdx/S, K split over the S
+                        //    CTAs of a thread-block cluster, reduced through DSMEM
     int32_t w_row0;     // first row of this layer's matrix in the weight tensor map
     int32_t x_plane_rows;  // row offset of the lo plane in the activation tensor map
     float* part;        // [tiles][nsub*128][Bp] fp32 accumulators of shared tiles (zero between uses)
@@ -44,7 +46,14 @@ struct GemmTC {
     EpiArgs epi;
     int32_t dbg;        // measurement knobs (test hook only): 1 no epilogue work, 2 no MMA issue,
                         // 4 shared tiles: store partial only, 8 skip the epilogue functor
+    unsigned long long* trace;  // test hook: [grid][8] %globaltimer stamps, or null
 };
+
+CVY_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int kGemmThreads = 192;
 
@@ -79,7 +88,7 @@ CVY_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
 // descriptor arithmetic: adding `bytes` (multiple of 16) to the start address field
 CVY_DEV uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
 
-template <typename T, int NSUB, bool MERGE, int BK>
+template <typename T, int NSUB, bool MERGE, int BK, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G) {
@@ -107,8 +116,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long T_iters = (long long)G.tiles * G.kblocks;
     const int Gc = gridDim.x;
-    const long long it0 = ((long long)blockIdx.x * T_iters) / Gc;
-    const long long it1 = ((long long)(blockIdx.x + 1) * T_iters) / Gc;
+    long long it0, it1;
+    int crank = 0;
+    if (G.split > 0) {
+        // cluster split-K: CTA (tile, rank) owns k-blocks [rank*KB/S, (rank+1)*KB/S) of one tile
+        const int tile = blockIdx.x / G.split;
+        crank = blockIdx.x % G.split;
+        it0 = (long long)tile * G.kblocks + ((long long)crank * G.kblocks) / G.split;
+        it1 = (long long)tile * G.kblocks + ((long long)(crank + 1) * G.kblocks) / G.split;
+    } else {
+        it0 = ((long long)blockIdx.x * T_iters) / Gc;
+        it1 = ((long long)(blockIdx.x + 1) * T_iters) / Gc;
+    }
 
     if (warp == 4 && lane == 0) {
         tma_prefetch_desc(&tmW);
@@ -129,6 +148,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
+    unsigned long long* tr = G.trace ? G.trace + (size_t)blockIdx.x * 8 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (warp == 4) {
         // ===================== TMA producer =====================
@@ -175,6 +196,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     phase ^= 1u;
                 }
             }
+            if (tr) tr[1] = gtimer();
         }
     } else if (warp == 5) {
         // ===================== MMA issuer =====================
@@ -246,8 +268,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int tile = (int)(it / G.kblocks);
             const long long tb = (long long)tile * G.kblocks, te = tb + G.kblocks;
             it = min(it1, te);
-            const int c_first = cta_of_iter(tb, T_iters, Gc);
-            const int c_last = cta_of_iter(te - 1, T_iters, Gc);
+            const int c_first = G.split > 0 ? 0 : cta_of_iter(tb, T_iters, Gc);
+            const int c_last = G.split > 0 ? 0 : cta_of_iter(te - 1, T_iters, Gc);
             if (!prepared) {
                 pdl_wait();
                 epilogue_prepare(P, G.epi, meta, et);
@@ -256,6 +278,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             mbar_wait(&tfull_bar[as], aphase);
             tc_fence_after();
+            if (tr && et == 0) tr[2 + (it >= it1 ? 1 : 0)] = gtimer();  // [2] first / [3] last segment's MMA done
             if (G.dbg & 1) {
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
@@ -267,7 +290,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             const uint32_t tacc = tmem_base + lane_off + (uint32_t)(as * NSUB * G.cols_per_sub);
             bool did_epi = false;
-            if (c_first == c_last) {
+            if (G.split > 1) {
+                // stage this CTA's partial in its (now idle) pipeline smem as 16-column units
+                // [sub][unit][row][16] for the cluster reduce-scatter after the role branches
+                float* stagep = reinterpret_cast<float*>(smem);
+                for (int s = 0; s < NSUB; ++s)
+                    for (int cb = 0; cb < Bp; cb += 32) {
+                        float v[32];
+                        tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
+                        if (MERGE) {
+                            float w[32];
+                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), w);
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) v[i] += w[i];
+                        }
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float4* dst = reinterpret_cast<float4*>(
+                                stagep + ((size_t)(s * (Bp / 16) + cb / 16 + h) * 128 + et) * 16);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                dst[q] = make_float4(v[16 * h + 4 * q], v[16 * h + 4 * q + 1], v[16 * h + 4 * q + 2],
+                                                     v[16 * h + 4 * q + 3]);
+                        }
+                    }
+                tc_fence_before();
+                mbar_arrive(&tempty_bar[as]);
+            } else if (c_first == c_last) {
                 // sole contributor: epilogue straight from TMEM (hi + lo planes summed)
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
@@ -279,7 +328,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
                         }
-                        if (!(G.dbg & 8)) epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
+                        if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
                     }
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
@@ -325,13 +374,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             }
 #pragma unroll
                             for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));
-                            if (!(G.dbg & 8)) epilogue_chunk<T>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
+                            if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
                         }
                     if (et == 0) G.tile_cnt[tile] = 0;
                     did_epi = true;
                 }
             }
-            if (G.epi.kind == EPI_LMHEAD && did_epi) {
+            if (EPI == EPI_LMHEAD && did_epi) {
                 __threadfence();
                 epi_sync();
                 if (et == 0) flags[1] = (atomicAdd(P.lm_done, 1) == G.tiles - 1);
@@ -344,20 +393,63 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     }
+    if (G.split > 1) {
+        // DSMEM reduce-scatter: rank r finishes the 16-column units u with u % S == r, summing
+        // the S partials in rank order (deterministic), then runs the epilogue on them
+        cluster_sync_all();
+        if (warp < 4) {
+            const int et = threadIdx.x;
+            const int units = NSUB * (Bp / 16);
+            const int tile = blockIdx.x / G.split;
+            const uint32_t base = smem_u32(smem);
+            for (int u = crank; u < units; u += G.split) {
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                const uint32_t off = (uint32_t)(((size_t)u * 128 + et) * 16 * 4);
+                for (int r = 0; r < G.split; ++r) {
+                    const uint32_t a = mapa_shared(base + off, (uint32_t)r);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float4 t4 = ld_dsmem_f4(a + 16u * q);
+                        v[4 * q] += t4.x;
+                        v[4 * q + 1] += t4.y;
+                        v[4 * q + 2] += t4.z;
+                        v[4 * q + 3] += t4.w;
+                    }
+                }
+                const int s = u / (Bp / 16), cb = (u % (Bp / 16)) * 16;
+                if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, threadIdx.x, 16);
+            }
+        }
+        cluster_sync_all();  // peers may still be reading this CTA's partial
+    }
+    if (tr && threadIdx.x == 0) tr[4] = gtimer();  // epilogue warps done
     tc_fence_before();
     __syncthreads();
     if (warp == 5) {
         tc_fence_after();
         tmem_dealloc(tmem_base, G.tmem_cols);
     }
+    if (tr && threadIdx.x == 0) tr[5] = gtimer();
 }
 
-// Host-side selection of the kernel instantiation for a plan.
+// Host-side selection of the kernel instantiation for a plan (split mode is a runtime field).
+template <typename T, int EPI>
+inline const void* gemm_tc_kernel_ptr_k(int nsub, bool merge, int bk) {
+    if (bk == 32) return (const void*)gemm_tc_kernel<T, 1, false, 32, EPI>;
+    if (merge) return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, true, 64, EPI> : (const void*)gemm_tc_kernel<T, 1, true, 64, EPI>;
+    return (const void*)gemm_tc_kernel<T, 1, false, 64, EPI>;
+}
 template <typename T>
-inline const void* gemm_tc_kernel_ptr(int nsub, bool merge, int bk) {
-    if (bk == 32) return (const void*)gemm_tc_kernel<T, 1, false, 32>;
-    if (merge) return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, true, 64> : (const void*)gemm_tc_kernel<T, 1, true, 64>;
-    return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, false, 64> : (const void*)gemm_tc_kernel<T, 1, false, 64>;
+inline const void* gemm_tc_kernel_ptr(int nsub, bool merge, int bk, int epi) {
+    switch (epi) {
+        case EPI_QKV: return gemm_tc_kernel_ptr_k<T, EPI_QKV>(nsub, merge, bk);
+        case EPI_RESID: return gemm_tc_kernel_ptr_k<T, EPI_RESID>(nsub, merge, bk);
+        case EPI_SWIGLU: return gemm_tc_kernel_ptr_k<T, EPI_SWIGLU>(nsub, merge, bk);
+        case EPI_LMHEAD: return gemm_tc_kernel_ptr_k<T, EPI_LMHEAD>(nsub, merge, bk);
+        default: return gemm_tc_kernel_ptr_k<T, EPI_STORE>(nsub, merge, bk);
+    }
 }
 
 }  // namespace cvy

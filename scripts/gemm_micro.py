@@ -12,7 +12,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     print(json.dumps({"N": N, "K": K, "B": B, "us": ms * 1e3, "GBps": N * K * 2 / ms / 1e6}))
     sys.exit(0)
 cases = [(4096, 4096, 64), (6144, 4096, 64), (28672, 4096, 64), (4096, 14336, 64), (32000, 4096, 64)]
-envs = [{}, {"CVY_GEMM_DEBUG": "4"}, {"CVY_GEMM_DEBUG": "1"}]
+envs = [{}, {"CVY_GEMM_DEBUG": "1"}]
 for env in envs:
     for (N, K, B) in cases:
         e = dict(os.environ); e.update(env)
