@@ -53,6 +53,63 @@ CVY_DEV void epilogue_prepare(const StepParams& P, const EpiArgs& E, EpiMeta& m,
     }
 }
 
+// 16-byte vector stores of a run of consecutive rows of one column (16-B aligned targets)
+template <typename T> CVY_DEV void store_row32(T* dst, const float* w);
+template <> CVY_DEV void store_row32<float>(float* dst, const float* w) {
+    float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+template <> CVY_DEV void store_row32<__nv_bfloat16>(__nv_bfloat16* dst, const float* w) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(w[8 * q], w[8 * q + 1]);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(w[8 * q + 2], w[8 * q + 3]);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(w[8 * q + 4], w[8 * q + 5]);
+        __nv_bfloat162 p3 = __floats2bfloat162_rn(w[8 * q + 6], w[8 * q + 7]);
+        d[q] = make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                          *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+    }
+}
+// (hi, lo) activation planes of a run of N consecutive rows (N = 16 or 32)
+template <typename T, int NR> CVY_DEV void store_act_rows(T* dst, size_t plane, const float* w);
+template <> CVY_DEV void store_act_rows<float, 32>(float* dst, size_t, const float* w) { store_row32<float>(dst, w); }
+template <> CVY_DEV void store_act_rows<float, 16>(float* dst, size_t, const float* w) {
+    float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+template <int NR> CVY_DEV void store_act_rows_bf16(__nv_bfloat16* dst, size_t plane, const float* w) {
+    uint32_t hi[NR / 2], lo[NR / 2];
+#pragma unroll
+    for (int r = 0; r < NR; r += 2) {
+        const __nv_bfloat16 h0 = __float2bfloat16_rn(w[r]), h1 = __float2bfloat16_rn(w[r + 1]);
+        const __nv_bfloat16 l0 = __float2bfloat16_rn(w[r] - __bfloat162float(h0));
+        const __nv_bfloat16 l1 = __float2bfloat16_rn(w[r + 1] - __bfloat162float(h1));
+        __nv_bfloat162 ph, pl;
+        ph.x = h0; ph.y = h1;
+        pl.x = l0; pl.y = l1;
+        hi[r / 2] = *reinterpret_cast<uint32_t*>(&ph);
+        lo[r / 2] = *reinterpret_cast<uint32_t*>(&pl);
+    }
+    uint4* dh = reinterpret_cast<uint4*>(dst);
+    uint4* dl = reinterpret_cast<uint4*>(dst + plane);
+#pragma unroll
+    for (int q = 0; q < NR / 8; ++q) {
+        dh[q] = make_uint4(hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
+        dl[q] = make_uint4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
+    }
+}
+template <> CVY_DEV void store_act_rows<__nv_bfloat16, 32>(__nv_bfloat16* dst, size_t plane, const float* w) {
+    store_act_rows_bf16<32>(dst, plane, w);
+}
+template <> CVY_DEV void store_act_rows<__nv_bfloat16, 16>(__nv_bfloat16* dst, size_t plane, const float* w) {
+    store_act_rows_bf16<16>(dst, plane, w);
+}
+template <typename T> CVY_DEV void store_act_row32(T* dst, size_t plane, const float* w) { store_act_rows<T, 32>(dst, plane, w); }
+template <typename T> CVY_DEV void store_act_row16(T* dst, size_t plane, const float* w) { store_act_rows<T, 16>(dst, plane, w); }
+
 // One 32-column chunk of one 128-row sub-tile.  n0 = first global row of the sub-tile.
 template <typename T, int KIND = -1>
 CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int cb, float* v, float* esm,
@@ -67,8 +124,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
             const int dim = n % hd;
             const int j = dim & (half - 1);
             const bool rot = n < qk_rows;
-            // all global inputs first (RoPE cos/sin of every column), then compute, then store:
-            // interleaving loads with stores would serialise them (possible aliasing)
+            // all global inputs first (RoPE cos/sin of every column), then compute, then store
             float2 cs[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i)
@@ -86,49 +142,74 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                 out[i] = dim < half ? (v[i] * cs[i].x - pv * cs[i].y) : (v[i] * cs[i].x + pv * cs[i].y);
             }
             epi_sync();
-            if (n < P.H * hd) {
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (i < ncols) P.q[(size_t)(cb + i) * (P.H * hd) + n] = out[i];
-            } else if (n < E.N) {
-                const int c = n >= qk_rows ? 1 : 0;
-                const int rel = n - P.H * hd - c * P.Hkv * hd;
-                const int g = rel / hd, e = rel % hd;
-                T* kv = reinterpret_cast<T*>(P.kv_pool) + (size_t)E.layer * P.n_pages * (size_t)(2 * P.Hkv * kPageTokens * hd) +
-                        (size_t)(c * P.Hkv + g) * (kPageTokens * hd) + e;
+            for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = out[i];
+            epi_sync();
+            // transposed stores: thread -> (column b, 32 consecutive rows), 16-byte vectors
+            {
+                const int col = et >> 2, part = et & 3;
+                const int r0 = n0 + part * 32;
+                if (col < ncols && r0 < E.N) {
+                    const int b = cb + col;
+                    float w[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const long long off = (i < ncols) ? M.kvoff[cb + i] : -1;
-                    if (off >= 0) kv[off] = DT<T>::from_f(out[i]);
-                }
-            }
-            break;
-        }
-        case EPI_RESID: {
-            T* act = reinterpret_cast<T*>(P.act);
-            const bool valid = n < E.N;
-            const float w = valid ? E.norm_w[n] : 0.f;
-            float xv[32];
+                    for (int r = 0; r < 32; ++r) w[r] = esm[(part * 32 + r) * kEsmLd + col];
+                    if (r0 < P.H * hd) {
+                        float4* dq = reinterpret_cast<float4*>(P.q + (size_t)b * (P.H * hd) + r0);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) xv[i] = (valid && i < ncols) ? P.x[(size_t)(cb + i) * P.d + n] : 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const float xn = xv[i] + v[i];
-                xv[i] = xn;
-                esm[et * kEsmLd + i] = (valid && i < ncols) ? xn * xn : 0.f;
-            }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                if (valid && i < ncols) {
-                    P.x[(size_t)(cb + i) * P.d + n] = xv[i];
-                    DT<T>::store_act(act + (size_t)(cb + i) * P.act_ld + n, (size_t)P.act_plane, xv[i] * w);
+                        for (int q = 0; q < 8; ++q) dq[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+                    } else if (M.kvoff[b] >= 0) {
+                        const int c = r0 >= qk_rows ? 1 : 0;
+                        const int rel = r0 - P.H * hd - c * P.Hkv * hd;
+                        const int g = rel / hd, e = rel % hd;
+                        T* kv = reinterpret_cast<T*>(P.kv_pool) +
+                                (size_t)E.layer * P.n_pages * (size_t)(2 * P.Hkv * kPageTokens * hd) + M.kvoff[b] +
+                                (size_t)(c * P.Hkv + g) * (kPageTokens * hd) + e;
+                        store_row32<T>(kv, w);
+                    }
                 }
             }
             epi_sync();
-            if (et < 32 && et < ncols) {
-                float acc = 0.f;
-                for (int r = 0; r < 128; ++r) acc += esm[r * kEsmLd + et];
-                if (n0 < E.N) P.ssq[(size_t)(n0 / 128) * P.Bmax + cb + et] = acc;
+            break;
+        }
+        case EPI_RESID: {
+            // v: this thread's row (n0 + et) for 32 columns -> esm; then thread -> (column b,
+            // 32 consecutive rows): x += v, act = x * w_norm (hi, lo), sum of squares
+#pragma unroll
+            for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = v[i];
+            epi_sync();
+            {
+                const int col = et >> 2, part = et & 3;
+                const int r0 = n0 + part * 32;
+                const bool ok = col < ncols && r0 < E.N;
+                const int b = cb + col;
+                float ss = 0.f;
+                if (ok) {
+                    float xv[32], wn[32];
+                    const float4* xs = reinterpret_cast<const float4*>(P.x + (size_t)b * P.d + r0);
+                    const float4* ws = reinterpret_cast<const float4*>(E.norm_w + r0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 a = xs[q], w4 = __ldg(ws + q);
+                        xv[4 * q] = a.x; xv[4 * q + 1] = a.y; xv[4 * q + 2] = a.z; xv[4 * q + 3] = a.w;
+                        wn[4 * q] = w4.x; wn[4 * q + 1] = w4.y; wn[4 * q + 2] = w4.z; wn[4 * q + 3] = w4.w;
+                    }
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) {
+                        xv[r] += esm[(part * 32 + r) * kEsmLd + col];
+                        ss += xv[r] * xv[r];
+                    }
+                    float4* xd = reinterpret_cast<float4*>(P.x + (size_t)b * P.d + r0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) xd[q] = make_float4(xv[4 * q], xv[4 * q + 1], xv[4 * q + 2], xv[4 * q + 3]);
+#pragma unroll
+                    for (int r = 0; r < 32; ++r) wn[r] *= xv[r];
+                    store_act_row32<T>(reinterpret_cast<T*>(P.act) + (size_t)b * P.act_ld + r0, (size_t)P.act_plane, wn);
+                }
+                // the 4 threads of a column are lanes 4c..4c+3 of one warp
+                ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+                ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+                if (ok && part == 0) P.ssq[(size_t)(n0 / 128) * P.Bmax + b] = ss;
             }
             epi_sync();
             break;
@@ -138,16 +219,19 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
 #pragma unroll
             for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = v[i] * s_scale[cb + i];
             epi_sync();
-            if (et < 64) {
-                T* hb = reinterpret_cast<T*>(P.h);
-                const int j = (n0 / 128) * 64 + et;
-                if (j < P.dff) {
-                    for (int i = 0; i < ncols; ++i) {
-                        float g = esm[et * kEsmLd + i];
-                        float u = esm[(et + 64) * kEsmLd + i];
-                        float a = g / (1.f + __expf(-g)) * u;
-                        DT<T>::store_act(hb + (size_t)(cb + i) * P.act_ld + j, (size_t)P.act_plane, a);
+            {
+                const int col = et >> 2, part = et & 3;   // part -> 16 consecutive j
+                const int j0 = (n0 / 128) * 64 + part * 16;
+                if (col < ncols && j0 < P.dff) {
+                    float a[16];
+#pragma unroll
+                    for (int r = 0; r < 16; ++r) {
+                        const float g = esm[(part * 16 + r) * kEsmLd + col];
+                        const float u = esm[(64 + part * 16 + r) * kEsmLd + col];
+                        a[r] = g / (1.f + __expf(-g)) * u;
                     }
+                    store_act_row16<T>(reinterpret_cast<T*>(P.h) + (size_t)(cb + col) * P.act_ld + j0,
+                                       (size_t)P.act_plane, a);
                 }
             }
             epi_sync();

@@ -259,7 +259,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int et = threadIdx.x;  // 0..127 == TMEM lane == tile row
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         const int rows = NSUB * 128;
-        const int first_tile = (int)(it0 / G.kblocks);
         bool prepared = false;
         int as = 0;
         uint32_t aphase = 0;
