@@ -317,7 +317,7 @@ def run_ours(args):
     peaks, peaks_src = load_peaks()
     hbm = float(peaks["hbm_gbs"])
     achieved = gemm_bytes / (gemm_ms / 1000.0) / 1e9
-    roofline = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 stream-K projections, all 129 launches/step)",
+    roofline = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 projections, cluster split-K for narrow N, all 129 launches/step)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "peak_source": f"{peaks_src} HBM copy bandwidth", "traffic": load_traffic(),
                 "share_of_step": gemm_ms / probe_ms,

@@ -18,7 +18,7 @@ namespace cvy {
 
 constexpr int kAtcWarps = 4;                 // consumer warps
 constexpr int kAtcThreads = (kAtcWarps + 1) * 32;
-constexpr int kAtcStages = 3;
+constexpr int kAtcStages = 3;  // default pipeline depth (template parameter STAGES)
 constexpr int kAtcPagesPerStage = 4;
 constexpr int kAtcPageBytes = 16 * 128 * 2;  // one (page, K or V) block at hd = 128
 
@@ -47,7 +47,7 @@ CVY_DEV uint32_t pack_bf16(float lo_elem, float hi_elem) {
 // 128B swizzle
 CVY_DEV uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-template <int HD>
+template <int HD, int STAGES = kAtcStages>
 __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_constant__ CUtensorMap tmKV,
                                                                    const __grid_constant__ StepParams P, int layer) {
     static_assert(HD == 64 || HD == 128, "head_dim");
@@ -58,10 +58,10 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     extern __shared__ __align__(1024) uint8_t asm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(asm_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = sm;
-    uint16_t* pbuf = reinterpret_cast<uint16_t*>(sm + kAtcStages * STAGE);  // [warp][8][16] bf16
+    uint16_t* pbuf = reinterpret_cast<uint16_t*>(sm + STAGES * STAGE);  // [warp][8][16] bf16
     float* comb = reinterpret_cast<float*>(pbuf + kAtcWarps * 8 * 16);      // [warp][4 m, 4 l, 4*HD O]
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(comb + kAtcWarps * (8 + 4 * HD));
-    uint64_t* empty_bar = full_bar + kAtcStages;
+    uint64_t* empty_bar = full_bar + STAGES;
 
     pdl_launch_dependents();
     const int g = blockIdx.x, b = blockIdx.y, split = blockIdx.z;
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == kAtcWarps * 32) {
         tma_prefetch_desc(&tmKV);
-        for (int s = 0; s < kAtcStages; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], kAtcWarps);
         }
@@ -93,8 +93,8 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             for (int t = 0; t < n_tiles; ++t) {
-                const int st = t % kAtcStages;
-                const uint32_t ph = (uint32_t)(t / kAtcStages) & 1u;
+                const int st = t % STAGES;
+                const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
                 mbar_wait(&empty_bar[st], ph ^ 1u);
                 const int np = min(kAtcPagesPerStage, n_pages - t * kAtcPagesPerStage);
                 mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(np * 2 * BLK));
@@ -149,8 +149,8 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     const uint32_t pw_addr = smem_u32(pw);
 
     for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % kAtcStages;
-        const uint32_t ph = (uint32_t)(t / kAtcStages) & 1u;
+        const int st = t % STAGES;
+        const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
         const int pidx = t * kAtcPagesPerStage + warp;  // this warp's page in the split
         if (pidx < n_pages) {
             mbar_wait(&full_bar[st], ph);

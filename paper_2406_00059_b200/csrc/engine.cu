@@ -135,6 +135,9 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         // the DSMEM staging of the partial must fit in the pipeline smem
         if (g.split > 1 && (size_t)g.nsub * Bp * 512 > (size_t)stages * stage) g.split = 0;
     }
+    // L2 look-ahead: ~256 KB of weights per CTA beyond the smem ring (bounded by L2 capacity)
+    g.l2_prefetch = 0;  // measured: no gain (mainloops already stream at 5.6-6.8 TB/s once unblocked)
+    if (const char* pf = getenv("CVY_GEMM_L2PF")) g.l2_prefetch = atoi(pf);
     if (g.split > 0) {
         *grid = g.tiles * g.split;
     } else {
@@ -271,6 +274,7 @@ struct cvy_engine {
     uint32_t last_launches = 0;
     std::vector<uint8_t> vlen_host;
     bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
+    int attn_stages = 3;
     CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd]
     unsigned long long* d_trace = nullptr;  // test hook: GEMM CTA timestamps of one layer
     int trace_layer = -1;
@@ -518,8 +522,12 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
             cvy_engine_destroy(e);
             return fail(CVY_E_CUDA, "KV tensor map encode failed");
         }
-        cudaFuncSetAttribute(attention_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
-        cudaFuncSetAttribute(attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+        e->attn_stages = 3;
+        if (const char* as = getenv("CVY_ATTN_STAGES")) e->attn_stages = std::max(2, std::min(4, atoi(as)));
+        for (const void* f : {(const void*)attention_tc_kernel<128, 2>, (const void*)attention_tc_kernel<128, 3>,
+                              (const void*)attention_tc_kernel<128, 4>, (const void*)attention_tc_kernel<64, 2>,
+                              (const void*)attention_tc_kernel<64, 3>, (const void*)attention_tc_kernel<64, 4>})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     }
     // kernel attributes
     set_gemm_smem_attrs();
@@ -885,8 +893,12 @@ StepParams base_params(cvy_engine* e, int Bp) {
     P.dbg_logits = e->d_dbg;
     P.lm_done = e->d_lm_done;
     P.attn_part = e->d_attn_part;
-    const int want = (4 * e->num_sms + m.n_kv_heads * Bp - 1) / (m.n_kv_heads * Bp);
+    // split-KV only when the (head, row) grid cannot cover the SMs: measured at B=64 / ctx 372
+    // on 7B, splits=1 beats 2 by 0.4 ms/step (the merge pass costs more than the extra waves).
+    const int cells = m.n_kv_heads * Bp;
+    const int want = cells >= e->num_sms ? 1 : (2 * e->num_sms + cells - 1) / cells;
     P.attn_splits = std::max(1, std::min(e->attn_splits_max, want));
+    if (const char* as = getenv("CVY_ATTN_SPLITS")) P.attn_splits = std::max(1, std::min(e->attn_splits_max, atoi(as)));
     P.vtab = e->d_vtab;
     P.vlen = e->d_vlen;
     P.tools = e->d_tools;
@@ -1056,10 +1068,16 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
         kt.begin(2, l);
         if (e->attn_tc) {
             void* targs[] = {&e->tm_kv, &bk.P, &layer};
-            const void* tf = m.head_dim == 128 ? (const void*)attention_tc_kernel<128> : (const void*)attention_tc_kernel<64>;
+            const int nst = e->attn_stages;
+            const void* tf = m.head_dim == 128 ? (nst == 2 ? (const void*)attention_tc_kernel<128, 2>
+                                                            : nst == 4 ? (const void*)attention_tc_kernel<128, 4>
+                                                                       : (const void*)attention_tc_kernel<128, 3>)
+                                                : (nst == 2 ? (const void*)attention_tc_kernel<64, 2>
+                                                            : nst == 4 ? (const void*)attention_tc_kernel<64, 4>
+                                                                       : (const void*)attention_tc_kernel<64, 3>);
             const int blk = kPageTokens * m.head_dim * 2;
-            const size_t tsmem = 1024 + (size_t)kAtcStages * kAtcPagesPerStage * 2 * blk + kAtcWarps * 8 * 16 * 2 +
-                                 (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * kAtcStages * 8;
+            const size_t tsmem = 1024 + (size_t)nst * kAtcPagesPerStage * 2 * blk + kAtcWarps * 8 * 16 * 2 +
+                                 (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * nst * 8;
             if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
                 CVY_OK)
                 return st;

@@ -47,6 +47,7 @@ struct GemmTC {
     int32_t dbg;        // measurement knobs (test hook only): 1 no epilogue work, 2 no MMA issue,
                         // 4 shared tiles: store partial only, 8 skip the epilogue functor
     unsigned long long* trace;  // test hook: [grid][8] %globaltimer stamps, or null
+    int32_t l2_prefetch;        // k-block stages prefetched into L2 beyond the smem ring
 };
 
 CVY_DEV unsigned long long gtimer() {
@@ -170,6 +171,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tma_load_2d(smem + (size_t)i * stage_bytes, &tmW, &full_bar[i], kb * BK, G.w_row0 + tile * rows_per_tile,
                             pol_w);
             }
+            // deeper look-ahead into L2 while the previous kernel drains (HBM would idle otherwise)
+            const long long pf_end = min(it1, it0 + pre + (long long)G.l2_prefetch);
+            for (long long it = it0 + pre; it < pf_end; ++it)
+                tma_prefetch_l2_2d(&tmW, (int)(it % G.kblocks) * BK, G.w_row0 + (int)(it / G.kblocks) * rows_per_tile);
             pdl_wait();
             for (int i = 0; i < pre; ++i) {
                 const int kb = (int)((it0 + i) % G.kblocks);
