@@ -317,9 +317,14 @@ def run_ours(args):
     peaks, peaks_src = load_peaks()
     hbm = float(peaks["hbm_gbs"])
     achieved = gemm_bytes / (gemm_ms / 1000.0) / 1e9
+    traffic = load_traffic()
     roofline = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 projections, cluster split-K for narrow N, all 129 launches/step)",
                 "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "peak_source": f"{peaks_src} HBM copy bandwidth", "traffic": load_traffic(),
+                "peak_source": f"{peaks_src} HBM copy bandwidth",
+                "traffic": (traffic or {}).get("per_launch_bytes"),
+                "traffic_detail": None if traffic is None else {
+                    "alg_per_launch_bytes": traffic["alg_per_launch_bytes"], "ratio": traffic["ratio"],
+                    "source": "profiles/gemm_traffic.json: " + traffic["source"]},
                 "share_of_step": gemm_ms / probe_ms,
                 "attention": {"achieved": kv_bytes / (attn_ms / 1000.0) / 1e9, "frac": kv_bytes / (attn_ms / 1000.0) / 1e9 / hbm,
                               "ms_per_step": attn_ms},

@@ -130,7 +130,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         int S = 1;
         // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
         while (allow_kernel_split && S < 4 && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
-        if (S == 3) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
+        if (S == 3 && !getenv("CVY_GEMM_ALLOW_S3")) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
         if (g.tiles <= num_sms) g.split = S;
         // the DSMEM staging of the partial must fit in the pipeline smem
         if (g.split > 1 && (size_t)g.nsub * Bp * 512 > (size_t)stages * stage) g.split = 0;
@@ -177,6 +177,7 @@ struct Upload {
 
 struct GemmPlan {
     CUtensorMap tmW, tmX;
+    CUtensorMap tmN;  // weights of the next GEMM in the step (L2 prefetch in the epilogue tail)
     GemmTC g;
     int grid;
     size_t smem;
@@ -509,11 +510,11 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     for (int p = (int)ec->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
     if (const char* tl = getenv("CVY_GEMM_TRACE_LAYER")) {
         e->trace_layer = atoi(tl);
-        if (cudaMalloc(&e->d_trace, sizeof(unsigned long long) * 8 * 4 * e->num_sms) != cudaSuccess) {
+        if (cudaMalloc(&e->d_trace, sizeof(unsigned long long) * kTraceStride * 4 * e->num_sms) != cudaSuccess) {
             cvy_engine_destroy(e);
             return fail(CVY_E_NOMEM, "trace buffer");
         }
-        cudaMemset(e->d_trace, 0, sizeof(unsigned long long) * 8 * 4 * e->num_sms);
+        cudaMemset(e->d_trace, 0, sizeof(unsigned long long) * kTraceStride * 4 * e->num_sms);
     }
     e->attn_tc = e->bf16 && (hd == 64 || hd == 128) && (H / Hkv) <= 4;
     if (e->attn_tc) {
@@ -935,7 +936,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         g.w_row0 = layer * N;
         if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD) {
             const int k = epi.kind == EPI_QKV ? 0 : epi.kind == EPI_SWIGLU ? 2 : (K == ::m_d(e) ? 1 : 3);
-            g.trace = e->d_trace + (size_t)k * 8 * e->num_sms;
+            g.trace = e->d_trace + (size_t)k * kTraceStride * e->num_sms;
         }
         g.part = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
@@ -997,6 +998,27 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
         if (!plan_gemm(e, bk, e->w.lm_head, V, d, 0, V, e->d_act, el, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
     }
+    // cross-kernel weight prefetch: GEMM i warms L2 with the first k-blocks of GEMM i+1 (the LM
+    // head warms the next step's layer-0 QKV) while its own epilogue drains
+    if (e->bf16) {
+        int pf_kb = 0;  // measured at B=64: 128 KB -1%, 256 KB -2% (the prefetch competes, nothing idles)
+        if (const char* pk = getenv("CVY_GEMM_PF_KB")) pf_kb = atoi(pk);
+        const size_t n = bk.plans.size();
+        for (size_t i = 0; i < n; ++i) {
+            GemmPlan& a = bk.plans[i];
+            const GemmPlan& b = bk.plans[(i + 1) % n];
+            GemmNext& nx = a.g.nx;
+            nx.tiles = b.g.tiles;
+            nx.kblocks = b.g.kblocks;
+            nx.split = b.g.split;
+            nx.rows_per_tile = 128 * b.g.nsub;
+            nx.w_row0 = b.g.w_row0;
+            nx.grid = b.grid;
+            nx.bk = b.g.bk;
+            nx.blocks = std::max(0, pf_kb * 1024 / (nx.rows_per_tile * nx.bk * 2));
+            a.tmN = b.tmW;
+        }
+    }
     auto res = e->buckets.emplace(Bp, std::move(bk));
     *out = &res.first->second;
     return CVY_OK;
@@ -1004,7 +1026,7 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
 
 cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
     if (e->bf16) {
-        void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g};
+        void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g, &gp.tmN};
         return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind), dim3(gp.grid),
                         dim3(kGemmThreads), gp.smem, args, true, gp.g.split > 1 ? gp.g.split : 1);
     }
@@ -1384,8 +1406,8 @@ cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap,
         case 5: src = e->d_ssq; n = (size_t)(e->m.d_model / 128) * B * 4; break;
         case 10: case 11: case 12: case 13:
             if (!e->d_trace) return fail(CVY_E_STATE, "set CVY_GEMM_TRACE_LAYER before engine create");
-            src = e->d_trace + (size_t)(which - 10) * 8 * e->num_sms;
-            n = sizeof(unsigned long long) * 8 * e->num_sms;
+            src = e->d_trace + (size_t)(which - 10) * kTraceStride * e->num_sms;
+            n = sizeof(unsigned long long) * kTraceStride * e->num_sms;
             break;
         default: return fail(CVY_E_INVAL, "unknown buffer");
     }
@@ -1565,7 +1587,7 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
         !make_tmap(&tmX, Xp, (uint64_t)(2 * Bp), (uint64_t)K, (uint64_t)K, xrows, (uint32_t)g.bk))
         return fail(CVY_E_CUDA, "tensor map encode failed");
     const void* kfn = gemm_tc_kernel_ptr<__nv_bfloat16>(g.nsub, g.merge != 0, g.bk, EPI_STORE);
-    void* args[] = {&tmW, &tmX, &P, &g};
+    void* args[] = {&tmW, &tmX, &P, &g, &tmW};
     cudaLaunchConfig_t lc;
     std::memset(&lc, 0, sizeof(lc));
     lc.gridDim = dim3(grid);
@@ -1594,23 +1616,23 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     if (getenv("CVY_GEMM_TRACE")) {
         // one traced launch: per-CTA globaltimer stamps relative to the earliest CTA start
         unsigned long long* tr = nullptr;
-        CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * grid));
-        CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * grid));
+        CUDA_TRY(cudaMalloc(&tr, sizeof(unsigned long long) * kTraceStride * grid));
+        CUDA_TRY(cudaMemset(tr, 0, sizeof(unsigned long long) * kTraceStride * grid));
         g.trace = tr;
-        void* targs[] = {&tmW, &tmX, &P, &g};
+        void* targs[] = {&tmW, &tmX, &P, &g, &tmW};
         CUDA_TRY(cudaLaunchKernelExC(&lc, kfn, targs));
         CUDA_TRY(cudaDeviceSynchronize());
-        std::vector<unsigned long long> h(8 * (size_t)grid);
+        std::vector<unsigned long long> h(kTraceStride * (size_t)grid);
         CUDA_TRY(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
         cudaFree(tr);
         g.trace = nullptr;
         unsigned long long t0 = ~0ull;
-        for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[8 * c]);
+        for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[kTraceStride * c]);
         double mx[6] = {0}, mn[6], sum[6] = {0};
         for (int k = 0; k < 6; ++k) mn[k] = 1e30;
         for (int c = 0; c < grid; ++c)
             for (int k = 0; k < 6; ++k) {
-                double v = h[8 * c + k] ? (h[8 * c + k] - t0) * 1e-3 : -1;
+                double v = h[kTraceStride * c + k] ? (h[kTraceStride * c + k] - t0) * 1e-3 : -1;
                 mx[k] = std::max(mx[k], v);
                 mn[k] = std::min(mn[k], v);
                 sum[k] += v;

@@ -23,6 +23,13 @@
 
 namespace cvy {
 
+// Geometry of the GEMM launched after this one (its weight stream is prefetched into L2 during
+// this kernel's epilogue tail, when HBM would otherwise idle).
+struct GemmNext {
+    int32_t tiles, kblocks, split, rows_per_tile, w_row0, grid, bk;
+    int32_t blocks;  // k-blocks prefetched per next-kernel CTA (0: off)
+};
+
 struct GemmTC {
     int32_t N;          // weight rows of this GEMM (one layer)
     int32_t K;
@@ -46,8 +53,9 @@ struct GemmTC {
     EpiArgs epi;
     int32_t dbg;        // measurement knobs (test hook only): 1 no epilogue work, 2 no MMA issue,
                         // 4 shared tiles: store partial only, 8 skip the epilogue functor
-    unsigned long long* trace;  // test hook: [grid][8] %globaltimer stamps, or null
+    unsigned long long* trace;  // test hook: [grid][kTraceStride] %globaltimer stamps, or null
     int32_t l2_prefetch;        // k-block stages prefetched into L2 beyond the smem ring
+    GemmNext nx;                // next GEMM of the step (prefetched through tmN)
 };
 
 CVY_DEV unsigned long long gtimer() {
@@ -57,6 +65,7 @@ CVY_DEV unsigned long long gtimer() {
 }
 
 constexpr int kGemmThreads = 192;
+constexpr int kTraceStride = 16;
 
 // shared-memory carve-up (host and device agree); rows are bk*2 bytes (one swizzle atom)
 struct GemmSmem {
@@ -73,6 +82,31 @@ struct GemmSmem {
                + 64u;                   // tmem addr + flags
     }
 };
+
+// Issue L2 prefetches of the next GEMM's first k-blocks (the ones its CTAs load first),
+// spread over the 32 lanes of one warp; this CTA covers next-kernel CTAs blockIdx.x + j*grid.
+CVY_DEV void prefetch_next_gemm(const GemmTC& G, const CUtensorMap* tmN, int lane) {
+    const GemmNext& nx = G.nx;
+    if (nx.blocks <= 0) return;
+    if (lane == 0) tma_prefetch_desc(tmN);
+    int j = 0;
+    for (int c = blockIdx.x; c < nx.grid; c += gridDim.x) {
+        long long a0, a1;
+        if (nx.split > 0) {
+            const int t = c / nx.split, r = c % nx.split;
+            a0 = (long long)t * nx.kblocks + ((long long)r * nx.kblocks) / nx.split;
+            a1 = (long long)t * nx.kblocks + ((long long)(r + 1) * nx.kblocks) / nx.split;
+        } else {
+            const long long T = (long long)nx.tiles * nx.kblocks;
+            a0 = ((long long)c * T) / nx.grid;
+            a1 = ((long long)(c + 1) * T) / nx.grid;
+        }
+        a1 = min(a1, a0 + (long long)nx.blocks);
+        for (long long i = a0; i < a1; ++i, ++j)
+            if ((j & 31) == lane)
+                tma_prefetch_l2_2d(tmN, (int)(i % nx.kblocks) * nx.bk, nx.w_row0 + (int)(i / nx.kblocks) * nx.rows_per_tile);
+    }
+}
 
 CVY_DEV int cta_of_iter(long long i, long long T, int G) {
     long long c = (i * G) / T;
@@ -92,7 +126,8 @@ CVY_DEV uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(by
 template <typename T, int NSUB, bool MERGE, int BK, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                   const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G) {
+                   const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G,
+                   const __grid_constant__ CUtensorMap tmN) {
     constexpr uint32_t ROW = BK * 2;                  // bytes per smem row
     constexpr uint32_t WB = NSUB * 128u * ROW;        // weight bytes per stage
     constexpr int KSTEPS = BK / 16;
@@ -149,7 +184,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
-    unsigned long long* tr = G.trace ? G.trace + (size_t)blockIdx.x * 8 : nullptr;
+    unsigned long long* tr = G.trace ? G.trace + (size_t)blockIdx.x * kTraceStride : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (warp == 4) {
@@ -203,6 +238,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
             if (tr) tr[1] = gtimer();
         }
+        // non-split: warm L2 with the next GEMM's first k-blocks right behind our own stream
+        __syncwarp();
+        if (G.split <= 1) prefetch_next_gemm(G, &tmN, lane);
     } else if (warp == 5) {
         // ===================== MMA issuer =====================
         const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)G.mma_n);
@@ -310,12 +348,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         }
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
-                            float4* dst = reinterpret_cast<float4*>(
-                                stagep + ((size_t)(s * (Bp / 16) + cb / 16 + h) * 128 + et) * 16);
+                            // [unit][q][row][4]: a warp's float4 stores (and the peers' loads)
+                            // cover 512 contiguous bytes -- no bank conflicts
+                            float4* dst = reinterpret_cast<float4*>(stagep) +
+                                          (size_t)(s * (Bp / 16) + cb / 16 + h) * 512 + et;
 #pragma unroll
                             for (int q = 0; q < 4; ++q)
-                                dst[q] = make_float4(v[16 * h + 4 * q], v[16 * h + 4 * q + 1], v[16 * h + 4 * q + 2],
-                                                     v[16 * h + 4 * q + 3]);
+                                dst[q * 128] = make_float4(v[16 * h + 4 * q], v[16 * h + 4 * q + 1], v[16 * h + 4 * q + 2],
+                                                           v[16 * h + 4 * q + 3]);
                         }
                     }
                 tc_fence_before();
@@ -401,6 +441,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // DSMEM reduce-scatter: rank r finishes the 16-column units u with u % S == r, summing
         // the S partials in rank order (deterministic), then runs the epilogue on them
         cluster_sync_all();
+        if (tr && threadIdx.x == 0) tr[6] = gtimer();  // partials staged cluster-wide
+        if (warp == 4) prefetch_next_gemm(G, &tmN, lane);  // overlaps the reduce below
         if (warp < 4) {
             const int et = threadIdx.x;
             const int units = NSUB * (Bp / 16);
@@ -410,22 +452,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = 0.f;
-                const uint32_t off = (uint32_t)(((size_t)u * 128 + et) * 16 * 4);
-                for (int r = 0; r < G.split; ++r) {
-                    const uint32_t a = mapa_shared(base + off, (uint32_t)r);
+                const uint32_t off = (uint32_t)(((size_t)u * 512 + et) * 16);
+                // all S*4 remote loads in flight at once (DSMEM round trips are ~200 cycles),
+                // then the sum in rank order
+                float4 t4[4][4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const float4 t4 = ld_dsmem_f4(a + 16u * q);
-                        v[4 * q] += t4.x;
-                        v[4 * q + 1] += t4.y;
-                        v[4 * q + 2] += t4.z;
-                        v[4 * q + 3] += t4.w;
+                for (int r = 0; r < 4; ++r)
+                    if (r < G.split) {
+                        const uint32_t a = mapa_shared(base + off, (uint32_t)r);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) t4[r][q] = ld_dsmem_f4(a + 2048u * q);
                     }
-                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    if (r < G.split) {
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            v[4 * q] += t4[r][q].x;
+                            v[4 * q + 1] += t4[r][q].y;
+                            v[4 * q + 2] += t4[r][q].z;
+                            v[4 * q + 3] += t4[r][q].w;
+                        }
+                    }
                 const int s = u / (Bp / 16), cb = (u % (Bp / 16)) * 16;
+                if (tr && et == 0 && u == crank) tr[8] = gtimer();
                 if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, threadIdx.x, 16);
+                if (tr && et == 0 && u == crank) tr[9] = gtimer();
             }
         }
+        if (tr && threadIdx.x == 0) tr[7] = gtimer();  // own units reduced + epilogued
         cluster_sync_all();  // peers may still be reading this CTA's partial
     }
     if (tr && threadIdx.x == 0) tr[4] = gtimer();  // epilogue warps done

@@ -20,7 +20,7 @@ for _ in range(8):
     eng.step()
 eng.sync()
 names = ["QKV", "O", "GU", "D"]
-tr = [np.frombuffer(eng.debug_buffer(10 + k), dtype=np.uint64).reshape(-1, 8).astype(np.float64) for k in range(4)]
+tr = [np.frombuffer(eng.debug_buffer(10 + k), dtype=np.uint64).reshape(-1, 16).astype(np.float64) for k in range(4)]
 t0 = min(t[:, 0][t[:, 0] > 0].min() for t in tr)
 prev_end = None
 for k in range(4):
@@ -30,6 +30,13 @@ for k in range(4):
     print(f"{names[k]:3s} CTAs {v.sum():3d}: start {st.min():8.2f}..{st.max():8.2f}  producer done avg {pd.mean():8.2f}  "
           f"last MMA avg {lm.mean():8.2f} max {lm.max():8.2f}  epi done avg {ep.mean():8.2f} max {ep.max():8.2f}  exit max {ex.max():8.2f} us"
           + (f"  gap from prev exit {st.min() - prev_end:6.2f}" if prev_end is not None else ""))
+    if (t[v, 6] > 0).all():
+        cs, rd = [(t[v, i] - t0) / 1e3 for i in (6, 7)]
+        print(f"      split-K: staged+cluster_sync avg {cs.mean():8.2f} max {cs.max():8.2f}  reduce+epi avg {rd.mean():8.2f} "
+              f"max {rd.max():8.2f}  (last MMA -> sync {(cs - lm).mean():5.2f}, reduce+epi {(rd - cs).mean():5.2f}, "
+              f"final sync {(ep - rd).mean():5.2f})")
+        d0, d1 = [(t[v, i] - t0) / 1e3 for i in (8, 9)]
+        print(f"      first unit: dsmem loads {(d0 - cs).mean():5.2f}  epilogue_chunk {(d1 - d0).mean():5.2f}  us")
     prev_end = ex.max()
 eng.poll_segments()
 eng.close()
