@@ -88,7 +88,9 @@ enum {
     CVY_ENGINE_NO_GRAPH = 1,     /* launch kernels directly instead of a CUDA graph          */
     CVY_ENGINE_DEBUG_LOGITS = 2, /* keep the last step's fp32 logits for cvy_debug_logits   */
     CVY_ENGINE_SCAN_OFF = 4,     /* trigger scan disabled for every slot (overhead A/B)      */
-    CVY_ENGINE_NO_PDL = 8        /* no programmatic dependent launch between kernels        */
+    CVY_ENGINE_NO_PDL = 8,       /* no programmatic dependent launch between kernels        */
+    CVY_ENGINE_NO_PERSISTENT = 16 /* one kernel per GEMM / attention instead of the
+                                     persistent all-layers kernel (A/B and parity)          */
 };
 
 typedef struct {
@@ -255,7 +257,8 @@ cvy_status cvy_perf(cvy_engine* e, cvy_perf_info* out);
  * launch disabled in that variant); cvy_kernel_times then returns the device time of each
  * launch of the most recently completed timed step, in launch order.
  * kind: 0 embed, 1 QKV GEMM, 2 attention, 3 attention merge, 4 O GEMM, 5 gate/up GEMM,
- *       6 down GEMM, 7 LM-head GEMM + sampling/scan epilogue. */
+ *       6 down GEMM, 7 LM-head GEMM + sampling/scan epilogue, 8 persistent all-layers kernel
+ *       (QKV, attention, O, gate/up and down of every layer in one launch), 9 its counter reset. */
 typedef struct {
     int32_t kind, layer;
     float ms;

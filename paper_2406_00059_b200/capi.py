@@ -19,7 +19,7 @@ MODE_PARTIAL, MODE_SEQUENTIAL = 0, 1
 SEG_FINAL, SEG_OVERFLOW, SEG_CANCELLED = 1, 2, 4
 DELIM_NONE = 0xFFFF
 NO_TOKEN = 0xFFFFFFFF
-ENGINE_NO_GRAPH, ENGINE_DEBUG_LOGITS, ENGINE_SCAN_OFF, ENGINE_NO_PDL = 1, 2, 4, 8
+ENGINE_NO_GRAPH, ENGINE_DEBUG_LOGITS, ENGINE_SCAN_OFF, ENGINE_NO_PDL, ENGINE_NO_PERSISTENT = 1, 2, 4, 8, 16
 
 c_i32, c_u32, c_u64, c_u16, c_f32, c_f64, c_sz, c_vp = (ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
                                                          ctypes.c_uint16, ctypes.c_float, ctypes.c_double,
@@ -77,7 +77,7 @@ class KernelTime(ctypes.Structure):
 
 
 KERNEL_KINDS = {0: "embed", 1: "gemm_qkv", 2: "attention", 3: "attention_merge", 4: "gemm_o", 5: "gemm_gate_up",
-                6: "gemm_down", 7: "gemm_lm_head+sample_scan"}
+                6: "gemm_down", 7: "gemm_lm_head+sample_scan", 8: "layers_persistent", 9: "persistent_reset"}
 
 
 class PerfInfo(ctypes.Structure):

@@ -30,11 +30,11 @@ def make_engine(shape, dtype, vocab, max_slots, seed, n_pages=None, flags=capi.E
 
 
 def free_running_parity(shape, dtype, vocab, prompts, max_new, seed, tol, prefix=0, synth_seeds=None,
-                        max_pages_per_slot=64, graph=True):
+                        max_pages_per_slot=64, graph=True, extra_flags=0):
     """Submit every prompt, step until all rounds end, and compare every step's GPU logits
     (cvy_debug_logits) with the oracle fed the same input tokens.  Returns (max_abs_diff,
     generated token lists)."""
-    flags = capi.ENGINE_DEBUG_LOGITS | (0 if graph else capi.ENGINE_NO_GRAPH)
+    flags = capi.ENGINE_DEBUG_LOGITS | (0 if graph else capi.ENGINE_NO_GRAPH) | extra_flags
     dm, eng = make_engine(shape, dtype, vocab, len(prompts), seed, flags=flags,
                           max_pages_per_slot=max_pages_per_slot)
     bf16 = dtype == "bf16"

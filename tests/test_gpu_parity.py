@@ -66,20 +66,28 @@ def test_tiny_fp32_with_synthetic_prefix():
 
 
 # ------------------------------------------------------------------ 7B shape
-def test_7b_two_layer_slice_bf16():
+@pytest.mark.parametrize("persistent", [True, False])
+def test_7b_two_layer_slice_bf16(persistent, monkeypatch):
+    """2-layer 7B slice through the persistent all-layers kernel (CVY_PERSISTENT=1) and through
+    the one-kernel-per-op path (CVY_ENGINE_NO_PERSISTENT)."""
+    monkeypatch.setenv("CVY_PERSISTENT", "1")
     shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
     vocab = synthetic_vocab(32000)
     prompts = [[1, 300, 5000], [1, 77], [1, 31999, 2000, 12]]
     d, _ = free_running_parity(shape, "bf16", vocab, prompts, max_new=3, seed=1003, tol=2e-2, prefix=40,
-                               synth_seeds=[11, 12, 13])
+                               synth_seeds=[11, 12, 13],
+                               extra_flags=0 if persistent else capi.ENGINE_NO_PERSISTENT)
     assert d < 2e-2
 
 
-@pytest.mark.parametrize("H,Hkv,hd,prefix", [(8, 2, 64, 90), (4, 2, 128, 230), (4, 4, 128, 17), (8, 8, 64, 300)])
-def test_tensor_core_attention_shapes(H, Hkv, hd, prefix):
+@pytest.mark.parametrize("H,Hkv,hd,prefix", [(8, 2, 64, 90), (4, 2, 128, 230), (4, 4, 128, 17), (8, 8, 64, 300),
+                                             (8, 2, 128, 500)])
+@pytest.mark.parametrize("persistent", ["1", "0"])
+def test_tensor_core_attention_shapes(H, Hkv, hd, prefix, persistent, monkeypatch):
     """The TMA + mma.sync attention kernel across head_dim 64/128 and GQA groups 1, 2, 4,
     contexts spanning several 4-page pipeline stages and split-KV partitions."""
     from inputs.configs import ModelShape
+    monkeypatch.setenv("CVY_PERSISTENT", persistent)
     shape = ModelShape(f"att-{H}-{Hkv}-{hd}", L=2, d=512, H=H, Hkv=Hkv, hd=hd, dff=1024, V=512, eps=1e-5,
                        rope_base=1e4, eos=-1)
     vocab = [bytes([i % 256]) * (1 + i // 256) for i in range(512)]
@@ -87,6 +95,38 @@ def test_tensor_core_attention_shapes(H, Hkv, hd, prefix):
     d, _ = free_running_parity(shape, "bf16", vocab, prompts, max_new=4, seed=1013, tol=2e-2, prefix=prefix,
                                synth_seeds=[21, 22, 23])
     assert d < 2e-3
+
+
+@pytest.mark.parametrize("persistent", ["1", "0"])
+def test_7b_slice_b40_long_contexts_sampled(persistent, monkeypatch):
+    """40 requests with 100..600-token synthetic contexts on a 2-layer 7B slice: many attention
+    segments per CTA (the persistent kernel snaps CTA shares to segment boundaries), multi-chunk
+    runs, stream-K tiles shared by several CTAs.  Sampled requests vs the oracle, two steps."""
+    monkeypatch.setenv("CVY_PERSISTENT", persistent)
+    shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
+    vocab = synthetic_vocab(32000)
+    B, seed = 40, 1006
+    dm, eng = make_engine(shape, "bf16", vocab, B, seed, max_pages_per_slot=40)
+    rng = random.Random(5)
+    prompts = [[1, rng.randrange(3, 32000), rng.randrange(3, 32000)] for _ in range(B)]
+    prefix = [100 + (i * 37) % 500 for i in range(B)]
+    rids = [eng.submit_request(p, 2, synth_prefix_len=prefix[i], synth_seed=100 + i) for i, p in enumerate(prompts)]
+    sample = [0, 7, 19, 33, 39]
+    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
+    oreqs = []
+    for i in sample:
+        r = oracle.Request(w, prefix[i] + 8)
+        r.synth_prefix(prefix[i], 100 + i)
+        oreqs.append(r)
+    for t in range(2):
+        eng.step()
+        eng.sync()
+        ora = oracle.step(oreqs, [prompts[i][t] for i in sample])
+        for j, i in enumerate(sample):
+            d = float(np.max(np.abs(eng.debug_logits(rids[i]) - ora[j])))
+            assert d < 2e-2, (i, t, d)
+    eng.poll_segments()
+    eng.close()
 
 
 @pytest.mark.slow
