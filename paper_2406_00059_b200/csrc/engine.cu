@@ -89,7 +89,7 @@ bool make_tmap(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
 //   Bp 160..256: 1 sub-tile, planes as two MMAs into one accumulator (N = Bp)
 //   Bp 512: 1 sub-tile, 2 batch halves of N = 256, 32-element K stages (64B swizzle)
 bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why,
-                 bool allow_kernel_split = true) {
+                 bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0) {
     g.N = N;
     g.K = K;
     g.merge = Bp <= 128;
@@ -98,6 +98,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     // (QKV, O, down): 128-row tiles with K split over a 2..4-CTA cluster (DSMEM reduction)
     g.nsub = (g.merge && N >= 8192) ? 2 : 1;
     if (const char* ns = getenv("CVY_GEMM_NSUB")) g.nsub = std::max(1, std::min(2, atoi(ns)));
+    if (nsub_override > 0) g.nsub = nsub_override;
     if (g.merge) {
         g.mma_n = 2 * Bp;
         g.nbh = 1;
@@ -127,7 +128,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     *smem = (size_t)stages * stage + fixed;
     // split mode: tiles <= SMs (one tile, or one cluster of S CTAs per tile)
     g.split = 0;
-    if (g.merge && !getenv("CVY_GEMM_STREAMK")) {
+    if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk) {
         int S = 1;
         // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
         while (allow_kernel_split && S < 4 && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
@@ -286,6 +287,8 @@ struct cvy_engine {
     int32_t* d_pk_done = nullptr;   // persistent kernel: [L][5] phase-done counters
     int32_t* d_att_cnt = nullptr;   // persistent kernel: split attention segment tickets
     float* d_att_part2 = nullptr;   // persistent kernel: [num_sms][2][G*(hd+2)] partials
+    float* d_pk_part = nullptr;     // persistent kernel: [2][num_sms][128 rows][<=128 cols] GEMM partials
+    uint32_t* d_pk_pflag = nullptr; // persistent kernel: [2][num_sms] partial tags
     int32_t* d_pk_err = nullptr;    // device alias of h_pk_err
     int32_t* h_pk_err = nullptr;    // first timed-out wait of the persistent kernel (0: none)
     bool pk_ok = false;             // model shape supported by the persistent kernel
@@ -520,6 +523,8 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
         ALLOC(e->d_pk_done, sizeof(int32_t) * (size_t)m->n_layers * kPkPhases);
         ALLOC(e->d_att_cnt, sizeof(int32_t) * (size_t)Bmax * Hkv);
         ALLOC(e->d_att_part2, sizeof(float) * (size_t)prop.multiProcessorCount * 2 * (H / Hkv) * (hd + 2));
+        ALLOC(e->d_pk_part, sizeof(float) * 2 * (size_t)prop.multiProcessorCount * 128 * std::min(Bmax, kPkMaxBp));
+        ALLOC(e->d_pk_pflag, sizeof(uint32_t) * 2 * (size_t)prop.multiProcessorCount);
         HALLOC(e->h_pk_err, e->d_pk_err, sizeof(int32_t) * (16 + 24 * (size_t)prop.multiProcessorCount));  // host-mapped: readable after a trap
     }
     e->max_patches = 4 * Bmax + 64;
@@ -619,7 +624,7 @@ void cvy_engine_destroy(cvy_engine* e) {
     void* dptrs[] = {e->d_trace, e->d_slots, e->d_page_table, e->d_in_buf, e->d_force_buf, e->d_rope, e->d_x, e->d_act, e->d_q,
                      e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches,
-                     e->d_pk_done, e->d_att_cnt, e->d_att_part2};
+                     e->d_pk_done, e->d_att_cnt, e->d_att_part2, e->d_pk_part, e->d_pk_pflag};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats, e->h_pk_err};
@@ -990,7 +995,11 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
     g.K = K;
     g.epi = epi;
     if (e->bf16) {
-        if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD)) return false;
+        // gate/up: optionally stream-K over every SM instead of 112 whole 256-row tiles (A/B knob)
+        const bool gu_sk = epi.kind == EPI_SWIGLU && getenv("CVY_GU_STREAMK") && atoi(getenv("CVY_GU_STREAMK")) != 0;
+        const int gu_nsub = (epi.kind == EPI_SWIGLU && getenv("CVY_GU_NSUB")) ? atoi(getenv("CVY_GU_NSUB")) : 0;
+        if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub))
+            return false;
         g.w_row0 = layer * N;
         if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD) {
             const int k = epi.kind == EPI_QKV ? 0 : epi.kind == EPI_SWIGLU ? 2 : (K == ::m_d(e) ? 1 : 3);
@@ -1101,9 +1110,11 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
         K.x_slot = 2u * Bp * 128u;
         K.att_ppslot = (int)(K.x_slot / 8192u);  // 1, 2 or 4 (Bp 32, 64, 128)
         K.att_su = 8 / K.att_ppslot;
-        K.x_arrivals = std::max(1, K.att_ppslot / 2);
+        K.x_arrivals = K.att_ppslot;
         K.x_stages = std::max<int>(K.att_su, (int)((96u * 1024u) / K.x_slot));
         if (const char* v = getenv("CVY_PK_XSTAGES")) K.x_stages = std::max(K.att_su, std::min(16, atoi(v)));
+        // the idle data ring doubles as the stream-K reduction scratch (kPkMaxCon x 16 KB)
+        K.x_stages = std::max<int>(K.x_stages, (int)((kPkMaxCon * 16384u + K.x_slot - 1) / K.x_slot));
         const uint32_t fixed = PkSmem::total(0, K.x_stages, K.x_slot) + 16 * 12;
         K.w_stages = std::min<int>(12, (int)((232448 - fixed) / kPkWStage));
         if (const char* v = getenv("CVY_PK_WSTAGES")) K.w_stages = std::max(2, std::min(K.w_stages, atoi(v)));
@@ -1113,13 +1124,15 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
         K.done = e->d_pk_done;
         K.att_cnt = e->d_att_cnt;
         K.att_part = e->d_att_part2;
-        K.part = e->d_gemm_acc;
-        K.tile_cnt = e->d_tile_cnt;
+        K.part = e->d_pk_part;
+        K.pflag = e->d_pk_pflag;
         K.err = e->d_pk_err;
         K.trace = e->d_trace;
         K.trace_layer = e->trace_layer;
         K.trace_phase = 1;
         if (const char* v = getenv("CVY_PK_TRACE_PHASE")) K.trace_phase = atoi(v);
+        K.dbg = 0;
+        if (const char* v = getenv("CVY_PK_DBG")) K.dbg = atoi(v);
         bk.pk_smem = PkSmem::total(K.w_stages, K.x_stages, K.x_slot);
         int nb = 0;
         if (ok && K.w_stages >= 2 && bk.pk_smem <= 232448 &&

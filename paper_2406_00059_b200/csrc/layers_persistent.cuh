@@ -26,12 +26,15 @@
 // inside a phase; the only cross-CTA waits are the phase-done counters, which every CTA
 // reaches (the grid is co-resident: one CTA per SM, cooperative launch).
 //
-// Warp roles (224 threads):
-//   warps 0-3  GEMM epilogues (TMEM lane = tile row) and attention consumers (mma.sync)
-//   warp 4     weight producer: TMA of W k-blocks into the W ring + L2 prefetch look-ahead
-//   warp 5     MMA issuer (tcgen05.mma, one lane) and TMEM owner
-//   warp 6     data producer: TMA of activation k-blocks (hi, lo planes) and KV pages into
-//              the D ring, each after its phase dependency
+// Warp roles (384 threads, 3 warpgroups; setmaxnreg moves registers from WG1 to WG0):
+//   WG0 warps 0-3   GEMM epilogues (TMEM lane = tile row) and attention consumers (mma.sync)
+//   WG1 warp 4      weight producer: TMA of W k-blocks into the W ring + L2 prefetch look-ahead
+//       warp 5      MMA issuer (tcgen05.mma, one lane) and TMEM owner
+//       warp 6      data producer: TMA of activation k-blocks (hi, lo planes) and KV pages into
+//                   the D ring, each after its phase dependency
+//       warp 7      idle
+//   WG2 warps 8-11  attention consumers (the attention phase runs on 8 warps, one KV page each
+//                   per 8-page unit: the mma.sync page loop is latency-bound)
 #pragma once
 #include "attention_tc.cuh"
 #include "common.cuh"
@@ -41,11 +44,15 @@
 
 namespace cvy {
 
-constexpr int kPkThreads = 224;
+constexpr int kPkThreads = 384;   // 3 warpgroups (see the role table above)
+constexpr int kPkAttWarps = 8;    // attention consumers: warps 0-3 and 8-11
+constexpr uint32_t kAttBar = 4;   // named barrier of the 256 attention threads
+constexpr uint32_t kWg2Bar = 5;   // named barrier of warpgroup 2
 constexpr int kPkPhases = 5;
 constexpr int kPkMaxBp = 128;
 constexpr uint32_t kPkWStage = 128u * 128u;          // 128 weight rows x 64 bf16 (128B swizzle)
 constexpr uint32_t kPkAttStage = 4u * 2u * 16u * 128u * 2u;  // 4 pages x (K, V) x 16 x 128 bf16
+constexpr int kPkMaxCon = 6;  // later contributors of one stream-K tile reduced per batch (host checks)
 constexpr int kPkTraceStride = 32;  // [0,5) data-producer phase start, [8,13) phase done,
                                       // [16,21) last accumulator received, [24,29) last MMA issued
 
@@ -58,32 +65,34 @@ struct PkParams {
     int32_t w_stages;    // W ring depth (16 KB slots)
     int32_t x_stages;    // D ring depth
     uint32_t x_slot;     // D ring slot bytes = one activation k-block (hi + lo planes: 2*Bp*128);
-                         // an attention unit (8 KV pages of 8 KB: 2 per consumer warp) spans
+                         // an attention unit (8 KV pages of 8 KB: one per attention warp) spans
                          // att_su consecutive slots
     int32_t att_ppslot;  // KV pages per D-ring slot (x_slot / 8 KB): 1, 2 or 4
     int32_t att_su;      // D-ring slots per attention unit (8 / att_ppslot)
-    int32_t x_arrivals;  // arrivals that release a D-ring slot: max(1, att_ppslot / 2) (the warps
-                         // sharing an attention slot, or as many tcgen05.commit for an X slot)
+    int32_t x_arrivals;  // arrivals that release a D-ring slot: att_ppslot (the attention warps
+                         // sharing a slot, or as many tcgen05.commit for an activation slot)
     uint32_t tmem_cols;
     int32_t l2_pf;       // weight k-blocks prefetched into L2 ahead of the ring
     int32_t* done;       // [L][5] phase-done counters, zeroed before every launch
     int32_t* att_cnt;    // [Bmax][Hkv] arrival tickets of split attention segments (self-resetting)
     float* att_part;     // [grid][2][G*(hd+2)] partial (num, max, den) of split segments
-    float* part;         // stream-K fp32 accumulators of shared tiles (zero between uses)
-    int32_t* tile_cnt;   // stream-K arrival tickets (self-resetting)
+    float* part;         // [2][grid][Bp/32][8][128][4] fp32: the partial tile of each CTA's first
+                         // (shared) segment of a GEMM phase, buffer = GEMM index & 1
+    uint32_t* pflag;     // [2][grid] tag of the partial last published by each CTA
     int32_t* err;        // first failing wait (diagnostics before the trap)
     unsigned long long* trace;  // [grid][kPkTraceStride] %globaltimer stamps of trace_layer, or null
     int32_t trace_layer;
     int32_t trace_phase;  // GEMM index (0..3) whose epilogue gets detailed stamps [5,6,7,13,14]
+    int32_t dbg;          // measurement knobs (CVY_PK_DBG): 1 = attention consumers skip all math
 };
 
 struct PkSmem {
     // offsets from the 1024-aligned base; host and device agree
     __host__ __device__ static constexpr uint32_t esm_bytes() { return 128u * kEsmLd * 4u; }
-    __host__ __device__ static constexpr uint32_t pbuf_bytes() { return (uint32_t)kAtcWarps * 8u * 32u * 2u; }
+    __host__ __device__ static constexpr uint32_t pbuf_bytes() { return (uint32_t)kPkAttWarps * 8u * 16u * 2u; }
     __host__ __device__ static constexpr uint32_t meta_bytes() { return (uint32_t)kPkMaxBp * 16u; }
     __host__ __device__ static constexpr uint32_t table_bytes() { return (uint32_t)(3 * kPkMaxBp + 4) * 4u; }
-    __host__ __device__ static constexpr uint32_t bar_bytes(int ws, int xs) { return (uint32_t)(2 * ws + 2 * xs + 4) * 8u + 64u; }
+    __host__ __device__ static constexpr uint32_t bar_bytes(int ws, int xs) { return (uint32_t)(2 * ws + 2 * xs + 6) * 8u + 64u; }
     __host__ __device__ static constexpr uint32_t total(int ws, int xs, uint32_t x_slot) {
         return 1024u + (uint32_t)ws * kPkWStage + (uint32_t)xs * x_slot + esm_bytes() + pbuf_bytes() + meta_bytes() +
                table_bytes() + bar_bytes(ws, xs);
@@ -146,6 +155,30 @@ CVY_DEV void pk_bar_wait(uint64_t* bar, uint32_t parity, int32_t* err, int code)
                 pk_fail(err, code, t0);
             }
         }
+    }
+}
+
+// 1D bulk copy global -> shared (async proxy), completion on an mbarrier (complete_tx)
+CVY_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem_dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+CVY_DEV void st_release_gpu_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+CVY_DEV uint32_t ld_acquire_gpu_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+CVY_DEV void pk_wait_tag(const uint32_t* p, uint32_t tag, int32_t* err, int code) {
+    if (ld_acquire_gpu_u32(p) == tag) return;
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire_gpu_u32(p) != tag) {
+        __nanosleep(32);
+        if (gtimer() - t0 > kPkTimeoutNs) pk_fail(err, code, t0);
     }
 }
 
@@ -217,7 +250,8 @@ CVY_DEV int pk_gp(int p) { return p == 0 ? 0 : p - 1; }
 template <int EPI>
 CVY_DEV void pk_gemm_epilogue(const StepParams& P, const PkParams& K, const EpiArgs& E, int gp, EpiMeta& meta,
                               float* esm, int* flags, uint64_t* tfull, uint64_t* tempty, uint32_t tmem_base,
-                              uint32_t& acnt, int et, int warp, unsigned long long* tr) {
+                              uint32_t& acnt, int et, int warp, unsigned long long* tr, uint32_t tag,
+                              uint64_t* red_bar, uint32_t& red_ph, uint8_t* scratch) {
     const PkGemm& g = K.g[gp];
     const int Gc = gridDim.x;
     const long long T = (long long)g.tiles * g.kblocks;
@@ -225,10 +259,13 @@ CVY_DEV void pk_gemm_epilogue(const StepParams& P, const PkParams& K, const EpiA
     pk_share(T, blockIdx.x, Gc, it, it1);
     const int Bp = P.Bp;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const int buf = gp & 1;
     while (it < it1) {
         const int tile = (int)(it / g.kblocks);
         const long long tb = (long long)tile * g.kblocks, te = tb + g.kblocks;
+        const long long seg_b = it;  // this CTA's segment of the tile: [seg_b, seg_e)
         it = min(it1, te);
+        const long long seg_e = it;
         const int c_first = cta_of_iter(tb, T, Gc), c_last = cta_of_iter(te - 1, T, Gc);
         const int as = (int)(acnt & 1u);
         pk_bar_wait(&tfull[as], (acnt >> 1) & 1u, K.err, (0x100 + gp) | (int)(min(acnt, 0x7FFFFu) << 12));
@@ -236,8 +273,8 @@ CVY_DEV void pk_gemm_epilogue(const StepParams& P, const PkParams& K, const EpiA
         if (tr && et == 0) tr[16 + (gp == 0 ? 0 : gp + 1)] = gtimer();
         const uint32_t tacc = tmem_base + lane_off + (uint32_t)(as * 2 * Bp);
         const bool dt = tr && et == 0 && gp == K.trace_phase;
+        if (dt) tr[15] = gtimer();  // accumulator of the segment received
         if (c_first == c_last) {
-            if (dt) tr[14] += 1;
             for (int cb = 0; cb < Bp; cb += 32) {
                 float v[32], w[32];
                 tmem_ld32(tacc + (uint32_t)cb, v);
@@ -248,56 +285,94 @@ CVY_DEV void pk_gemm_epilogue(const StepParams& P, const PkParams& K, const EpiA
             }
             tc_fence_before();
             mbar_arrive(&tempty[as]);
+        } else if (seg_b != tb) {
+            // a later contributor: publish this partial (coalesced [chunk][q][row][4]) + tag
+            float4* mine = reinterpret_cast<float4*>(K.part) + ((size_t)buf * Gc + blockIdx.x) * (size_t)Bp * 32;
+            for (int cb = 0; cb < Bp; cb += 32) {
+                float v[32], w[32];
+                tmem_ld32(tacc + (uint32_t)cb, v);
+                tmem_ld32(tacc + (uint32_t)(Bp + cb), w);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    __stcg(mine + ((size_t)(cb / 32) * 8 + q) * 128 + et,
+                           make_float4(v[4 * q] + w[4 * q], v[4 * q + 1] + w[4 * q + 1], v[4 * q + 2] + w[4 * q + 2],
+                                       v[4 * q + 3] + w[4 * q + 3]));
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[as]);
+            __threadfence();
+            epi_sync();
+            if (et == 0) st_release_gpu_u32(K.pflag + (size_t)buf * Gc + blockIdx.x, tag);
         } else {
-            float* acc = K.part + (size_t)tile * 128 * Bp;
+            // the tile's first CTA (reaches it last in its range): add the later contributors'
+            // partials in CTA order -- deterministic -- and run the epilogue.  The partial chunks
+            // (16 KB each) are bulk-copied into the data ring, idle here: the next phase's loads
+            // wait for this phase's done counter, which this CTA has not bumped yet.
+            // tags of every later contributor (one thread each, in parallel), then the proxy fence
+            // that orders the bulk copies after them
+            {
+                int j = 0;
+                for (long long i = seg_e; i < te; ++j) {
+                    const int c = cta_of_iter(i, T, Gc);
+                    if ((j & 127) == et) pk_wait_tag(K.pflag + (size_t)buf * Gc + c, tag, K.err, 0x140 + gp);
+                    i = (T * (c + 1)) / Gc;
+                }
+            }
+            fence_proxy_async_global();
+            epi_sync();
+            if (dt) tr[5] = gtimer();
             for (int cb = 0; cb < Bp; cb += 32) {
                 float v[32], w[32];
                 tmem_ld32(tacc + (uint32_t)cb, v);
                 tmem_ld32(tacc + (uint32_t)(Bp + cb), w);
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] += w[i];
-                float* dst = acc + (size_t)et * Bp + cb;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            }
-            tc_fence_before();
-            mbar_arrive(&tempty[as]);
-            if (dt) tr[5] = gtimer();
-            __threadfence();
-            epi_sync();
-            if (et == 0) flags[0] = (atomicAdd(&K.tile_cnt[tile], 1) == pk_contributors(T, Gc, tb, te) - 1);
-            epi_sync();
-            if (dt) tr[6] = gtimer();
-            if (flags[0]) {
-                __threadfence();
-                for (int cb = 0; cb < Bp; cb += 32) {
-                    float v[32];
-                    float4* src = reinterpret_cast<float4*>(acc + (size_t)et * Bp + cb);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 t4 = __ldcg(src + q);
-                        v[4 * q] = t4.x;
-                        v[4 * q + 1] = t4.y;
-                        v[4 * q + 2] = t4.z;
-                        v[4 * q + 3] = t4.w;
+                if (cb + 32 >= Bp) {
+                    tc_fence_before();
+                    mbar_arrive(&tempty[as]);
+                }
+                for (long long i = seg_e; i < te;) {
+                    // a batch of up to kPkMaxCon contributors' 16 KB chunks, CTA order
+                    int con[kPkMaxCon];
+                    int n = 0;
+                    for (; i < te && n < kPkMaxCon; ++n) {
+                        con[n] = cta_of_iter(i, T, Gc);
+                        i = (T * (con[n] + 1)) / Gc;
                     }
+                    if (et == 0) {
+                        mbar_arrive_expect_tx(red_bar, (uint32_t)n * 16384u);
+                        for (int j = 0; j < n; ++j)
+                            bulk_g2s(scratch + (size_t)j * 16384,
+                                     reinterpret_cast<const float4*>(K.part) + ((size_t)buf * Gc + con[j]) * (size_t)Bp * 32 +
+                                         (size_t)(cb / 32) * 8 * 128,
+                                     16384u, red_bar);
+                    }
+                    pk_bar_wait(red_bar, red_ph, K.err, 0x150 + gp);
+                    red_ph ^= 1u;
+                    if (dt) tr[cb == 0 ? 6 : 13] = gtimer();
+                    for (int j = 0; j < n; ++j) {
+                        const float4* src = reinterpret_cast<const float4*>(scratch + (size_t)j * 16384) + et;
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));
-                    epilogue_chunk<__nv_bfloat16, EPI>(P, E, tile * 128, cb, v, esm, meta, et);
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 t4 = src[(size_t)q * 128];
+                            v[4 * q] += t4.x;
+                            v[4 * q + 1] += t4.y;
+                            v[4 * q + 2] += t4.z;
+                            v[4 * q + 3] += t4.w;
+                        }
+                    }
+                    epi_sync();  // scratch is refilled by the next batch
                 }
-                if (et == 0) K.tile_cnt[tile] = 0;
-                if (dt) {
-                    tr[7] = gtimer();
-                    tr[13] += 1;
-                }
+                epilogue_chunk<__nv_bfloat16, EPI>(P, E, tile * 128, cb, v, esm, meta, et);
+                if (dt) tr[cb == 0 ? 7 : 14] = gtimer();
             }
-            epi_sync();  // flags[0] is rewritten by the next shared tile
         }
         ++acnt;
     }
 }
 
-// ------------------------------------------------------------------ attention phase (warps 0-3)
+// ------------------------------------------------------------------ attention phase (8 warps)
+CVY_DEV void att_sync() { named_bar_sync(kAttBar, kPkAttWarps * 32); }
 struct PkAttRun {
     float m_run[2], l_run[2];
     float o[8][4];
@@ -308,6 +383,7 @@ struct PkAttRun {
 // partial and the last arriving CTA of the segment combines all partials in CTA order
 CVY_DEV void pk_att_finish(const StepParams& P, const PkParams& K, PkAttRun& R, float* comb, int* flags, int b, int g,
                            int seg_s, int seg_e, int run_s, int run_e, long long U, int et, int warp, int lane) {
+    // et: attention thread index 0..255, warp: attention warp index 0..7
     constexpr int HD = 128, KSTEPS = 8;
     const int G = P.H / P.Hkv;
     const int tig = lane & 3, grp = lane >> 2;
@@ -332,7 +408,7 @@ CVY_DEV void pk_att_finish(const StepParams& P, const PkParams& K, PkAttRun& R, 
             cw[8 + (h0 + 1) * HD + 16 * i + grp + 8] = R.o[i][3];
         }
     }
-    epi_sync();
+    att_sync();
     const bool complete = (run_s == seg_s) && (run_e == seg_e);
     const int Gc = gridDim.x;
     long long u0, u1;
@@ -340,13 +416,13 @@ CVY_DEV void pk_att_finish(const StepParams& P, const PkParams& K, PkAttRun& R, 
     const size_t pstride = (size_t)G * (HD + 2);
     float* mypart = K.att_part + ((size_t)blockIdx.x * 2 + (run_s == u0 ? 0 : 1)) * pstride;
     __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(P.o) + (size_t)b * P.act_ld + (size_t)g * G * HD;
-    for (int idx = et; idx < G * HD; idx += kEpiThreads) {
+    for (int idx = et; idx < G * HD; idx += (kPkAttWarps * 32)) {
         const int j = idx / HD, e = idx % HD;
         float mstar = -INFINITY;
-        for (int w = 0; w < kAtcWarps; ++w) mstar = fmaxf(mstar, comb[w * (8 + 4 * HD) + j]);
+        for (int w = 0; w < kPkAttWarps; ++w) mstar = fmaxf(mstar, comb[w * (8 + 4 * HD) + j]);
         float num = 0.f, den = 0.f;
         if (mstar != -INFINITY) {
-            for (int w = 0; w < kAtcWarps; ++w) {
+            for (int w = 0; w < kPkAttWarps; ++w) {
                 const float* c = comb + w * (8 + 4 * HD);
                 if (c[j] == -INFINITY) continue;
                 const float sc = exp2f(c[j] - mstar);
@@ -367,12 +443,12 @@ CVY_DEV void pk_att_finish(const StepParams& P, const PkParams& K, PkAttRun& R, 
     if (!complete) {
         const int c_first = cta_of_iter(seg_s, U, Gc), c_last = cta_of_iter(seg_e - 1, U, Gc);
         __threadfence();
-        epi_sync();
+        att_sync();
         if (et == 0) flags[1] = (atomicAdd(&K.att_cnt[b * P.Hkv + g], 1) == pk_contributors(U, Gc, seg_s, seg_e) - 1);
-        epi_sync();
+        att_sync();
         if (flags[1]) {
             __threadfence();
-            for (int idx = et; idx < G * HD; idx += kEpiThreads) {
+            for (int idx = et; idx < G * HD; idx += (kPkAttWarps * 32)) {
                 const int j = idx / HD;
                 float M = -INFINITY;
                 for (int c = c_first; c <= c_last; ++c) {
@@ -401,7 +477,7 @@ CVY_DEV void pk_att_finish(const StepParams& P, const PkParams& K, PkAttRun& R, 
             if (et == 0) K.att_cnt[b * P.Hkv + g] = 0;
         }
     }
-    epi_sync();  // comb / flags reuse
+    att_sync();  // comb / flags reuse
 }
 
 CVY_DEV void pk_att_load_q(const StepParams& P, PkAttRun& R, int b, int g, int lane) {
@@ -627,6 +703,69 @@ CVY_DEV void pk_att_pages2(PkAttRun& R, uint32_t ka, uint32_t kb, bool has_b, ui
     __syncwarp();
 }
 
+// One layer's attention over this CTA's units [u0, u1) on the 8 attention warps (aw = 0..7,
+// at = 0..255).  Unit = 8 KV pages of one (slot, kv head); warp aw takes page aw of the unit,
+// which sits in D-ring use xcnt + aw / ppslot; each warp releases its slot itself.
+CVY_DEV void pk_attention_phase(const StepParams& P, const PkParams& K, long long u0, long long u1, long long U,
+                                const int* att_pre, const int* att_nch, const int* att_nkeys, uint8_t* xring,
+                                uint64_t* xfull, uint64_t* xempty, float* comb, uint16_t* pbuf, int* flags,
+                                uint32_t& xcnt, int aw, int at, int lane, unsigned long long* tr) {
+    const int SX = K.x_stages, Bp = P.Bp, G = P.H / P.Hkv;
+    const int ppslot = K.att_ppslot;
+    uint16_t* pw = pbuf + aw * 128;
+    PkAttRun R;
+    int run_s = (int)u0;
+    const bool atr = tr != nullptr && at == 0;
+    unsigned long long t_wait = 0, t_fin = 0, t_q = 0, t_page = 0;
+    int n_runs = 0;
+    for (long long u = u0; u < u1; ++u) {
+        int b, g, chunk;
+        pk_att_decode(att_pre, att_nch, Bp, (int)u, b, g, chunk);
+        const int nchb = att_nch[b];
+        const int seg_s = att_pre[b] + g * nchb, seg_e = seg_s + nchb;
+        if ((u == u0 || chunk == 0) && !(K.dbg & 1)) {
+            run_s = (int)u;
+            const unsigned long long ta = atr ? gtimer() : 0;
+            pk_att_load_q(P, R, b, g, lane);
+            if (atr) {
+                t_q += gtimer() - ta;
+                ++n_runs;
+            }
+        }
+        const int nkeys = att_nkeys[b];
+        const int npg = (nkeys + 15) / 16;
+        const int pidx = chunk * 8 + aw;
+        const uint32_t use = xcnt + (uint32_t)(aw / ppslot);
+        const int s = (int)(use % (uint32_t)SX);
+        const unsigned long long tw = atr ? gtimer() : 0;
+        pk_bar_wait(&xfull[s], (use / (uint32_t)SX) & 1u, K.err,
+                    (pidx < npg ? 0x510 : 0x511) | (int)(min(use, 0x7FFFFu) << 12));
+        const unsigned long long tp = atr ? gtimer() : 0;
+        if (atr) t_wait += tp - tw;
+        if (pidx < npg && !(K.dbg & 1)) {
+            const uint32_t kbase = smem_u32(xring + (size_t)s * K.x_slot + (size_t)(aw % ppslot) * 8192);
+            pk_att_page(R, kbase, kbase + 4096, pw, pidx * 16, nkeys, G, lane);
+        }
+        if (atr) t_page += gtimer() - tp;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[s]);
+        xcnt += (uint32_t)K.att_su;
+        if ((u == u1 - 1 || chunk == nchb - 1) && !(K.dbg & 1)) {
+            const unsigned long long tf = atr ? gtimer() : 0;
+            pk_att_finish(P, K, R, comb, flags, b, g, seg_s, seg_e, run_s, (int)u + 1, U, at, aw, lane);
+            if (atr) t_fin += gtimer() - tf;
+        }
+    }
+    if (atr) {
+        tr[21] = t_wait;
+        tr[22] = t_page;
+        tr[23] = t_q;
+        tr[29] = t_fin;
+        tr[30] = (unsigned long long)n_runs;
+        tr[31] = (unsigned long long)(u1 - u0);
+    }
+}
+
 // ------------------------------------------------------------------ the kernel
 __global__ void __launch_bounds__(kPkThreads, 1)
     layers_persistent_kernel(const __grid_constant__ CUtensorMap tmWqkv, const __grid_constant__ CUtensorMap tmWo,
@@ -655,7 +794,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     uint64_t* xempty = xfull + SX;
     uint64_t* tfull = xempty + SX;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* red_bar = tempty + 2;  // stream-K reduction bulk copies
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 2);
     int* flags = reinterpret_cast<int*>(tmem_slot + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -691,6 +831,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
             mbar_init(&tfull[s], 1);
             mbar_init(&tempty[s], kEpiThreads);
         }
+        mbar_init(red_bar, 1);
         fence_mbar_init();
     }
     if (warp == 6 && lane == 0) {
@@ -733,11 +874,15 @@ __global__ void __launch_bounds__(kPkThreads, 1)
     }
     __syncthreads();
     const uint32_t tmem_base = *tmem_slot;
+    const uint32_t step_tag = (uint32_t)*P.step_ctr;  // distinguishes partial tags across steps
     const long long U = att_pre[kPkMaxBp];
     const int nseg = att_nkeys[kPkMaxBp];
     // note: att_pre[b] for b >= Bp equals U (nch = 0), so decoding may search [0, Bp)
     unsigned long long* tr = (K.trace != nullptr) ? K.trace + (size_t)cta * kPkTraceStride : nullptr;
 
+    if (warp >= 4 && warp < 8) {
+    // ===================== WG1: producers + MMA issuer (few registers) =====================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
     if (warp == 4) {
         // ===================== weight producer =====================
         // Single thread; the per-item path is a handful of integer adds (no divisions: a 64-bit
@@ -812,74 +957,77 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         }
     } else if (warp == 6) {
         // ===================== data producer (activations, KV pages) =====================
-        if (lane == 0) {
-            const uint64_t pol_x = policy_evict_last();
-            const uint64_t pol_kv = policy_evict_first();
-            const uint32_t xrow = (uint32_t)Bp * 128u;  // one plane of one k-block
-            long long u0, u1;
-            pk_att_range(att_pre, att_nch, Bp, U, nseg, cta, Gc, u0, u1);
-            uint32_t cnt = 0;
-            for (int l = 0; l < L; ++l) {
-                for (int p = 0; p < kPkPhases; ++p) {
-                    if (p > 0 || l > 0) {
+        // Activation k-blocks: lane 0.  KV pages: the whole warp -- an 8-page unit is 32 TMA
+        // boxes (page, K/V, 64-dim half), one per lane, after lane 0 armed the unit's slots.
+        const uint64_t pol_x = policy_evict_last();
+        const uint64_t pol_kv = policy_evict_first();
+        const uint32_t xrow = (uint32_t)Bp * 128u;  // one plane of one k-block
+        long long u0, u1;
+        pk_att_range(att_pre, att_nch, Bp, U, nseg, cta, Gc, u0, u1);
+        uint32_t cnt = 0;
+        for (int l = 0; l < L; ++l) {
+            for (int p = 0; p < kPkPhases; ++p) {
+                if (p > 0 || l > 0) {
+                    if (lane == 0)
                         pk_wait_done(K.done + (p > 0 ? l * kPkPhases + p - 1 : (l - 1) * kPkPhases + 4), Gc, K.err,
                                      (0x300 + p) | ((l * 8 + p) << 12));
-                        fence_proxy_async_global();
-                    }
-                    if (tr && l == K.trace_layer) tr[p] = gtimer();
-                    if (p == 1) {
-                        const int ppslot = K.att_ppslot;
-                        // software pipeline: the next unit's page ids are loaded while this unit
-                        // waits for its ring slots
-                        int nb = 0, ng = 0, nchunk = 0, nnp = 0, npage[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                        auto fetch = [&](long long uu) {
-                            pk_att_decode(att_pre, att_nch, Bp, (int)uu, nb, ng, nchunk);
-                            nnp = min(8, (att_nkeys[nb] + 15) / 16 - nchunk * 8);
-                            const int32_t* pt = P.page_table + (size_t)nb * P.max_pages + nchunk * 8;
-#pragma unroll
-                            for (int pg = 0; pg < 8; ++pg) npage[pg] = pg < nnp ? __ldg(pt + pg) : 0;
-                        };
-                        if (u0 < u1) fetch(u0);
-                        for (long long u = u0; u < u1; ++u) {
-                            const int g = ng, np = nnp;
-                            int page[8];
-#pragma unroll
-                            for (int pg = 0; pg < 8; ++pg) page[pg] = npage[pg];
-                            if (u + 1 < u1) fetch(u + 1);
+                    __syncwarp();
+                    fence_proxy_async_global();
+                }
+                if (tr && l == K.trace_layer && lane == 0) tr[p] = gtimer();
+                if (p == 1) {
+                    const int ppslot = K.att_ppslot;
+                    const int pg = lane >> 2, cc = (lane >> 1) & 1, hh = lane & 1;
+                    // software pipeline: each lane's page id of the next unit loads while this
+                    // unit's slots are armed
+                    int nb = 0, ng = 0, nchunk = 0, nnp = 0, npage = 0;
+                    auto fetch = [&](long long uu) {
+                        pk_att_decode(att_pre, att_nch, Bp, (int)uu, nb, ng, nchunk);
+                        nnp = min(8, (att_nkeys[nb] + 15) / 16 - nchunk * 8);
+                        npage = pg < nnp ? __ldg(P.page_table + (size_t)nb * P.max_pages + nchunk * 8 + pg) : 0;
+                    };
+                    if (u0 < u1) fetch(u0);
+                    for (long long u = u0; u < u1; ++u) {
+                        const int g = ng, np = nnp, page = npage;
+                        if (u + 1 < u1) fetch(u + 1);
+                        if (lane == 0) {
                             for (int j = 0; j < K.att_su; ++j) {
-                                const int s = (int)(cnt % (uint32_t)SX);
-                                pk_bar_wait(&xempty[s], ((cnt / (uint32_t)SX) & 1u) ^ 1u, K.err,
-                                            0x310 | (int)(min(cnt, 0x7FFFFu) << 12));
+                                const uint32_t c2 = cnt + (uint32_t)j;
+                                const int s = (int)(c2 % (uint32_t)SX);
+                                pk_bar_wait(&xempty[s], ((c2 / (uint32_t)SX) & 1u) ^ 1u, K.err,
+                                            0x310 | (int)(min(c2, 0x7FFFFu) << 12));
                                 const int pg0 = j * ppslot, pg1 = min(np, pg0 + ppslot);
                                 mbar_arrive_expect_tx(&xfull[s], (uint32_t)max(0, pg1 - pg0) * 2u * 4096u);
-                                uint8_t* dst = xring + (size_t)s * K.x_slot;
-                                for (int pg = pg0; pg < pg1; ++pg) {
-                                    for (int c = 0; c < 2; ++c) {
-                                        const int row0 = ((((l * P.n_pages + page[pg]) * 2 + c) * Hkv) + g) * 16;
-                                        uint8_t* d2 = dst + (size_t)((pg - pg0) * 2 + c) * 4096;
-                                        tma_load_2d(d2, &tmKV, &xfull[s], 0, row0, pol_kv);
-                                        tma_load_2d(d2 + 2048, &tmKV, &xfull[s], 64, row0, pol_kv);
-                                    }
-                                }
-                                ++cnt;
                             }
                         }
-                    } else {
-                        const int q = pk_gp(p);
-                        const int kblocks = K.g[q].kblocks;
+                        __syncwarp();
+                        if (pg < np) {
+                            const uint32_t c2 = cnt + (uint32_t)(pg / ppslot);
+                            const int s = (int)(c2 % (uint32_t)SX);
+                            const int row0 = ((((l * P.n_pages + page) * 2 + cc) * Hkv) + g) * 16;
+                            uint8_t* dst = xring + (size_t)s * K.x_slot + (size_t)((pg % ppslot) * 2 + cc) * 4096 + hh * 2048;
+                            tma_load_2d(dst, &tmKV, &xfull[s], hh * 64, row0, pol_kv);
+                        }
+                        cnt += (uint32_t)K.att_su;
+                    }
+                } else {
+                    const int q = pk_gp(p);
+                    const int kblocks = K.g[q].kblocks;
+                    long long a0, a1;
+                    pk_share((long long)K.g[q].tiles * kblocks, cta, Gc, a0, a1);
+                    if (lane == 0) {
                         const CUtensorMap* xmap = (p == 2) ? &tmXo : (p == 4) ? &tmXh : &tmXact;
-                        long long a0, a1;
-                        pk_share((long long)K.g[q].tiles * kblocks, cta, Gc, a0, a1);
                         int kb = (int)(a0 % kblocks);
                         int s = (int)(cnt % (uint32_t)SX);
                         uint32_t ph = (cnt / (uint32_t)SX) & 1u;
+                        uint32_t c2 = cnt;
                         for (int it = (int)a0; it < (int)a1; ++it) {
-                            pk_bar_wait(&xempty[s], ph ^ 1u, K.err, (0x320 + p) | (int)(min(cnt, 0x7FFFFu) << 12));
+                            pk_bar_wait(&xempty[s], ph ^ 1u, K.err, (0x320 + p) | (int)(min(c2, 0x7FFFFu) << 12));
                             mbar_arrive_expect_tx(&xfull[s], 2u * xrow);
                             uint8_t* dst = xring + (size_t)s * K.x_slot;
                             tma_load_2d(dst, xmap, &xfull[s], kb * 64, 0, pol_x);
                             tma_load_2d(dst + xrow, xmap, &xfull[s], kb * 64, (int)P.Bmax, pol_x);
-                            ++cnt;
+                            ++c2;
                             if (++kb == kblocks) kb = 0;
                             if (++s == SX) {
                                 s = 0;
@@ -887,6 +1035,8 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                             }
                         }
                     }
+                    cnt += (uint32_t)(a1 - a0);
+                    __syncwarp();
                 }
             }
         }
@@ -957,14 +1107,15 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                 if (tr && l == K.trace_layer && lane == 0) tr[24 + p] = gtimer();
             }
         }
-    } else {
-        // ===================== epilogue / attention warps 0-3 =====================
+    }
+    } else if (warp < 4) {
+        // ===================== WG0: epilogue / attention warps 0-3 =====================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
         const int et = threadIdx.x;
         const int G = P.H / Hkv;
         long long u0, u1;
         pk_att_range(att_pre, att_nch, Bp, U, nseg, cta, Gc, u0, u1);
-        uint32_t xcnt = 0, acnt = 0;
-        uint16_t* pw = pbuf + warp * 256;
+        uint32_t xcnt = 0, acnt = 0, red_ph = 0;
         for (int l = 0; l < L; ++l) {
             for (int p = 0; p < kPkPhases; ++p) {
                 if (p > 0 || l > 0) {
@@ -974,78 +1125,12 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     epi_sync();
                 }
                 if (p == 1) {
-                    // ---- paged attention over this CTA's units
-                    PkAttRun R;
-                    int run_s = (int)u0;
-                    const bool atr = tr && l == K.trace_layer && et == 0;
-                    unsigned long long t_wait = 0, t_fin = 0, t_q = 0, t_page = 0;
-                    int n_runs = 0;
-                    for (long long u = u0; u < u1; ++u) {
-                        int b, g, chunk;
-                        pk_att_decode(att_pre, att_nch, Bp, (int)u, b, g, chunk);
-                        const int nchb = att_nch[b];
-                        const int seg_s = att_pre[b] + g * nchb, seg_e = seg_s + nchb;
-                        if (u == u0 || chunk == 0) {
-                            run_s = (int)u;
-                            const unsigned long long ta = atr ? gtimer() : 0;
-                            pk_att_load_q(P, R, b, g, lane);
-                            // warm L1 with the next run's q rows (G heads x 512 B)
-                            if (warp == 0 && seg_e < u1 && lane < 4 * G) {
-                                int b2, g2, c2;
-                                pk_att_decode(att_pre, att_nch, Bp, seg_e, b2, g2, c2);
-                                const float* q2 = P.q + (size_t)b2 * (P.H * 128) + (size_t)g2 * G * 128 + lane * 32;
-                                asm volatile("prefetch.global.L1 [%0];" ::"l"(q2));
-                            }
-                            if (atr) {
-                                t_q += gtimer() - ta;
-                                ++n_runs;
-                            }
-                        }
-                        const int nkeys = att_nkeys[b];
-                        const int npg = (nkeys + 15) / 16;
-                        // this warp's pages: 2*warp, 2*warp+1 of the unit; page q of the unit
-                        // lives in slot q / ppslot at local page q % ppslot
-                        const int ppslot = K.att_ppslot;
-                        const int pa = chunk * 8 + 2 * warp;
-                        const bool has_a = pa < npg, has_b = pa + 1 < npg;
-                        const uint32_t use_a = xcnt + (uint32_t)((2 * warp) / ppslot);
-                        const uint32_t use_b = xcnt + (uint32_t)((2 * warp + 1) / ppslot);
-                        const int sa = (int)(use_a % (uint32_t)SX), sb = (int)(use_b % (uint32_t)SX);
-                        const unsigned long long tw = atr ? gtimer() : 0;
-                        pk_bar_wait(&xfull[sa], (use_a / (uint32_t)SX) & 1u, K.err,
-                                    (has_a ? 0x510 : 0x511) | (int)(min(use_a, 0x7FFFFu) << 12));
-                        if (use_b != use_a)
-                            pk_bar_wait(&xfull[sb], (use_b / (uint32_t)SX) & 1u, K.err,
-                                        0x512 | (int)(min(use_b, 0x7FFFFu) << 12));
-                        const unsigned long long tp = atr ? gtimer() : 0;
-                        if (atr) t_wait += tp - tw;
-                        if (has_a) {
-                            const uint32_t ka = smem_u32(xring + (size_t)sa * K.x_slot + (size_t)((2 * warp) % ppslot) * 8192);
-                            const uint32_t kb = smem_u32(xring + (size_t)sb * K.x_slot + (size_t)((2 * warp + 1) % ppslot) * 8192);
-                            pk_att_pages2(R, ka, kb, has_b, pw, pa * 16, pa * 16 + 16, nkeys, G, lane);
-                        }
-                        if (atr) t_page += gtimer() - tp;
-                        __syncwarp();
-                        // release the slot(s) this warp owns (each slot's warps arrive once)
-                        if (lane == 0) {
-                            mbar_arrive(&xempty[sa]);
-                            if (use_b != use_a) mbar_arrive(&xempty[sb]);
-                        }
-                        xcnt += (uint32_t)K.att_su;
-                        if (u == u1 - 1 || chunk == nchb - 1) {
-                            const unsigned long long tf = atr ? gtimer() : 0;
-                            pk_att_finish(P, K, R, esm, flags, b, g, seg_s, seg_e, run_s, (int)u + 1, U, et, warp, lane);
-                            if (atr) t_fin += gtimer() - tf;
-                        }
-                    }
-                    if (atr) {
-                        tr[21] = t_wait;
-                        tr[22] = t_page;
-                        tr[23] = t_q;
-                        tr[29] = t_fin;
-                        tr[30] = (unsigned long long)n_runs;
-                        tr[31] = (unsigned long long)(u1 - u0);
-                    }
+                    pk_attention_phase(P, K, u0, u1, U, att_pre, att_nch, att_nkeys, xring, xfull, xempty, esm, pbuf,
+                                       flags, xcnt, warp, et, lane, l == K.trace_layer ? tr : nullptr);
+                    // warpgroup 2's attention stores are fenced before this barrier too
+                    fence_proxy_async_global();
+                    __threadfence();
+                    att_sync();
                     if (tr && l == K.trace_layer && et == 0) tr[17] = gtimer();
                 } else {
                     const int q = pk_gp(p);
@@ -1070,13 +1155,16 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     epi_sync();
                     if (p == 0)
                         pk_gemm_epilogue<EPI_QKV>(P, K, E, q, meta, esm, flags, tfull, tempty, tmem_base, acnt, et, warp,
-                                                     l == K.trace_layer ? tr : nullptr);
+                                                     l == K.trace_layer ? tr : nullptr, ((step_tag * 128u + (uint32_t)l) << 3) + (uint32_t)q + 1u,
+                                                     red_bar, red_ph, xring);
                     else if (p == 3)
                         pk_gemm_epilogue<EPI_SWIGLU>(P, K, E, q, meta, esm, flags, tfull, tempty, tmem_base, acnt, et, warp,
-                                                     l == K.trace_layer ? tr : nullptr);
+                                                     l == K.trace_layer ? tr : nullptr, ((step_tag * 128u + (uint32_t)l) << 3) + (uint32_t)q + 1u,
+                                                     red_bar, red_ph, xring);
                     else
                         pk_gemm_epilogue<EPI_RESID>(P, K, E, q, meta, esm, flags, tfull, tempty, tmem_base, acnt, et, warp,
-                                                     l == K.trace_layer ? tr : nullptr);
+                                                     l == K.trace_layer ? tr : nullptr, ((step_tag * 128u + (uint32_t)l) << 3) + (uint32_t)q + 1u,
+                                                     red_bar, red_ph, xring);
                 }
                 // phase done: every store of this CTA's phase work is visible (generic and to
                 // the async proxy that the next phase's TMA loads use) before the counter moves
@@ -1087,6 +1175,30 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                     if (tr && l == K.trace_layer) tr[8 + p] = gtimer();
                     red_release_gpu_add(K.done + l * kPkPhases + p, 1);
                 }
+            }
+        }
+    }
+    else {
+        // ===================== WG2: attention warps 8-11 =====================
+        const int at = threadIdx.x - 128;  // 128..255 among the attention threads
+        long long u0, u1;
+        pk_att_range(att_pre, att_nch, Bp, U, nseg, cta, Gc, u0, u1);
+        uint32_t xcnt = 0;
+        for (int l = 0; l < L; ++l) {
+            for (int p = 0; p < kPkPhases; ++p) {
+                if (p != 1) {
+                    long long a0, a1;
+                    pk_share((long long)K.g[pk_gp(p)].tiles * K.g[pk_gp(p)].kblocks, cta, Gc, a0, a1);
+                    xcnt += (uint32_t)(a1 - a0);
+                    continue;
+                }
+                if (at == 128) pk_wait_done(K.done + l * kPkPhases, Gc, K.err, 0x601 | (l << 12));
+                named_bar_sync(kWg2Bar, 128);
+                pk_attention_phase(P, K, u0, u1, U, att_pre, att_nch, att_nkeys, xring, xfull, xempty, esm, pbuf,
+                                   flags, xcnt, warp - 4, at, lane, nullptr);
+                fence_proxy_async_global();
+                __threadfence();
+                att_sync();
             }
         }
     }

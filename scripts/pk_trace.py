@@ -39,8 +39,10 @@ def colz(i):
     v = v[v > 0]
     v = (v - t0) / 1e3
     return f"n={len(v)} {v.min():7.2f} {v.mean():7.2f} {v.max():7.2f}" if len(v) else "none"
-print("  last shared seg: reds issued", colz(5), "| fence+ticket", colz(6), "| last-arriver epi done", colz(7))
-print("  last-arriver epilogues per CTA:", np.bincount(t[:, 13].astype(int)), " sole per CTA:", np.bincount(t[:, 14].astype(int)))
+red = t[:, 5] > 0
+print("  reducers n=%d: acc received -> tags ok %.2f | chunk0 copies %.2f | chunk0 epi %.2f | chunk1 copies %.2f | chunk1 epi %.2f us (avg deltas)" % (
+    red.sum(), *(np.mean((t[red, b_] - t[red, a_]) / 1e3) for a_, b_ in ((15, 5), (5, 6), (6, 7), (7, 13), (13, 14)))))
+print("  reducers: acc received at %.2f avg, done at %.2f avg / %.2f max" % (((t[red, 15] - t0) / 1e3).mean(), ((t[red, 14] - t0) / 1e3).mean(), ((t[red, 14] - t0) / 1e3).max()))
 print("attention per CTA (us, avg/max): wait xfull %.2f/%.2f  page compute(warp0) %.2f/%.2f  q load %.2f/%.2f  finish %.2f/%.2f  runs %.1f units %.1f" % (
     t[:, 21].mean() / 1e3, t[:, 21].max() / 1e3, t[:, 22].mean() / 1e3, t[:, 22].max() / 1e3, t[:, 23].mean() / 1e3,
     t[:, 23].max() / 1e3, t[:, 29].mean() / 1e3, t[:, 29].max() / 1e3, t[:, 30].mean(), t[:, 31].mean()))
