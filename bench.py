@@ -456,7 +456,12 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--latency-only", default="", help="comma list of workloads: run only the latency A/B")
     ap.add_argument("--latency-batch", type=int, default=0, help="override every workload's batch")
+    ap.add_argument("--fig6", action="store_true", help="NEXT-4: Fig. 6 tool/decode ratio sweep on the engine")
+    ap.add_argument("--fig6-batch", type=int, default=16)
     args = ap.parse_args()
+    if args.fig6:
+        print(json.dumps({"fig6": run_fig6(args.fig6_batch, verbose=True)}), flush=True)
+        return
     if args.latency_only:
         ws = args.latency_only.split(",")
         base = {"codegen": 64, "search": 128, "planning": 256, "validation": 512}
@@ -514,6 +519,54 @@ def run_latency(workloads, batches, device=0, verbose=False):
         out[w] = res
     eng.close()
     return out
+
+
+# ------------------------------------------------------------------ NEXT-4: Fig. 6 sweep
+def run_fig6(B, ratios=(0.1, 0.25, 0.5, 1.0, 2.0, 4.0, 10.0), n_lines=12, device=0, verbose=False, shape=None):
+    """PAPER.md:240-242 (Fig. 6): latency improvement of tool partial execution as a function of
+    the tool/decode time ratio r = t_i/g_i, measured on the engine.  Each request decodes one
+    round of n_lines lines on the 7B-shape engine; line j's tool cost is r x its share of the
+    round's decode time (per-token decode time calibrated by a cost-free Sequential run).
+    Reported per r: the measured ratio r_meas = mean t / mean g, the paper's best case
+    (1 + r)/max(1, r) - 1 = min(r, 1/r) at r_meas (g_{n+1} = 0: the request ends with its
+    tools), and the measured improvement L_seq/L_par - 1."""
+    import numpy as np
+    from inputs.configs import MISTRAL_7B
+    from inputs.tool_workloads import build_sweep
+    from inputs.vocab import synthetic_vocab
+    from paper_2406_00059_b200 import capi
+    from paper_2406_00059_b200.engine import DeviceModel, Engine
+    from paper_2406_00059_b200.runtime import Runtime
+    dm = DeviceModel(shape or MISTRAL_7B, "bf16", B * 24 + 64, seed=1003, device=device)
+    eng = Engine(dm, synthetic_vocab(32000), max_slots=B, max_pages_per_slot=20, device=device)
+    tool = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n"])
+
+    def run(r, mode, tok_s):
+        _, specs, ntok = build_sweep(B, tool, r, tok_s, n_lines)
+        rt = Runtime(eng, mode)
+        logs = rt.run(specs)
+        lat = float(np.mean([lg.t_done - lg.t_submit for lg in logs]))
+        g = float(np.mean([lg.round_final[0] - lg.round_start[0] for lg in logs]))
+        t = float(np.mean([sum(w.cost_s for w in lg.seg_work[0]) for lg in logs]))
+        return lat, g, t, ntok
+
+    _, g0, _, ntok = run(0.0, capi.MODE_SEQUENTIAL, 0.0)   # warm-up + calibration
+    _, g0, _, ntok = run(0.0, capi.MODE_SEQUENTIAL, 0.0)
+    tok_s = g0 / ntok
+    rows = []
+    for r in ratios:
+        lp, gp, tp, _ = run(r, capi.MODE_PARTIAL, tok_s)
+        ls, gs, ts, _ = run(r, capi.MODE_SEQUENTIAL, tok_s)
+        r_meas = 0.5 * (tp / gp + ts / gs)
+        row = {"r": r, "r_meas": r_meas, "theory": (1.0 + r_meas) / max(1.0, r_meas) - 1.0,
+               "measured": ls / lp - 1.0, "L_par_ms": lp * 1e3, "L_seq_ms": ls * 1e3, "g_ms": gp * 1e3,
+               "t_ms": tp * 1e3}
+        rows.append(row)
+        if verbose:
+            print(json.dumps(row), flush=True)
+    eng.close()
+    return {"batch": B, "lines_per_round": n_lines, "tokens_per_round": ntok, "decode_ms_per_token": tok_s * 1e3,
+            "rows": rows}
 
 
 if __name__ == "__main__":

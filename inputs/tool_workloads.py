@@ -14,6 +14,9 @@ PAPER.md:119); these distributions are calibration knobs, identical in both mode
               stage 3; answer 60 tokens.
   validation: one 12-member JSON call (JSON_MEMBER parser), validator 0.05 ms per member;
               a `location` member without ", ST" aborts the request.
+  sweep     : NEXT-4 / Fig. 6: one round of n lines through the interpreter
+              stub, each line costing r x (its share of the round's decode time), so that the
+              round's tool time t = r x g for a chosen ratio r; one serial instance.
 No method arithmetic lives here.
 """
 from __future__ import annotations
@@ -139,3 +142,34 @@ def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
 
 TOOLS = {"interp": ("PARSER_LITERAL", [b"\n"]), "search": ("PARSER_LITERAL", [b"\n"]),
          "planner": ("PARSER_JSON_OBJECT", []), "validator": ("PARSER_JSON_MEMBER", [])}
+
+
+def build_sweep(B: int, tool_id: int, r: float, tok_s: float, n_lines: int = 24, seed: int = 3000):
+    """Fig. 6 sweep requests (NEXT-4): every request decodes n_lines lines; line j costs
+    r * tok_s * (tokens attributed to line j), tokens attributed in proportion to bytes, so the
+    round's tool time is r times its decode time at a per-token decode time tok_s (measured on
+    the engine by the caller).  Returns (vocab, [RequestSpec], tokens_per_round)."""
+    from paper_2406_00059_b200.runtime import RequestSpec, Round, SegmentWork
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    specs = []
+    n_tok = 0
+    for b in range(B):
+        rng = random.Random(seed * 100003 + b)
+        lines = []
+        for j in range(n_lines):
+            v = "x%d" % rng.randrange(100)
+            lines.append(rng.choice([f"{v} = compute({rng.randrange(1000)}, {rng.randrange(1000)})",
+                                     f"print({v} + {rng.randrange(100)})",
+                                     f"{v} = np.mean(data[{rng.randrange(64)}:])"]))
+        text = "\n".join(lines) + "\n"
+        ids = tok.encode(text)
+        n_tok += len(ids)
+        per_byte = tok_s * len(ids) / len(text.encode())
+        costs = [r * per_byte * (len(ln) + 1) for ln in lines]
+
+        def plan(j, data, costs=costs):
+            return SegmentWork(costs[j] if j < len(costs) else 0.0, 0)
+        specs.append(RequestSpec([1, rng.randrange(259, 32000)], [Round(ids, tool_id, plan)], synth_prefix=64,
+                                 synth_seed=b))
+    return vocab, specs, n_tok / max(1, B)

@@ -248,10 +248,24 @@ class Runtime:
         return logs
 
 
-def summarize(logs, mode: int, des_check: bool = True):
-    """Per-request latency (submit -> completion) stats and the DES recomputation."""
+def round_timelines(log: RequestLog):
+    """Per round of one request: decode time g (round start -> FINAL polled) and the logged
+    segments as (availability offset, cost, instance, deps) -- the inputs of the paper's
+    latency model, for an external schedule cross-check."""
+    rounds = []
+    for i in range(len(log.round_start)):
+        g = (log.round_final[i] - log.round_start[i]) if log.round_final[i] else 0.0
+        segs = [(a - log.round_start[i], w.cost_s, w.instance, list(w.deps))
+                for a, w in zip(log.seg_avail[i], log.seg_work[i])]
+        rounds.append({"g": g, "segs": segs})
+    return rounds
+
+
+def summarize(logs, mode: int, des=None):
+    """Per-request latency (submit -> completion) stats.  `des`, if given, is a schedule model
+    callable(rounds, partial) -> (latency_s, detail) recomputing each request from its logged
+    timeline (the tests pass the oracle's O-3 DES); the max deviation is reported."""
     import numpy as np
-    from oracle.latency import Segment, request_latency  # test/measurement infrastructure only
     lat = np.array([(lg.t_done - lg.t_submit) * 1e3 for lg in logs])
     out = {"n": len(logs), "mean_ms": float(lat.mean()), "std_ms": float(lat.std()),
            "p50_ms": float(np.percentile(lat, 50)), "p95_ms": float(np.percentile(lat, 95))}
@@ -259,21 +273,13 @@ def summarize(logs, mode: int, des_check: bool = True):
     if det:
         out["detection_ms_mean"] = float(np.mean(det))
         out["aborted"] = len(det)
-    if des_check:
+    if des is not None:
         errs = []
         for lg in logs:
             if lg.t_abort is not None:
                 continue
-            rounds = []
-            for i in range(len(lg.round_start)):
-                g = (lg.round_final[i] - lg.round_start[i]) if lg.round_final[i] else 0.0
-                segs = [Segment(a - lg.round_start[i], w.cost_s, w.instance, list(w.deps))
-                        for a, w in zip(lg.seg_avail[i], lg.seg_work[i])]
-                rounds.append({"g": g, "segs": segs})
-            # the DES recomputes the request from the logged availability times and costs
-            # (oracle/latency.py, O-3); it must agree within one poll quantum + one step
-            des, _ = request_latency(rounds, partial=(mode == capi.MODE_PARTIAL))
-            errs.append(abs(des - (lg.t_done - lg.t_submit)))
+            model, _ = des(round_timelines(lg), mode == capi.MODE_PARTIAL)
+            errs.append(abs(model - (lg.t_done - lg.t_submit)))
         if errs:
             out["des_max_abs_err_ms"] = float(max(errs) * 1e3)
     return out

@@ -104,6 +104,13 @@ class FakeEngine:
         pass
 
 
+def oracle_des(rounds, partial):
+    """The runtime's logged timelines through the oracle's O-3 schedule (oracle/latency.py)."""
+    from oracle.latency import Segment, request_latency
+    rr = [{"g": r["g"], "segs": [Segment(a, c, i, d) for a, c, i, d in r["segs"]]} for r in rounds]
+    return request_latency(rr, partial)
+
+
 def run(workload, B, mode):
     from inputs.vocab import synthetic_vocab
     vocab = synthetic_vocab(32000)
@@ -113,7 +120,7 @@ def run(workload, B, mode):
     _, specs = build(workload, B, ids, seed=9)
     rt = Runtime(eng, mode)
     logs = rt.run(specs, timeout_s=120)
-    return logs, summarize(logs, mode)
+    return logs, summarize(logs, mode, des=oracle_des)
 
 
 @pytest.mark.parametrize("workload", ["codegen", "search", "planning"])
@@ -143,3 +150,28 @@ def test_codegen_only_last_line_after_decode(monkeypatch):
         # every tool segment but the tail of the script finished before/near the FINAL
         late = [e for e in ends if e > final + 0.05]
         assert len(late) <= 2
+
+
+# ------------------------------------------------------------------ NEXT-4: Fig. 6 sweep
+def test_sweep_builder_tool_time_is_r_times_decode_time():
+    """build_sweep assigns line costs so a round's tool time is r x its decode time at the
+    given per-token time (tokens attributed by bytes): sum of costs == r * tok_s * tokens."""
+    from inputs.tool_workloads import build_sweep
+    for r in (0.1, 1.0, 7.0):
+        _, specs, _ = build_sweep(3, 0, r, 0.002, n_lines=10)
+        for sp in specs:
+            rd = sp.rounds[0]
+            total = sum(rd.plan(j, b"").cost_s for j in range(10))
+            assert abs(total - r * 0.002 * len(rd.forced)) < 1e-12 + 1e-9 * total
+
+
+@pytest.mark.gpu
+def test_fig6_sweep_on_engine_below_theory():
+    """NEXT-4 on a 2-layer 7B slice: measured improvement L_seq/L_par - 1 stays below the
+    paper's best case min(r, 1/r) and reaches a good part of it."""
+    import bench
+    from inputs.configs import MISTRAL_7B, slice_of
+    out = bench.run_fig6(4, ratios=(0.5, 1.0, 3.0), n_lines=8, shape=slice_of(MISTRAL_7B, L=2, name="7b-L2"))
+    for row in out["rows"]:
+        assert row["measured"] <= row["theory"] + 0.05, row
+        assert row["measured"] >= 0.4 * row["theory"], row
