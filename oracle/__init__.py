@@ -160,9 +160,56 @@ def argmax(logits: np.ndarray) -> int:
     return lib().orc_argmax(_dp(x), x.shape[0])
 
 
-PARSER_LITERAL, PARSER_JSON_MEMBER, PARSER_JSON_OBJECT = 0, 1, 2
-FLAG_FINAL, FLAG_OVERFLOW, FLAG_CANCELLED = 1, 2, 4
+PARSER_LITERAL, PARSER_JSON_MEMBER, PARSER_JSON_OBJECT, PARSER_FENCE = 0, 1, 2, 3
+FLAG_FINAL, FLAG_OVERFLOW, FLAG_CANCELLED, FLAG_OPEN, FLAG_CLOSE = 1, 2, 4, 8, 16
 DELIM_NONE = 0xFFFF
+
+
+def fence_records(tag: bytes, max_seg: int, S: bytes):
+    """FENCE region grammar (NEXT-2; reading R21) -- the paper's CodeGen indicators:
+    "We use the markdown code block syntax ```python and ``` as the indicators for the start
+    and end of the tool"; a complete line of code inside is one partial-
+    execution piece ("a complete line of Python code is decoded").
+
+    Plain definition, step by step:
+      1. Line units: S is cut after every '\n' byte; a run of max_seg bytes without '\n' is
+         cut too (an overflow unit), and the rest of that line is a continuation unit.
+      2. A unit is a marker only if it starts a line (is not a continuation): the open marker
+         is exactly b"```" + tag + b"\n", the close marker exactly b"```\n".
+      3. Walking the units in order with a region flag (initially outside):
+           outside: the open marker -> OPEN record, region opens; anything else -> nothing;
+           inside:  the close marker -> CLOSE record, region closes;
+                    any other '\n'-terminated unit -> piece record (delim_id 0);
+                    an overflow unit -> piece record with OVERFLOW (delim_id NONE).
+      4. The trailing incomplete unit (no '\n', shorter than max_seg) is left for FINAL.
+    Returns (records [(start, end, delim_id, flags)], start of the trailing unit)."""
+    open_m, close_m = b"```" + tag + b"\n", b"```\n"
+    units = []          # (start, end, ends_with_newline, is_continuation)
+    start, cont = 0, False
+    for i in range(len(S)):
+        if S[i] == 0x0A:
+            units.append((start, i + 1, True, cont))
+            start, cont = i + 1, False
+        elif i + 1 - start == max_seg:
+            units.append((start, i + 1, False, cont))
+            start, cont = i + 1, True
+    recs = []
+    inside = False
+    for (a, b, nl, c) in units:
+        u = S[a:b]
+        if not inside:
+            if nl and not c and u == open_m:
+                recs.append((a, b, 0, FLAG_OPEN))
+                inside = True
+        else:
+            if nl and not c and u == close_m:
+                recs.append((a, b, 0, FLAG_CLOSE))
+                inside = False
+            elif nl:
+                recs.append((a, b, 0, 0))
+            else:
+                recs.append((a, b, DELIM_NONE, FLAG_OVERFLOW))
+    return recs, start
 
 
 def segment(kind: int, delims: list[bytes], max_seg: int, stream: bytes):

@@ -8,7 +8,7 @@ device scan must publish (R5-R13), following SURVEY.md 8(c) O-2 steps 
      SPEC.md:102); e_t = sum_{s<=t} |T[y_s]|.
   2./3. cuts from oracle.segment (plain definition).
   4. round end (EOS, max_new_tokens, forced-stream end, cancel): one FINAL record
-     for the tail S[c_last, |S|), possibly empty.
+     for the tail S[c_last, |S|), possibly empty (FENCE: the trailing incomplete line).
   token_index of a cut = min{t : e_t >= c_j} - 1 (0-based index of the generated
   token holding the cut's last byte: "emit completed pieces ... immediately",
   PAPER.md:144).  FINAL carries N-1 (0xFFFFFFFF when the round generated nothing).
@@ -17,7 +17,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from . import DELIM_NONE, FLAG_CANCELLED, FLAG_FINAL, segment
+from . import DELIM_NONE, FLAG_CANCELLED, FLAG_FINAL, PARSER_FENCE, fence_records, segment
 
 NO_TOKEN = 0xFFFFFFFF
 
@@ -58,7 +58,17 @@ def round_records(tokens, vocab_bytes, kind: int, delims: list[bytes], max_seg: 
     recs = []
     c_prev = 0
     seq = seq_start
-    for (c, did, fl) in segment(kind, delims, max_seg, S):
+    if kind == PARSER_FENCE:
+        # region grammar: records need not tile S (text outside a region is not tool input)
+        fr, c_prev = fence_records(delims[0], max_seg, S)
+        for (a, c, did, fl) in fr:
+            t1 = next(t for t, e in enumerate(ends) if e >= c)
+            recs.append(Record(round_idx, seq, t1, a, c - a, did, fl, S[a:c]))
+            seq += 1
+        cuts = []
+    else:
+        cuts = segment(kind, delims, max_seg, S)
+    for (c, did, fl) in cuts:
         t1 = next(t for t, e in enumerate(ends) if e >= c)  # min{t : e_t >= c} - 1 (0-based)
         recs.append(Record(round_idx, seq, t1, c_prev, c - c_prev, did, fl, S[c_prev:c]))
         seq += 1

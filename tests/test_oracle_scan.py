@@ -254,3 +254,116 @@ def test_four_stage_plan_gives_four_object_cuts():
     for (e, did, fl), line in zip(cuts, S.split(b"\n")):
         assert did == 1 and fl == 0
     assert [json.loads(x) for x in S.decode().strip().split("\n")][3]["id"] == 4
+
+
+# ------------------------------------------------------------------ FENCE region grammar (NEXT-2)
+FEN = oracle.PARSER_FENCE
+
+
+def regex_fence(S: bytes, tag: bytes):
+    """Independent reading of the fence grammar without overflow: split S into '\\n'-terminated
+    lines with a regex, then pair markers with a running flag."""
+    recs, inside = [], False
+    for m in re.finditer(rb"[^\n]*\n", S):
+        a, b, line = m.start(), m.end(), m.group(0)
+        if not inside and line == b"```" + tag + b"\n":
+            recs.append((a, b, 0, oracle.FLAG_OPEN))
+            inside = True
+        elif inside and line == b"```\n":
+            recs.append((a, b, 0, oracle.FLAG_CLOSE))
+            inside = False
+        elif inside:
+            recs.append((a, b, 0, 0))
+    tail = S.rfind(b"\n") + 1
+    return recs, tail
+
+
+def test_fence_bruteforce_equals_regex_reading():
+    """Every string up to length 9 over {`, p, \\n, a} (tag 'p': markers "```p\\n" / "```\\n")."""
+    n = 0
+    for S in all_strings([b"`", b"p", b"\n", b"a"], 9):
+        assert oracle.fence_records(b"p", BIG, S) == regex_fence(S, b"p"), S
+        n += 1
+    assert n == sum(4 ** k for k in range(10))
+
+
+def test_fence_paper_codegen_script_13_pieces():
+    """the ```python / ``` indicators delimit the tool; lines 1-13 of the
+    script are pieces; prose before/after the block is not tool input."""
+    S = ("Here is the code.\n```python\n" + SINE_SCRIPT_13 + "```\nIt saves sine.png").encode()
+    recs, tail = oracle.fence_records(b"python", 4096, S)
+    assert [f for (_, _, _, f) in recs] == [oracle.FLAG_OPEN] + [0] * 13 + [oracle.FLAG_CLOSE]
+    lines = SINE_SCRIPT_13.encode().splitlines(keepends=True)
+    assert [S[a:b] for (a, b, _, f) in recs if f == 0] == lines
+    assert S[tail:] == b"It saves sine.png"
+
+
+def test_fence_other_tags_and_nesting_are_text():
+    S = b"```bash\nls\n```\n```python\nx=1\n```python\n```\ny\n"
+    recs, _ = oracle.fence_records(b"python", 4096, S)
+    # the bash block is prose; inside the python block a second opener is just a line
+    assert [(S[a:b], f) for (a, b, _, f) in recs] == [
+        (b"```python\n", oracle.FLAG_OPEN), (b"x=1\n", 0), (b"```python\n", 0), (b"```\n", oracle.FLAG_CLOSE)]
+
+
+def test_fence_overflow_inside_and_outside():
+    S = b"aaaaaaa\n```p\nbbbbbbbbbbbbb\n```\ncc"
+    recs, tail = oracle.fence_records(b"p", 6, S)
+    # outside: overflow units emit nothing; inside: OVERFLOW pieces, then the line's rest
+    assert [(S[a:b], d, f) for (a, b, d, f) in recs] == [
+        (b"```p\n", 0, oracle.FLAG_OPEN), (b"bbbbbb", oracle.DELIM_NONE, oracle.FLAG_OVERFLOW),
+        (b"bbbbbb", oracle.DELIM_NONE, oracle.FLAG_OVERFLOW), (b"b\n", 0, 0), (b"```\n", 0, oracle.FLAG_CLOSE)]
+    assert S[tail:] == b"cc"
+    # a continuation unit never matches a marker even if its bytes do
+    recs2, _ = oracle.fence_records(b"p", 6, b"xxxxxx```p\nq\n")
+    assert recs2 == []
+    # a marker longer than max_seg can never open a region
+    assert oracle.fence_records(b"p", 4, b"```p\nx\n")[0] == []
+
+
+def test_fence_invariants_random():
+    rng = random.Random(11)
+    alpha = [b"`", b"p", b"\n", b"a", b"```p\n", b"```\n"]
+    for _ in range(3000):
+        S = b"".join(rng.choice(alpha) for _ in range(rng.randrange(0, 24)))
+        M = rng.choice([3, 5, 8, BIG])
+        recs, tail = oracle.fence_records(b"p", M, S)
+        ends = [b for (_, b, _, _) in recs]
+        assert ends == sorted(ends) and all(b <= tail for b in ends)
+        depth = 0
+        for (a, b, d, f) in recs:
+            assert 0 < b - a <= M
+            if f == oracle.FLAG_OPEN:
+                assert depth == 0 and S[a:b] == b"```p\n"
+                depth = 1
+            elif f == oracle.FLAG_CLOSE:
+                assert depth == 1 and S[a:b] == b"```\n"
+                depth = 0
+            else:
+                assert depth == 1
+                assert (f == 0 and S[b - 1:b] == b"\n") or (f == oracle.FLAG_OVERFLOW and b - a == M)
+        assert b"\n" not in S[tail:] and len(S) - tail < M
+
+
+@pytest.mark.parametrize("L", range(1, 8))
+def test_fence_token_index_every_tokenization(L):
+    vocab = {}
+    rng = random.Random(100 + L)
+    strings = [s for s in all_strings([b"`", b"p", b"\n", b"a"], L) if len(s) == L]
+    strings = [b"```p\n" + s + b"\n```\n" for s in rng.sample(strings, min(60, len(strings)))]
+    for S in strings:
+        base, tail = oracle.fence_records(b"p", BIG, S)
+        n = len(S)
+        for _ in range(40):
+            cut = sorted(rng.sample(range(1, n), rng.randrange(0, min(6, n - 1))))
+            bounds = [0] + cut + [n]
+            pieces = [S[bounds[i]:bounds[i + 1]] for i in range(len(bounds) - 1)]
+            ids = [vocab.setdefault(p, len(vocab)) for p in pieces]
+            table = {v: k for k, v in vocab.items()}
+            recs, stream = round_records(ids, table, FEN, [b"p"], BIG)
+            assert stream == S
+            assert [(r.byte_offset, r.byte_offset + r.byte_len, r.delim_id, r.flags) for r in recs[:-1]] == base
+            for r in recs[:-1]:
+                last = r.byte_offset + r.byte_len - 1
+                assert r.token_index == max(i for i in range(len(pieces)) if bounds[i] <= last)
+            assert recs[-1].byte_offset == tail and recs[-1].flags == oracle.FLAG_FINAL
