@@ -464,7 +464,7 @@ def main():
         return
     if args.latency_only:
         ws = args.latency_only.split(",")
-        base = {"codegen": 64, "search": 128, "planning": 256, "validation": 512}
+        base = {"codegen": 64, "codegen_fence": 64, "search": 128, "planning": 256, "validation": 512}
         bs = {w: (args.latency_batch or base[w]) for w in ws}
         print(json.dumps({"latency": run_latency(ws, bs, verbose=True)}), flush=True)
         return
@@ -488,8 +488,8 @@ def run_latency(workloads, batches, device=0, verbose=False):
     from paper_2406_00059_b200 import capi
     from paper_2406_00059_b200.engine import DeviceModel, Engine
     from paper_2406_00059_b200.runtime import Runtime, summarize
-    prefixes = {"codegen": 128, "search": 256, "planning": 512, "validation": 1792}
-    max_tokens = {"codegen": 440, "search": 560, "planning": 400, "validation": 320}
+    prefixes = {"codegen": 128, "codegen_fence": 128, "search": 256, "planning": 512, "validation": 1792}
+    max_tokens = {"codegen": 440, "codegen_fence": 460, "search": 560, "planning": 400, "validation": 320}
     pages_per = {w: (prefixes[w] + max_tokens[w] + 31) // 16 + 1 for w in workloads}
     need = max(batches[w] * pages_per[w] for w in workloads) + 64
     dm = DeviceModel(MISTRAL_7B, "bf16", need, seed=1002, device=device)

@@ -63,13 +63,26 @@ typedef enum { CVY_DTYPE_BF16 = 0, CVY_DTYPE_FP32 = 1 } cvy_dtype;
  * JSON_MEMBER: a ',' at depth 1 or the bracket closing depth 1 ends a segment
  *          ("field complete", validator).
  * JSON_OBJECT: the bracket returning depth to 0 ends a segment ("a complete stage of the
- *          plan"). */
-typedef enum { CVY_PARSER_LITERAL = 0, CVY_PARSER_JSON_MEMBER = 1, CVY_PARSER_JSON_OBJECT = 2 } cvy_parser_kind;
+ *          plan").
+ * FENCE:   region grammar (R21): the line "```" TAG "\n" opens the tool region and
+ *          the line "```\n" closes it ("the markdown code block syntax ```python and ``` as the
+ *          indicators for the start and end of the tool"); every line inside is
+ *          one segment ("a complete line of Python code").  Lines outside a
+ *          region are not tool input and produce no record; the open / close marker lines are
+ *          records flagged CVY_SEG_OPEN / CVY_SEG_CLOSE.  TAG = the single delimiter (1..8
+ *          bytes, no '\n').  A line reaching max_segment_bytes is cut (OVERFLOW inside a
+ *          region, silently outside); its continuation is never a marker. */
+typedef enum {
+    CVY_PARSER_LITERAL = 0,
+    CVY_PARSER_JSON_MEMBER = 1,
+    CVY_PARSER_JSON_OBJECT = 2,
+    CVY_PARSER_FENCE = 3
+} cvy_parser_kind;
 
 /* Host dispatch policy only; the device path is identical in both modes. */
 typedef enum { CVY_MODE_PARTIAL = 0, CVY_MODE_SEQUENTIAL = 1 } cvy_exec_mode;
 
-enum { CVY_SEG_FINAL = 1, CVY_SEG_OVERFLOW = 2, CVY_SEG_CANCELLED = 4 };
+enum { CVY_SEG_FINAL = 1, CVY_SEG_OVERFLOW = 2, CVY_SEG_CANCELLED = 4, CVY_SEG_OPEN = 8, CVY_SEG_CLOSE = 16 };
 #define CVY_DELIM_NONE 0xFFFFu
 #define CVY_NO_TOKEN 0xFFFFFFFFu
 
@@ -153,7 +166,9 @@ const char* cvy_last_error(void);
 int32_t cvy_abi_version(void);
 
 /* Tool registration (before the first submit).  LITERAL: 1..8 distinct delimiters of
- * 1..8 bytes each.  JSON kinds take no delimiters.  max_segment_bytes 0 => 4096.
+ * 1..8 bytes each.  JSON kinds take no delimiters.  FENCE: exactly one delimiter = the
+ * fence tag (1..8 bytes, no '\n'); max_segment_bytes must be >= tag length + 4 (the open
+ * marker line must fit one segment).  max_segment_bytes 0 => 4096.
  * Errors: E_DUP name clash, E_INVAL bad delimiters, E_STATE after the first submit,
  * E_FULL more than 64 tools. */
 typedef struct {

@@ -3,7 +3,8 @@ with seeded tool-stub cost models (SURVEY.md 8(d) "Configs res
 
 The paper gives no per-line or per-call tool costs (its Fig. 3 blocks are "not to scale",
 PAPER.md:119); these distributions are calibration knobs, identical in both modes:
-  codegen   : Python-interpreter stub, one serial instance; a line costs U(50,300) ms if it
+  codegen   : Python-interpreter stub, one serial instance (codegen_fence: the same inside a
+              ```python block between prose, FENCE parser); a line costs U(50,300) ms if it
               imports, U(300,600) ms for the final render line, U(1,20) ms otherwise; a `:`
               block is buffered until its closing blank line.
   search    : 3 `search("...")` lines, each followed by the code drafted for that language
@@ -117,6 +118,13 @@ def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
             text = codegen_script(rng, 40)
             rounds = [Round(tok.encode(text)[:420], tool_ids["interp"], _codegen_plan(rng))]
             prefix = 128
+        elif workload == "codegen_fence":
+            # the paper's own indicators: prose, a ```python block, prose; the
+            # FENCE parser (NEXT-2) sends only the block's lines to the interpreter
+            text = ("Here is the script.\n```python\n" + codegen_script(rng, 36) + "```\n" +
+                    "It draws the sine wave and saves the figure to sine.png.")
+            rounds = [Round(tok.encode(text)[:440], tool_ids["interp_fence"], _codegen_plan(rng))]
+            prefix = 128
         elif workload == "search":
             r0 = tok.encode(search_session(rng, 3))
             obs = tok.encode("\n[OBSERVATION search]\n" + prose(rng, 60) + "\n")[:96]
@@ -140,7 +148,8 @@ def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
     return vocab, specs
 
 
-TOOLS = {"interp": ("PARSER_LITERAL", [b"\n"]), "search": ("PARSER_LITERAL", [b"\n"]),
+TOOLS = {"interp": ("PARSER_LITERAL", [b"\n"]), "interp_fence": ("PARSER_FENCE", [b"python"]),
+         "search": ("PARSER_LITERAL", [b"\n"]),
          "planner": ("PARSER_JSON_OBJECT", []), "validator": ("PARSER_JSON_MEMBER", [])}
 
 

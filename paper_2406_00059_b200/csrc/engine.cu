@@ -665,6 +665,23 @@ cvy_status cvy_register_tool(cvy_engine* e, const cvy_tool_desc* t, int32_t* too
         td.n_delims = (int32_t)t->n_delims;
     } else if (t->parser == CVY_PARSER_JSON_MEMBER || t->parser == CVY_PARSER_JSON_OBJECT) {
         if (t->n_delims != 0) return fail(CVY_E_INVAL, "JSON parsers take no delimiters");
+    } else if (t->parser == CVY_PARSER_FENCE) {
+        // the open marker line "```" TAG "\n" packed little-endian into dpack[0..1]
+        if (t->n_delims != 1 || !t->delims || !t->delim_lens || !t->delims[0])
+            return fail(CVY_E_INVAL, "FENCE takes exactly one delimiter: the fence tag");
+        const uint32_t L = t->delim_lens[0];
+        if (L < 1 || L > 8) return fail(CVY_E_INVAL, "fence tag length must be 1..8");
+        uint8_t marker[16] = {'`', '`', '`'};
+        for (uint32_t j = 0; j < L; ++j) {
+            if (t->delims[0][j] == '\n') return fail(CVY_E_INVAL, "fence tag must not contain a newline");
+            marker[3 + j] = t->delims[0][j];
+        }
+        marker[3 + L] = '\n';
+        const int mlen = (int)L + 4;
+        if (td.max_seg < mlen) return fail(CVY_E_INVAL, "max_segment_bytes shorter than the fence open line");
+        for (int k = 0; k < mlen; ++k) td.dpack[k >> 3] |= (uint64_t)marker[k] << (8 * (k & 7));
+        td.dlen[0] = mlen;
+        td.n_delims = 1;
     } else {
         return fail(CVY_E_INVAL, "unknown parser kind");
     }

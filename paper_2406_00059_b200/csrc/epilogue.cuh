@@ -290,6 +290,36 @@ CVY_DEV void scan_byte(SlotDev& s, const ToolDev& t, uint8_t b, uint32_t tok_idx
     const uint32_t p = s.stream_len;
     const uint32_t since = p - s.seg_start;
     int hit = -1;
+    if (t.kind == CVY_PARSER_FENCE) {
+        // region grammar (R21): seg_start = start of the current line unit, depth = inside a
+        // region, esc = mismatch bits (1: not the open marker, 2: not the close marker,
+        // 4: continuation of an overflowed line -- never a marker)
+        const uint32_t k = since - 1;  // index of this byte in the unit
+        const uint32_t olen = (uint32_t)t.dlen[0];
+        if (k >= olen || b != (uint8_t)(t.dpack[k >> 3] >> (8 * (k & 7)))) s.esc |= 1;
+        if (k >= 4 || b != (k < 3 ? (uint8_t)'`' : (uint8_t)'\n')) s.esc |= 2;
+        if (b == '\n') {
+            const bool marker_ok = !(s.esc & 4);
+            if (!s.depth) {
+                if (marker_ok && !(s.esc & 1) && since == olen) {
+                    scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_OPEN);
+                    s.depth = 1;
+                }
+            } else if (marker_ok && !(s.esc & 2) && since == 4) {
+                scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_CLOSE);
+                s.depth = 0;
+            } else {
+                scan_emit(so, s.seg_start, since, tok_idx, 0, 0);
+            }
+            s.seg_start = p;
+            s.esc = 0;
+        } else if ((int)since == t.max_seg) {
+            if (s.depth) scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW);
+            s.seg_start = p;
+            s.esc = 4;
+        }
+        return;
+    }
     if (t.kind == CVY_PARSER_LITERAL) {
         s.win = (s.win << 8) | b;
         const uint32_t avail = since < 8 ? since : 8;

@@ -154,6 +154,8 @@ class Runtime:
         rnd = log.round
         spec_round = log.spec.rounds[rnd]
         is_final = bool(r.flags & capi.SEG_FINAL)
+        if r.flags & (capi.SEG_OPEN | capi.SEG_CLOSE):
+            return  # FENCE region markers are indicators, not tool input
         if not is_final or r.byte_len > 0:
             if spec_round.tool_id >= 0 and spec_round.plan is not None:
                 j = len(log.seg_work[rnd])

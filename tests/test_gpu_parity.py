@@ -230,6 +230,44 @@ def test_vocab32k_all_parsers_bitexact_b64():
     eng.close()
 
 
+def fenced_text(rng, tag="python"):
+    """Prose, a bash block (not the tool's tag), the tool's fenced block with code lines and
+    one very long line, trailing prose (an unterminated last line is the FINAL tail)."""
+    code = codegen_script(rng, rng.randrange(4, 12))
+    long_line = "x = [" + ", ".join(str(rng.randrange(1000)) for _ in range(40)) + "]\n"
+    return ("Sure, here is the plan.\n```bash\npip install torch\n```\n```" + tag + "\n" + code + long_line +
+            "```\nThe figure is saved" + (" as sine.png" if rng.random() < 0.5 else ".\n"))
+
+
+def test_fence_region_grammar_bitexact():
+    """NEXT-2 FENCE parser on the device: byte-level vocab (tiny) and the synthetic 32k vocab
+    (markers split across and inside multi-byte tokens), OPEN / piece / CLOSE records, an
+    OVERFLOW cut inside the region (max_segment_bytes 64), bit-exact vs oracle.fence_records."""
+    for shape, vocab, B in ((TINY, BYTE_VOCAB, 6), (slice_of(TINY, L=2, V=32000, name="tiny-v32k"), synthetic_vocab(32000), 24)):
+        dm, eng = make_engine(shape, "bf16", vocab, B, 1008, max_pages_per_slot=64)
+        t_py = eng.register_tool("py", capi.PARSER_FENCE, [b"python"], max_segment_bytes=64)
+        t_sh = eng.register_tool("sh", capi.PARSER_FENCE, [b"bash"])
+        rng = random.Random(13)
+        reqs, meta = [], []
+        for i in range(B):
+            tag, tool, ms = ("python", t_py, 64) if i % 3 else ("bash", t_sh, 4096)
+            text = fenced_text(rng, "python")
+            if len(vocab) == 256:
+                f = list(text.encode())[:900]
+            else:
+                f = Tokenizer(vocab).encode(text)[:500]
+            reqs.append(([1, 7], f, tool, 1000))
+            meta.append((f, tag.encode(), ms))
+        rids, got = run_forced(eng, reqs)
+        n_open = 0
+        for rid, (f, tag, ms) in zip(rids, meta):
+            exp = expected_records(f, vocab, oracle.PARSER_FENCE, [tag], ms)
+            assert as_tuples(got[rid]) == exp, rid
+            n_open += sum(1 for r in exp if r[6] & oracle.FLAG_OPEN)
+        assert n_open >= B  # every request opened its region
+        eng.close()
+
+
 def test_eos_ends_round_and_multi_round_inject():
     """EOS (id 2, no bytes) ends round 0; the observation is injected and round 1 generates;
     records and seq continue across rounds."""
@@ -330,7 +368,12 @@ def test_tool_registration_errors():
                          (("b", capi.PARSER_LITERAL, []), capi.CVY_E_INVAL),
                          (("c", capi.PARSER_LITERAL, [b"123456789"]), capi.CVY_E_INVAL),
                          (("d", capi.PARSER_LITERAL, [b";", b";"]), capi.CVY_E_INVAL),
-                         (("e", capi.PARSER_JSON_MEMBER, [b","]), capi.CVY_E_INVAL)]:
+                         (("e", capi.PARSER_JSON_MEMBER, [b","]), capi.CVY_E_INVAL),
+                         (("f", capi.PARSER_FENCE, []), capi.CVY_E_INVAL),
+                         (("g", capi.PARSER_FENCE, [b"py", b"sh"]), capi.CVY_E_INVAL),
+                         (("h", capi.PARSER_FENCE, [b"py\n"]), capi.CVY_E_INVAL),
+                         (("i", capi.PARSER_FENCE, [b"pythonpy3"]), capi.CVY_E_INVAL),
+                         (("j", capi.PARSER_FENCE, [b"python"], 8), capi.CVY_E_INVAL)]:
         with pytest.raises(capi.CvyError) as ei:
             eng.register_tool(*args)
         assert ei.value.status == status
