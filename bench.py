@@ -456,6 +456,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--latency-only", default="", help="comma list of workloads: run only the latency A/B")
     ap.add_argument("--latency-batch", type=int, default=0, help="override every workload's batch")
+    ap.add_argument("--latency-inflight", type=int, default=0,
+                    help="NEXT-3 abort-and-refill: run each workload's requests through this many slots")
     ap.add_argument("--fig6", action="store_true", help="NEXT-4: Fig. 6 tool/decode ratio sweep on the engine")
     ap.add_argument("--fig6-batch", type=int, default=16)
     args = ap.parse_args()
@@ -466,7 +468,8 @@ def main():
         ws = args.latency_only.split(",")
         base = {"codegen": 64, "codegen_fence": 64, "search": 128, "planning": 256, "validation": 512}
         bs = {w: (args.latency_batch or base[w]) for w in ws}
-        print(json.dumps({"latency": run_latency(ws, bs, verbose=True)}), flush=True)
+        print(json.dumps({"latency": run_latency(ws, bs, verbose=True, inflight=args.latency_inflight or None)}),
+              flush=True)
         return
     if args.warmup < 3:
         args.warmup = 3
@@ -478,7 +481,7 @@ def main():
 
 
 # ------------------------------------------------------------------ latency: partial vs sequential
-def run_latency(workloads, batches, device=0, verbose=False):
+def run_latency(workloads, batches, device=0, verbose=False, inflight=None):
     """Request completion latency with tool partial execution vs sequential tool execution on
     the four workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool
     costs in both modes (the baseline is the same code with partial execution
@@ -487,13 +490,15 @@ def run_latency(workloads, batches, device=0, verbose=False):
     from inputs.tool_workloads import TOOLS, build
     from paper_2406_00059_b200 import capi
     from paper_2406_00059_b200.engine import DeviceModel, Engine
+    import numpy as np
     from paper_2406_00059_b200.runtime import Runtime, summarize
     prefixes = {"codegen": 128, "codegen_fence": 128, "search": 256, "planning": 512, "validation": 1792}
     max_tokens = {"codegen": 440, "codegen_fence": 460, "search": 560, "planning": 400, "validation": 320}
     pages_per = {w: (prefixes[w] + max_tokens[w] + 31) // 16 + 1 for w in workloads}
-    need = max(batches[w] * pages_per[w] for w in workloads) + 64
+    slots = {w: (inflight or batches[w]) for w in workloads}
+    need = max(slots[w] * pages_per[w] for w in workloads) + 64
     dm = DeviceModel(MISTRAL_7B, "bf16", need, seed=1002, device=device)
-    Bmax = max(batches[w] for w in workloads)
+    Bmax = max(slots[w] for w in workloads)
     from inputs.vocab import synthetic_vocab
     eng = Engine(dm, synthetic_vocab(32000), max_slots=Bmax, max_pages_per_slot=max(pages_per.values()) + 2,
                  device=device)
@@ -504,9 +509,15 @@ def run_latency(workloads, batches, device=0, verbose=False):
         for mode, label in ((capi.MODE_PARTIAL, "partial"), (capi.MODE_SEQUENTIAL, "sequential")):
             _, specs = build(w, batches[w], tool_ids)
             rt = Runtime(eng, mode)
-            logs = rt.run(specs)
+            t0 = time.perf_counter()
+            logs = rt.run(specs, max_inflight=inflight)
             res[label] = summarize(logs, mode)
             res[label]["steps"] = rt.steps
+            if inflight:
+                # abort-and-refill (NEXT-3): makespan of the whole queue through `inflight` slots
+                span = max(lg.t_done for lg in logs) - t0
+                res[label].update(makespan_s=span, requests_per_s=len(logs) / span, slots=inflight,
+                                  queue_latency_mean_ms=float(np.mean([lg.t_done - t0 for lg in logs])) * 1e3)
             if verbose:
                 print(w, label, res[label], flush=True)
         p, s_ = res["partial"]["mean_ms"], res["sequential"]["mean_ms"]
@@ -516,6 +527,8 @@ def run_latency(workloads, batches, device=0, verbose=False):
             d_p, d_s = res["partial"]["detection_ms_mean"], res["sequential"]["detection_ms_mean"]
             res["detection_speedup"] = d_s / d_p - 1.0  # PAPER.md:203 reports 376.4%
         res["batch"] = batches[w]
+        if inflight:
+            res["throughput_gain"] = res["partial"]["requests_per_s"] / res["sequential"]["requests_per_s"] - 1.0
         out[w] = res
     eng.close()
     return out

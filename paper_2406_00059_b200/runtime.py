@@ -67,6 +67,7 @@ class RequestLog:
     pending_tools: int = 0
     final_seen: bool = False
     done: bool = False
+    released: bool = False
 
 
 class Runtime:
@@ -82,6 +83,9 @@ class Runtime:
         self.inst_free = {}        # (req, round, instance) -> t
         self.by_rid = {}
         self.active = 0
+        self.max_inflight = None
+        self.waiting = []
+        self.logs = []
         self.stop = False
         self.steps = 0
 
@@ -127,16 +131,42 @@ class Runtime:
         rnd = log.round
         spec = log.spec
         if log.t_abort is not None or rnd + 1 >= len(spec.rounds):
-            log.done = True
-            log.t_done = now
-            self.active -= 1
-            self.cv.notify_all()
+            self._finish(log, now)
             return
         nxt = spec.rounds[rnd + 1]
         log.round = rnd + 1
         log.final_seen = False
         self._open_round(log, now)
         self.eng.inject_observation(log.rid, spec.rounds[rnd].observation, len(nxt.forced), forced=nxt.forced)
+
+    def _finish(self, log: RequestLog, t_done: float):
+        log.done = True
+        log.t_done = t_done
+        self.active -= 1
+        if self.max_inflight is not None:
+            # abort-and-refill (NEXT-3): the slot and its KV pages go back to the engine now
+            # (applied at the next step boundary) and a waiting request takes them, so an
+            # early abort ("saving the resources ... for decoding subsequent
+            # tokens") turns into throughput
+            self.eng.release_request(log.rid)
+            log.released = True
+            if self.waiting:
+                self._submit(self.waiting.pop(0))
+        self.cv.notify_all()
+
+    def _submit(self, spec: RequestSpec):
+        lg = RequestLog(spec)
+        r0 = spec.rounds[0]
+        lg.t_submit = time.perf_counter()
+        lg.rid = self.eng.submit_request(spec.prompt, len(r0.forced), tool_id=r0.tool_id, mode=self.mode,
+                                         forced=r0.forced, synth_prefix_len=spec.synth_prefix,
+                                         synth_seed=spec.synth_seed,
+                                         reserve_tokens=sum(len(rr.forced) + len(rr.observation) + 2
+                                                            for rr in spec.rounds[1:]) + len(r0.observation))
+        self._open_round(lg, lg.t_submit)
+        self.by_rid[lg.rid] = lg
+        self.logs.append(lg)
+        return lg
 
     def _open_round(self, log: RequestLog, now: float):
         log.round_start.append(now)
@@ -172,10 +202,7 @@ class Runtime:
             log.round_final[rnd] = now
             log.final_seen = True
             if r.flags & capi.SEG_CANCELLED:
-                log.done = True
-                log.t_done = now if log.t_abort is None else log.t_abort
-                self.active -= 1
-                self.cv.notify_all()
+                self._finish(log, now if log.t_abort is None else log.t_abort)
                 return
             if self.mode == capi.MODE_SEQUENTIAL:
                 for j in log.held:
@@ -205,24 +232,20 @@ class Runtime:
                 time.sleep(0.00005)
 
     # ---------------------------------------------------------------- driver
-    def run(self, specs: list[RequestSpec], timeout_s: float = 600.0):
-        logs = []
+    def run(self, specs: list[RequestSpec], timeout_s: float = 600.0, max_inflight: int | None = None):
+        """Run every request to completion.  max_inflight: admit at most this many at a time
+        and refill a slot the moment its request completes or aborts (NEXT-3); None submits
+        everything at t=0 and releases at the end."""
+        self.logs = []
+        self.max_inflight = max_inflight
         t0 = time.perf_counter()
         with self.lock:
-            for spec in specs:
-                lg = RequestLog(spec)
-                r0 = spec.rounds[0]
-                lg.t_submit = time.perf_counter()
-                lg.rid = self.eng.submit_request(spec.prompt, len(r0.forced), tool_id=r0.tool_id, mode=self.mode,
-                                                 forced=r0.forced, synth_prefix_len=spec.synth_prefix,
-                                                 synth_seed=spec.synth_seed,
-                                                 reserve_tokens=sum(len(rr.forced) + len(rr.observation) + 2
-                                                                    for rr in spec.rounds[1:]) +
-                                                 len(r0.observation))
-                self._open_round(lg, lg.t_submit)
-                self.by_rid[lg.rid] = lg
-                logs.append(lg)
-            self.active = len(logs)
+            first = specs if max_inflight is None else specs[:max_inflight]
+            self.waiting = [] if max_inflight is None else list(specs[max_inflight:])
+            for spec in first:
+                self._submit(spec)
+            self.active = len(specs)
+        logs = self.logs
         th = threading.Thread(target=self._poller, daemon=True)
         th.start()
         try:
@@ -246,7 +269,8 @@ class Runtime:
                 self.stop = True
             th.join()
         for lg in logs:
-            self.eng.release_request(lg.rid)
+            if not lg.released:
+                self.eng.release_request(lg.rid)
         return logs
 
 

@@ -175,3 +175,29 @@ def test_fig6_sweep_on_engine_below_theory():
     for row in out["rows"]:
         assert row["measured"] <= row["theory"] + 0.05, row
         assert row["measured"] >= 0.4 * row["theory"], row
+
+
+def test_refill_admits_waiting_requests_and_partial_aborts_free_slots_sooner():
+    """NEXT-3 abort-and-refill on the fake engine: 8 validation requests through 2 slots; every
+    request completes, at most 2 are in flight at any time, and Partial mode (aborts detected
+    at the offending member) finishes the queue sooner than Sequential (detected at FINAL)."""
+    from inputs.vocab import synthetic_vocab
+    vocab = synthetic_vocab(32000)
+    ids = {name: i for i, name in enumerate(TOOLS)}
+    kinds = {i: (getattr(oracle, TOOLS[n][0]), TOOLS[n][1]) for n, i in ids.items()}
+    spans = {}
+    for mode in (capi.MODE_PARTIAL, capi.MODE_SEQUENTIAL):
+        eng = FakeEngine(vocab, kinds)
+        _, specs = build("validation", 8, ids, seed=21)
+        rt = Runtime(eng, mode)
+        t0 = time.perf_counter()
+        logs = rt.run(specs, timeout_s=120, max_inflight=2)
+        assert len(logs) == 8 and all(lg.done for lg in logs)
+        events = sorted([(lg.t_submit, 1) for lg in logs] + [(lg.t_done, -1) for lg in logs])
+        live = peak = 0
+        for _, d in events:
+            live += d
+            peak = max(peak, live)
+        assert peak <= 2
+        spans[mode] = max(lg.t_done for lg in logs) - t0
+    assert spans[capi.MODE_PARTIAL] < spans[capi.MODE_SEQUENTIAL]
