@@ -160,7 +160,7 @@ def argmax(logits: np.ndarray) -> int:
     return lib().orc_argmax(_dp(x), x.shape[0])
 
 
-PARSER_LITERAL, PARSER_JSON_MEMBER, PARSER_JSON_OBJECT, PARSER_FENCE = 0, 1, 2, 3
+PARSER_LITERAL, PARSER_JSON_MEMBER, PARSER_JSON_OBJECT, PARSER_FENCE, PARSER_CALL, PARSER_PLAN = 0, 1, 2, 3, 4, 5
 FLAG_FINAL, FLAG_OVERFLOW, FLAG_CANCELLED, FLAG_OPEN, FLAG_CLOSE = 1, 2, 4, 8, 16
 DELIM_NONE = 0xFFFF
 
@@ -232,3 +232,104 @@ def segment(kind: int, delims: list[bytes], max_seg: int, stream: bytes):
     if n < 0:
         raise RuntimeError("orc_segment overflow")
     return [(int(ce[j]), int(di[j]), int(fl[j])) for j in range(n)]
+
+
+def _line_units(S: bytes, max_seg: int):
+    """Step 1 shared by the line-based grammars: '\n'-terminated units and max_seg cuts
+    (start, end, ends_with_newline, is_continuation)."""
+    units = []
+    start, cont = 0, False
+    for i in range(len(S)):
+        if S[i] == 0x0A:
+            units.append((start, i + 1, True, cont))
+            start, cont = i + 1, False
+        elif i + 1 - start == max_seg:
+            units.append((start, i + 1, False, cont))
+            start, cont = i + 1, True
+    return units, start
+
+
+def call_records(tag: bytes, max_seg: int, S: bytes):
+    """CALL region grammar (NEXT-2; reading R22).  SPEC.md:80: "the sentinel
+    `@call NAME ` begins a region for tool NAME (ToolStart fires as soon as NAME and the
+    trailing space are seen ...); the remainder up to a balanced-brace end is a JSON object ...
+    emitting FieldComplete ... region closes at the brace balance returning to zero"; the
+    paper's Search/Database trigger is "when Conveyor identifies the function name of the
+    tool".  Step by step, byte by byte with a cursor c (start of the
+    current piece or line):
+      outside a region: a line (bytes since the last '\n' or stream start, not a continuation
+        of a max_seg cut) equal to b"@call " + tag + b" " opens the region -> OPEN record
+        [c, p), c = p; a '\n' sets c = p; a line reaching max_seg bytes sets c = p and makes
+        the rest of the line a continuation (never a marker);
+      inside: the JSON automaton of JSON_MEMBER (R10-R11, depth/in_str/esc from 0): ',' at
+        depth 1 -> piece record (delim 0), the bracket returning depth to 0 -> CLOSE record
+        (delim 1) and the region ends (the rest of that line is not at a line start);
+        a piece reaching max_seg bytes -> OVERFLOW record (delim NONE).
+    FINAL = S[c, |S|).  Returns (records [(start, end, delim_id, flags)], c)."""
+    marker = b"@call " + tag + b" "
+    recs = []
+    inside = False
+    c = 0
+    line_ok = True            # the current line started at c and is not a continuation
+    depth = in_str = esc = 0
+    for i in range(len(S)):
+        p = i + 1
+        b = S[i]
+        if not inside:
+            if b == 0x0A:
+                c, line_ok = p, True
+            elif line_ok and S[c:p] == marker:
+                recs.append((c, p, 0, FLAG_OPEN))
+                inside, c = True, p
+                depth = in_str = esc = 0
+            elif p - c == max_seg:
+                c, line_ok = p, False
+            continue
+        hit = -1
+        if in_str:
+            if esc:
+                esc = 0
+            elif b == 0x5C:
+                esc = 1
+            elif b == 0x22:
+                in_str = 0
+        elif depth == 0:
+            if b in (0x7B, 0x5B):
+                depth = 1
+        else:
+            if b == 0x22:
+                in_str = 1
+            elif b in (0x7B, 0x5B):
+                depth = min(depth + 1, 127)
+            elif b in (0x7D, 0x5D):
+                depth -= 1
+                if depth == 0:
+                    hit = 1
+            elif b == 0x2C and depth == 1:
+                hit = 0
+        if hit == 1:
+            recs.append((c, p, 1, FLAG_CLOSE))
+            inside, c, line_ok = False, p, (b == 0x0A)
+        elif hit == 0:
+            recs.append((c, p, 0, 0))
+            c = p
+        elif p - c == max_seg:
+            recs.append((c, p, DELIM_NONE, FLAG_OVERFLOW))
+            c = p
+    return recs, c
+
+
+def plan_records(max_seg: int, S: bytes):
+    r"""PLAN line grammar (NEXT-2; reading R23).  SPEC.md:81: "each newline-
+    terminated line matching `#E<digits> = <Name>[<args>]` is one ToolData stage piece
+    carrying the full line; non-matching lines are PlainText" (LLMCompiler plans; the paper's
+    planning trigger is "a complete stage of the plan is generated").
+    Line units as in FENCE (max_seg cuts, continuations never match); a unit is a stage iff
+    it is not a continuation, ends with '\n' and its bytes match
+    #E[0-9]+ = [A-Za-z0-9_]+\[[^\n]*\]\n  exactly -> piece record (delim 0).
+    FINAL = the trailing incomplete unit."""
+    import re
+    pat = re.compile(rb"#E[0-9]+ = [A-Za-z0-9_]+\[[^\n]*\]\n")
+    units, tail = _line_units(S, max_seg)
+    recs = [(a, b, 0, 0) for (a, b, nl, c) in units if nl and not c and pat.fullmatch(S[a:b])]
+    return recs, tail

@@ -17,7 +17,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from . import DELIM_NONE, FLAG_CANCELLED, FLAG_FINAL, PARSER_FENCE, fence_records, segment
+from . import (DELIM_NONE, FLAG_CANCELLED, FLAG_FINAL, PARSER_CALL, PARSER_FENCE, PARSER_PLAN, call_records,
+               fence_records, plan_records, segment)
 
 NO_TOKEN = 0xFFFFFFFF
 
@@ -58,9 +59,14 @@ def round_records(tokens, vocab_bytes, kind: int, delims: list[bytes], max_seg: 
     recs = []
     c_prev = 0
     seq = seq_start
-    if kind == PARSER_FENCE:
-        # region grammar: records need not tile S (text outside a region is not tool input)
-        fr, c_prev = fence_records(delims[0], max_seg, S)
+    if kind in (PARSER_FENCE, PARSER_CALL, PARSER_PLAN):
+        # region grammars: records need not tile S (text outside a region is not tool input)
+        if kind == PARSER_FENCE:
+            fr, c_prev = fence_records(delims[0], max_seg, S)
+        elif kind == PARSER_CALL:
+            fr, c_prev = call_records(delims[0], max_seg, S)
+        else:
+            fr, c_prev = plan_records(max_seg, S)
         for (a, c, did, fl) in fr:
             t1 = next(t for t, e in enumerate(ends) if e >= c)
             recs.append(Record(round_idx, seq, t1, a, c - a, did, fl, S[a:c]))

@@ -367,3 +367,163 @@ def test_fence_token_index_every_tokenization(L):
                 last = r.byte_offset + r.byte_len - 1
                 assert r.token_index == max(i for i in range(len(pieces)) if bounds[i] <= last)
             assert recs[-1].byte_offset == tail and recs[-1].flags == oracle.FLAG_FINAL
+
+
+# ------------------------------------------------------------------ CALL / PLAN grammars (NEXT-2)
+CAL, PLN = oracle.PARSER_CALL, oracle.PARSER_PLAN
+
+
+def search_call_reading(S: bytes, tag: bytes):
+    """Independent reading of CALL without overflow, search-based instead of a byte automaton:
+    find the next line start whose line begins with the marker, then walk the JSON value with
+    an explicit stack to its end, cutting at depth-1 commas; continue after the value."""
+    marker = b"@call " + tag + b" "
+    recs, pos = [], 0
+    while True:
+        starts = [0] + [m.end() for m in re.finditer(rb"\n", S)]
+        cand = [s for s in starts if s >= pos and S.startswith(marker, s)]
+        if not cand:
+            break
+        a = cand[0]
+        recs.append((a, a + len(marker), 0, oracle.FLAG_OPEN))
+        c = a + len(marker)
+        stack, in_s, esc, i, closed = [], False, False, c, False
+        while i < len(S):
+            ch = S[i:i + 1]
+            if in_s:
+                if esc:
+                    esc = False
+                elif ch == b"\\":
+                    esc = True
+                elif ch == b'"':
+                    in_s = False
+            elif not stack:
+                if ch in (b"{", b"["):
+                    stack.append(ch)
+            elif ch == b'"':
+                in_s = True
+            elif ch in (b"{", b"["):
+                stack.append(ch)
+            elif ch in (b"}", b"]"):
+                stack.pop()
+                if not stack:
+                    recs.append((c, i + 1, 1, oracle.FLAG_CLOSE))
+                    pos, closed = i + 1, True
+                    break
+            elif ch == b"," and len(stack) == 1:
+                recs.append((c, i + 1, 0, 0))
+                c = i + 1
+            i += 1
+        if not closed:
+            return recs, c
+        # the rest of the closing line is not at a line start: resume at the next line
+        nl = S.find(b"\n", pos)
+        if nl < 0:
+            return recs, _tail_after(S, pos)
+        pos = nl + 1
+    return recs, _tail_after(S, pos if recs else 0)
+
+
+def _tail_after(S, pos):
+    """FINAL start outside a region: the start of the last line at or after pos."""
+    k = S.rfind(b"\n", pos)
+    return pos if k < 0 else k + 1
+
+
+def test_call_random_equals_search_reading():
+    rng = random.Random(17)
+    toks = [b"@call s ", b"@call s", b"@call t ", b"{", b"}", b"[", b"]", b",", b'"', b"\\", b"a", b"\n", b" "]
+    for _ in range(20000):
+        S = b"".join(rng.choice(toks) for _ in range(rng.randrange(0, 16)))
+        got = oracle.call_records(b"s", BIG, S)
+        assert got == search_call_reading(S, b"s"), S
+
+
+def test_call_search_workload_fields_from_serialisation():
+    """Three consecutive calls (the Search workload issues three): OPEN at the
+    marker, one piece per member (boundaries from per-member json.dumps), CLOSE at the object end."""
+    rng = random.Random(3)
+    for _ in range(200):
+        objs = [{f"k{j}": rng.choice(["a, b", 7, "x}y", [1, 2], {"z": "}"}]) for j in range(rng.randrange(1, 5))}
+                for _ in range(3)]
+        parts = [b"Let me look these up.\n"]
+        for o in objs:
+            parts.append(b"@call search " + json.dumps(o).encode() + b"\n")
+        S = b"".join(parts) + b"Answer"
+        recs, tail = oracle.call_records(b"search", BIG, S)
+        flags = [f for (_, _, _, f) in recs]
+        assert flags.count(oracle.FLAG_OPEN) == 3 and flags.count(oracle.FLAG_CLOSE) == 3
+        for o in objs:
+            items = list(o.items())
+            want = [("{" if j == 0 else " ") + json.dumps(k) + ": " + json.dumps(v) + ("," if j + 1 < len(items) else "}")
+                    for j, (k, v) in enumerate(items)]
+            got = [S[a:b].decode() for (a, b, d, f) in recs[:len(items) + 1][1:]]
+            assert got == want
+            recs = recs[len(items) + 1:]
+        assert S[tail:] == b"Answer"
+
+
+def test_call_marker_must_start_a_line_and_overflow():
+    S = b"x @call s {\"a\": 1}\n@call s {\"a\": 12345678901}\n"
+    recs, _ = oracle.call_records(b"s", 12, S)
+    assert [(S[a:b], d, f) for (a, b, d, f) in recs] == [
+        (b"@call s ", 0, oracle.FLAG_OPEN), (b'{"a": 123456', oracle.DELIM_NONE, oracle.FLAG_OVERFLOW),
+        (b"78901}", 1, oracle.FLAG_CLOSE)]
+
+
+def plan_line_reading(line: bytes) -> bool:
+    """Hand-written check of one '\\n'-terminated line: #E<digits> = <Name>[<args>]."""
+    if not (line.startswith(b"#E") and line.endswith(b"]\n")):
+        return False
+    i = 2
+    while i < len(line) and line[i:i + 1].isdigit():
+        i += 1
+    if i == 2 or line[i:i + 3] != b" = ":
+        return False
+    i += 3
+    j = i
+    while j < len(line) and (line[j:j + 1].isalnum() or line[j:j + 1] == b"_"):
+        j += 1
+    if j == i or line[j:j + 1] != b"[":
+        return False
+    return b"\n" not in line[j + 1:-1]
+
+
+def test_plan_random_equals_hand_reading():
+    rng = random.Random(19)
+    toks = [b"#E", b"#", b"E", b"1", b"23", b" = ", b"=", b" ", b"search", b"_", b"[", b"]", b"\n", b"x"]
+    for _ in range(20000):
+        S = b"".join(rng.choice(toks) for _ in range(rng.randrange(0, 18)))
+        recs, tail = oracle.plan_records(BIG, S)
+        want = [(m.start(), m.end(), 0, 0) for m in re.finditer(rb"[^\n]*\n", S) if plan_line_reading(m.group(0))]
+        assert (recs, tail) == (want, S.rfind(b"\n") + 1), S
+
+
+def test_plan_four_stages():
+    """a 4-stage plan (two searches, a calculator, a formatter)."""
+    S = (b"Plan:\n#E1 = search[Microsoft market cap]\n#E2 = search[Apple market cap]\n"
+         b"#E3 = calculator[#E1 / #E2]\n#E4 = formatter[ratio: #E3]\nThen answer.")
+    recs, tail = oracle.plan_records(4096, S)
+    assert len(recs) == 4 and all(S[b - 2:b] == b"]\n" for (_, b, _, _) in recs)
+    assert S[tail:] == b"Then answer."
+
+
+@pytest.mark.parametrize("kind,tag", [(CAL, b"s"), (PLN, b"")])
+def test_region_grammars_token_index_random_splits(kind, tag):
+    rng = random.Random(23 + kind)
+    vocab = {}
+    texts = [b'@call s {"a": 1, "b": [2, 3]}\nx\n@call s {"c": "}"}', b"#E1 = s[a]\n#E2 = t[b]\nz"]
+    for S in texts * 30:
+        n = len(S)
+        cut = sorted(rng.sample(range(1, n), rng.randrange(0, 8)))
+        bounds = [0] + cut + [n]
+        pieces = [S[bounds[i]:bounds[i + 1]] for i in range(len(bounds) - 1)]
+        ids = [vocab.setdefault(p, len(vocab)) for p in pieces]
+        table = {v: k for k, v in vocab.items()}
+        recs, stream = round_records(ids, table, kind, [tag], BIG)
+        base, tail = (oracle.call_records(tag, BIG, S) if kind == CAL else oracle.plan_records(BIG, S))
+        assert [(r.byte_offset, r.byte_offset + r.byte_len, r.delim_id, r.flags) for r in recs[:-1]] == base
+        for r in recs[:-1]:
+            last = r.byte_offset + r.byte_len - 1
+            assert r.token_index == max(i for i in range(len(pieces)) if bounds[i] <= last)
+        assert recs[-1].byte_offset == tail
