@@ -466,7 +466,7 @@ def main():
         return
     if args.latency_only:
         ws = args.latency_only.split(",")
-        base = {"codegen": 64, "codegen_fence": 64, "search": 128, "planning": 256, "validation": 512}
+        base = {"codegen": 64, "codegen_fence": 64, "search": 128, "search_call": 128, "planning": 256, "validation": 512}
         bs = {w: (args.latency_batch or base[w]) for w in ws}
         print(json.dumps({"latency": run_latency(ws, bs, verbose=True, inflight=args.latency_inflight or None)}),
               flush=True)
@@ -492,8 +492,8 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None):
     from paper_2406_00059_b200.engine import DeviceModel, Engine
     import numpy as np
     from paper_2406_00059_b200.runtime import Runtime, summarize
-    prefixes = {"codegen": 128, "codegen_fence": 128, "search": 256, "planning": 512, "validation": 1792}
-    max_tokens = {"codegen": 440, "codegen_fence": 460, "search": 560, "planning": 400, "validation": 320}
+    prefixes = {"codegen": 128, "codegen_fence": 128, "search": 256, "search_call": 256, "planning": 512, "validation": 1792}
+    max_tokens = {"codegen": 440, "codegen_fence": 460, "search": 560, "search_call": 560, "planning": 400, "validation": 320}
     pages_per = {w: (prefixes[w] + max_tokens[w] + 31) // 16 + 1 for w in workloads}
     slots = {w: (inflight or batches[w]) for w in workloads}
     need = max(slots[w] * pages_per[w] for w in workloads) + 64

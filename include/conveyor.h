@@ -71,12 +71,23 @@ typedef enum { CVY_DTYPE_BF16 = 0, CVY_DTYPE_FP32 = 1 } cvy_dtype;
  *          region are not tool input and produce no record; the open / close marker lines are
  *          records flagged CVY_SEG_OPEN / CVY_SEG_CLOSE.  TAG = the single delimiter (1..8
  *          bytes, no '\n').  A line reaching max_segment_bytes is cut (OVERFLOW inside a
- *          region, silently outside); its continuation is never a marker. */
+ *          region, silently outside); its continuation is never a marker.
+ * CALL:    (R22) a line starting with "@call " TAG " " opens a call region the
+ *          moment the space after the tool name arrives ("identifies the function name of
+ *          the tool") -> CVY_SEG_OPEN record; inside, the JSON
+ *          argument object is cut like JSON_MEMBER (one segment per completed field) and the
+ *          bracket returning depth to 0 is a CVY_SEG_CLOSE record; text outside is not input.
+ *          TAG = the single delimiter (1..8 bytes, no '\n').
+ * PLAN:    (R23) each line matching  #E<digits> = <Name>[<args>]  is one segment ("a
+ *          complete stage of the plan"); other lines produce no
+ *          record.  No delimiters. */
 typedef enum {
     CVY_PARSER_LITERAL = 0,
     CVY_PARSER_JSON_MEMBER = 1,
     CVY_PARSER_JSON_OBJECT = 2,
-    CVY_PARSER_FENCE = 3
+    CVY_PARSER_FENCE = 3,
+    CVY_PARSER_CALL = 4,
+    CVY_PARSER_PLAN = 5
 } cvy_parser_kind;
 
 /* Host dispatch policy only; the device path is identical in both modes. */

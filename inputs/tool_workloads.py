@@ -33,8 +33,10 @@ def _codegen_plan(rng):
     state = {"pending": 0.0, "in_block": False}
     costs = {}
 
-    def plan(j, data: bytes):
+    def plan(j, data: bytes, flags: int = 0):
         from paper_2406_00059_b200.runtime import SegmentWork
+        if flags & (8 | 16):
+            return None  # FENCE markers (CVY_SEG_OPEN / CLOSE) are indicators, not code
         line = data.decode(errors="replace")
         body = line.strip()
         if j not in costs:
@@ -65,7 +67,7 @@ def _search_plan(rng):
     costs = [rng.uniform(0.2, 1.0) for _ in range(16)]
     seen = [0]
 
-    def plan(j, data: bytes):
+    def plan(j, data: bytes, flags: int = 0):
         from paper_2406_00059_b200.runtime import SegmentWork
         if not data.strip().startswith(b"search("):
             return None  # drafted code lines are not tool input
@@ -75,10 +77,28 @@ def _search_plan(rng):
     return plan
 
 
+def _search_call_plan(rng):
+    """@call search {...} regions (CALL parser, R22): the OPEN record (function name decoded)
+    starts the search tool's fixed setup (connection, U(100,300) ms) on a fresh instance; the
+    argument fields arrive as pieces; the CLOSE record (object complete) runs the query
+    (U(200,1000) ms) on the same instance, after its setup."""
+    state = {"inst": -1}
+
+    def plan(j, data: bytes, flags: int = 0):
+        from paper_2406_00059_b200.runtime import SegmentWork
+        if flags & 8:
+            state["inst"] += 1
+            return SegmentWork(rng.uniform(0.1, 0.3), instance=state["inst"])
+        if flags & 16:
+            return SegmentWork(rng.uniform(0.2, 1.0), instance=state["inst"])
+        return SegmentWork(0.0, instance=max(state["inst"], 0))
+    return plan
+
+
 def _planning_plan(rng):
     costs = [rng.uniform(0.2, 1.0), rng.uniform(0.2, 1.0)]
 
-    def plan(j, data: bytes):
+    def plan(j, data: bytes, flags: int = 0):
         from paper_2406_00059_b200.runtime import SegmentWork
         txt = data.decode(errors="replace")
         try:
@@ -94,7 +114,7 @@ def _planning_plan(rng):
 
 
 def _validation_plan():
-    def plan(j, data: bytes):
+    def plan(j, data: bytes, flags: int = 0):
         from paper_2406_00059_b200.runtime import SegmentWork
         txt = data.decode(errors="replace")
         bad = False
@@ -131,6 +151,19 @@ def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
             r1 = tok.encode("The answer: " + prose(rng, 80))[:100]
             rounds = [Round(r0, tool_ids["search"], _search_plan(rng), obs), Round(r1, -1)]
             prefix = 256
+        elif workload == "search_call":
+            # the Search workload with @call syntax: each call is decoded as
+            # "@call search {json args}" between drafted code lines
+            parts = []
+            for k in range(3):
+                parts.append("@call search " + json.dumps({"q": "hello world in " + ["Python", "C++", "Java"][k],
+                                                           "site": "stackoverflow.com", "n": 3}))
+                parts.append(codegen_script(rng, 6).strip())
+            r0 = tok.encode("\n".join(parts) + "\n")
+            obs = tok.encode("\n[OBSERVATION search]\n" + prose(rng, 60) + "\n")[:96]
+            r1 = tok.encode("The answer: " + prose(rng, 80))[:100]
+            rounds = [Round(r0, tool_ids["search_call"], _search_call_plan(rng), obs), Round(r1, -1)]
+            prefix = 256
         elif workload == "planning":
             r0 = tok.encode(plan_with_thoughts(rng))
             obs = tok.encode("\n[OBSERVATION plan]\n" + prose(rng, 30) + "\n")[:48]
@@ -149,6 +182,7 @@ def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
 
 
 TOOLS = {"interp": ("PARSER_LITERAL", [b"\n"]), "interp_fence": ("PARSER_FENCE", [b"python"]),
+         "search_call": ("PARSER_CALL", [b"search"]),
          "search": ("PARSER_LITERAL", [b"\n"]),
          "planner": ("PARSER_JSON_OBJECT", []), "validator": ("PARSER_JSON_MEMBER", [])}
 
@@ -177,7 +211,7 @@ def build_sweep(B: int, tool_id: int, r: float, tok_s: float, n_lines: int = 24,
         per_byte = tok_s * len(ids) / len(text.encode())
         costs = [r * per_byte * (len(ln) + 1) for ln in lines]
 
-        def plan(j, data, costs=costs):
+        def plan(j, data, flags=0, costs=costs):
             return SegmentWork(costs[j] if j < len(costs) else 0.0, 0)
         specs.append(RequestSpec([1, rng.randrange(259, 32000)], [Round(ids, tool_id, plan)], synth_prefix=64,
                                  synth_seed=b))

@@ -14,7 +14,7 @@ CVY_E_NOTFOUND, CVY_E_STATE, CVY_E_DUP, CVY_E_CUDA, CVY_E_NCCL = -5, -6, -7, -8,
 STATUS_NAMES = {0: "OK", -1: "E_INVAL", -2: "E_NOMEM", -3: "E_FULL", -4: "E_AGAIN", -5: "E_NOTFOUND",
                 -6: "E_STATE", -7: "E_DUP", -8: "E_CUDA", -9: "E_NCCL"}
 DTYPE_BF16, DTYPE_FP32 = 0, 1
-PARSER_LITERAL, PARSER_JSON_MEMBER, PARSER_JSON_OBJECT, PARSER_FENCE = 0, 1, 2, 3
+PARSER_LITERAL, PARSER_JSON_MEMBER, PARSER_JSON_OBJECT, PARSER_FENCE, PARSER_CALL, PARSER_PLAN = 0, 1, 2, 3, 4, 5
 MODE_PARTIAL, MODE_SEQUENTIAL = 0, 1
 SEG_FINAL, SEG_OVERFLOW, SEG_CANCELLED, SEG_OPEN, SEG_CLOSE = 1, 2, 4, 8, 16
 DELIM_NONE = 0xFFFF

@@ -665,23 +665,29 @@ cvy_status cvy_register_tool(cvy_engine* e, const cvy_tool_desc* t, int32_t* too
         td.n_delims = (int32_t)t->n_delims;
     } else if (t->parser == CVY_PARSER_JSON_MEMBER || t->parser == CVY_PARSER_JSON_OBJECT) {
         if (t->n_delims != 0) return fail(CVY_E_INVAL, "JSON parsers take no delimiters");
-    } else if (t->parser == CVY_PARSER_FENCE) {
-        // the open marker line "```" TAG "\n" packed little-endian into dpack[0..1]
+    } else if (t->parser == CVY_PARSER_FENCE || t->parser == CVY_PARSER_CALL) {
+        // the open marker ("```" TAG "\n" / "@call " TAG " ") packed little-endian into dpack[0..1]
+        const bool fence = t->parser == CVY_PARSER_FENCE;
         if (t->n_delims != 1 || !t->delims || !t->delim_lens || !t->delims[0])
-            return fail(CVY_E_INVAL, "FENCE takes exactly one delimiter: the fence tag");
+            return fail(CVY_E_INVAL, "FENCE / CALL take exactly one delimiter: the tag");
         const uint32_t L = t->delim_lens[0];
-        if (L < 1 || L > 8) return fail(CVY_E_INVAL, "fence tag length must be 1..8");
-        uint8_t marker[16] = {'`', '`', '`'};
+        if (L < 1 || L > 8) return fail(CVY_E_INVAL, "tag length must be 1..8");
+        uint8_t marker[16];
+        const char* pre = fence ? "```" : "@call ";
+        const uint32_t np = fence ? 3 : 6;
+        for (uint32_t j = 0; j < np; ++j) marker[j] = (uint8_t)pre[j];
         for (uint32_t j = 0; j < L; ++j) {
-            if (t->delims[0][j] == '\n') return fail(CVY_E_INVAL, "fence tag must not contain a newline");
-            marker[3 + j] = t->delims[0][j];
+            if (t->delims[0][j] == '\n') return fail(CVY_E_INVAL, "tag must not contain a newline");
+            marker[np + j] = t->delims[0][j];
         }
-        marker[3 + L] = '\n';
-        const int mlen = (int)L + 4;
-        if (td.max_seg < mlen) return fail(CVY_E_INVAL, "max_segment_bytes shorter than the fence open line");
+        marker[np + L] = fence ? '\n' : ' ';
+        const int mlen = (int)(np + L + 1);
+        if (td.max_seg < mlen) return fail(CVY_E_INVAL, "max_segment_bytes shorter than the open marker");
         for (int k = 0; k < mlen; ++k) td.dpack[k >> 3] |= (uint64_t)marker[k] << (8 * (k & 7));
         td.dlen[0] = mlen;
         td.n_delims = 1;
+    } else if (t->parser == CVY_PARSER_PLAN) {
+        if (t->n_delims != 0) return fail(CVY_E_INVAL, "PLAN takes no delimiters");
     } else {
         return fail(CVY_E_INVAL, "unknown parser kind");
     }

@@ -320,6 +320,57 @@ CVY_DEV void scan_byte(SlotDev& s, const ToolDev& t, uint8_t b, uint32_t tok_idx
         }
         return;
     }
+    if (t.kind == CVY_PARSER_PLAN) {
+        // R23: per-line DFA over  #E<digits> = <Name>[<args>]\n  in depth (0 = line start,
+        // 9 = last byte ']', 10 = dead: mismatch or continuation of a max_seg cut)
+        int st = s.depth;
+        if (b == '\n') {
+            if (st == 9) scan_emit(so, s.seg_start, since, tok_idx, 0, 0);
+            s.seg_start = p;
+            st = 0;
+        } else {
+            const bool dig = b >= '0' && b <= '9';
+            const bool nam = dig || (b >= 'A' && b <= 'Z') || (b >= 'a' && b <= 'z') || b == '_';
+            switch (st) {
+                case 0: st = b == '#' ? 1 : 10; break;
+                case 1: st = b == 'E' ? 2 : 10; break;
+                case 2: st = dig ? 3 : 10; break;
+                case 3: st = dig ? 3 : (b == ' ' ? 4 : 10); break;
+                case 4: st = b == '=' ? 5 : 10; break;
+                case 5: st = b == ' ' ? 6 : 10; break;
+                case 6: st = nam ? 7 : 10; break;
+                case 7: st = nam ? 7 : (b == '[' ? 8 : 10); break;
+                case 8: case 9: st = b == ']' ? 9 : 8; break;
+                default: break;
+            }
+            if ((int)since == t.max_seg) {
+                s.seg_start = p;
+                st = 10;
+            }
+        }
+        s.depth = st;
+        return;
+    }
+    if (t.kind == CVY_PARSER_CALL && !(s.win & 1)) {
+        // R22, outside a call region: win bit 1 = this line can no longer be the marker
+        // (mismatch, continuation of a max_seg cut, or the rest of a line after a close)
+        const uint32_t k = since - 1;
+        const uint32_t mlen = (uint32_t)t.dlen[0];
+        if (k >= mlen || b != (uint8_t)(t.dpack[k >> 3] >> (8 * (k & 7)))) s.win |= 2;
+        if (b == '\n') {
+            s.seg_start = p;
+            s.win = 0;
+        } else if (!(s.win & 2) && since == mlen) {
+            scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_OPEN);
+            s.seg_start = p;
+            s.win = 1;  // inside; JSON automaton from its start state
+            s.depth = s.in_str = s.esc = 0;
+        } else if ((int)since == t.max_seg) {
+            s.seg_start = p;
+            s.win |= 2;
+        }
+        return;
+    }
     if (t.kind == CVY_PARSER_LITERAL) {
         s.win = (s.win << 8) | b;
         const uint32_t avail = since < 8 ? since : 8;
@@ -340,8 +391,23 @@ CVY_DEV void scan_byte(SlotDev& s, const ToolDev& t, uint8_t b, uint32_t tok_idx
             if (b == '"') s.in_str = 1;
             else if (b == '{' || b == '[') { if (s.depth < 127) s.depth += 1; }
             else if (b == '}' || b == ']') { s.depth -= 1; if (s.depth == 0) hit = 1; }
-            else if (b == ',' && s.depth == 1 && t.kind == CVY_PARSER_JSON_MEMBER) hit = 0;
+            else if (b == ',' && s.depth == 1 && t.kind != CVY_PARSER_JSON_OBJECT) hit = 0;
         }
+    }
+    if (t.kind == CVY_PARSER_CALL) {
+        // inside a call region: member pieces, the closing bracket ends the region
+        if (hit == 1) {
+            scan_emit(so, s.seg_start, since, tok_idx, 1, CVY_SEG_CLOSE);
+            s.seg_start = p;
+            s.win = 2;  // outside, rest of this line is not a line start
+        } else if (hit == 0) {
+            scan_emit(so, s.seg_start, since, tok_idx, 0, 0);
+            s.seg_start = p;
+        } else if ((int)since == t.max_seg) {
+            scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW);
+            s.seg_start = p;
+        }
+        return;
     }
     if (hit >= 0) {
         scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)hit, 0);

@@ -38,7 +38,7 @@ class SegmentWork:
 class Round:
     forced: list                 # teacher-forced generated tokens of the round
     tool_id: int                 # -1: no tool
-    plan: object = None          # callable(seg_index, seg_bytes) -> SegmentWork
+    plan: object = None          # callable(seg_index, seg_bytes, flags) -> SegmentWork | None
     observation: list = field(default_factory=list)  # tokens injected before the next round
 
 
@@ -184,12 +184,13 @@ class Runtime:
         rnd = log.round
         spec_round = log.spec.rounds[rnd]
         is_final = bool(r.flags & capi.SEG_FINAL)
-        if r.flags & (capi.SEG_OPEN | capi.SEG_CLOSE):
-            return  # FENCE region markers are indicators, not tool input
         if not is_final or r.byte_len > 0:
             if spec_round.tool_id >= 0 and spec_round.plan is not None:
                 j = len(log.seg_work[rnd])
-                work = spec_round.plan(j, r.data)
+                # plan(index, bytes, flags): region markers (CVY_SEG_OPEN / CLOSE) are passed
+                # so a plan can ignore them (FENCE) or start the tool on them (CALL: "when
+                # Conveyor identifies the function name of the tool")
+                work = spec_round.plan(j, r.data, r.flags)
                 if work is not None:
                     log.seg_work[rnd].append(work)
                     log.seg_avail[rnd].append(now)

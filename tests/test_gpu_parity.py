@@ -3,6 +3,7 @@
 Tolerances (BASELINE.json north_star): logits max-abs 1e-4 on the fp32 path and 2e-2 on the
 bf16 path; trigger positions and segment records bit-exact under teacher forcing.
 """
+import json
 import random
 
 import numpy as np
@@ -268,6 +269,56 @@ def test_fence_region_grammar_bitexact():
         eng.close()
 
 
+def call_text(rng):
+    """Prose, three @call search lines with JSON arguments (commas and braces inside strings,
+    a nested list), an @call for another tool (prose), a long argument (OVERFLOW), trailing prose."""
+    lines = ["I need to look up three things."]
+    for _ in range(3):
+        args = {"q": rng.choice(["hello, world", "a}b{c", "how to \"quote\""]), "n": rng.randrange(10),
+                "opts": [1, 2, {"k": "v"}]}
+        lines.append("@call search " + json.dumps(args))
+    lines.append("@call calculator " + json.dumps({"x": 2}))
+    lines.append("@call search " + json.dumps({"long": "y" * rng.randrange(40, 90)}))
+    return "\n".join(lines) + "\nThat is all" + ("\n" if rng.random() < 0.5 else "")
+
+
+def plan_text(rng):
+    stages = ["#E1 = search[Microsoft market cap]", "#E2 = search[Apple market cap]",
+              "#E3 = calculator[#E1 / #E2]", "#E4 = formatter[ratio=#E3]"]
+    noise = ["Thought: compare the two.", "#E5 = bad name[x]", "#E = search[x]", "#E6 = ok[unterminated"]
+    lines = ["Plan:"] + [x for st in stages for x in (st, rng.choice(noise))]
+    return "\n".join(lines) + "\n#E7 = last[" + "z" * rng.randrange(1, 80) + "]"
+
+
+@pytest.mark.parametrize("grammar", ["call", "plan"])
+def test_call_and_plan_grammars_bitexact(grammar):
+    """NEXT-2 CALL (R22) and PLAN (R23) parsers on the device, byte-level and 32k vocabularies,
+    with a 64-byte max segment (OVERFLOW inside a call), bit-exact vs the oracle."""
+    for shape, vocab, B in ((TINY, BYTE_VOCAB, 6), (slice_of(TINY, L=2, V=32000, name="tiny-v32k"), synthetic_vocab(32000), 24)):
+        dm, eng = make_engine(shape, "bf16", vocab, B, 1009, max_pages_per_slot=64)
+        if grammar == "call":
+            tool = eng.register_tool("search", capi.PARSER_CALL, [b"search"], max_segment_bytes=64)
+            kind, dl, ms, gen = oracle.PARSER_CALL, [b"search"], 64, call_text
+        else:
+            tool = eng.register_tool("planner", capi.PARSER_PLAN, [], max_segment_bytes=64)
+            kind, dl, ms, gen = oracle.PARSER_PLAN, [b""], 64, plan_text
+        rng = random.Random(29)
+        reqs, meta = [], []
+        for i in range(B):
+            text = gen(rng)
+            f = list(text.encode())[:900] if len(vocab) == 256 else Tokenizer(vocab).encode(text)[:500]
+            reqs.append(([1, 7], f, tool, 1000))
+            meta.append(f)
+        rids, got = run_forced(eng, reqs)
+        n_rec = 0
+        for rid, f in zip(rids, meta):
+            exp = expected_records(f, vocab, kind, dl, ms)
+            assert as_tuples(got[rid]) == exp, rid
+            n_rec += len(exp) - 1
+        assert n_rec >= 4 * B
+        eng.close()
+
+
 def test_eos_ends_round_and_multi_round_inject():
     """EOS (id 2, no bytes) ends round 0; the observation is injected and round 1 generates;
     records and seq continue across rounds."""
@@ -373,7 +424,10 @@ def test_tool_registration_errors():
                          (("g", capi.PARSER_FENCE, [b"py", b"sh"]), capi.CVY_E_INVAL),
                          (("h", capi.PARSER_FENCE, [b"py\n"]), capi.CVY_E_INVAL),
                          (("i", capi.PARSER_FENCE, [b"pythonpy3"]), capi.CVY_E_INVAL),
-                         (("j", capi.PARSER_FENCE, [b"python"], 8), capi.CVY_E_INVAL)]:
+                         (("j", capi.PARSER_FENCE, [b"python"], 8), capi.CVY_E_INVAL),
+                         (("k", capi.PARSER_CALL, []), capi.CVY_E_INVAL),
+                         (("l", capi.PARSER_CALL, [b"search"], 12), capi.CVY_E_INVAL),
+                         (("m", capi.PARSER_PLAN, [b"#"]), capi.CVY_E_INVAL)]:
         with pytest.raises(capi.CvyError) as ei:
             eng.register_tool(*args)
         assert ei.value.status == status

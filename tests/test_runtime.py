@@ -123,7 +123,7 @@ def run(workload, B, mode):
     return logs, summarize(logs, mode, des=oracle_des)
 
 
-@pytest.mark.parametrize("workload", ["codegen", "codegen_fence", "search", "planning"])
+@pytest.mark.parametrize("workload", ["codegen", "codegen_fence", "search", "search_call", "planning"])
 def test_partial_beats_sequential_and_matches_des(workload):
     _, p = run(workload, 3, capi.MODE_PARTIAL)
     _, s = run(workload, 3, capi.MODE_SEQUENTIAL)
