@@ -458,6 +458,8 @@ def main():
     ap.add_argument("--latency-batch", type=int, default=0, help="override every workload's batch")
     ap.add_argument("--latency-inflight", type=int, default=0,
                     help="NEXT-3 abort-and-refill: run each workload's requests through this many slots")
+    ap.add_argument("--chunked-prefill", action="store_true",
+                    help="NEXT-1: prompts / observations as batched prefill passes (CVY_ENGINE_CHUNKED_PREFILL)")
     ap.add_argument("--fig6", action="store_true", help="NEXT-4: Fig. 6 tool/decode ratio sweep on the engine")
     ap.add_argument("--fig6-batch", type=int, default=16)
     args = ap.parse_args()
@@ -468,7 +470,10 @@ def main():
         ws = args.latency_only.split(",")
         base = {"codegen": 64, "codegen_fence": 64, "search": 128, "search_call": 128, "planning": 256, "validation": 512}
         bs = {w: (args.latency_batch or base[w]) for w in ws}
-        print(json.dumps({"latency": run_latency(ws, bs, verbose=True, inflight=args.latency_inflight or None)}),
+        from paper_2406_00059_b200 import capi
+        fl = capi.ENGINE_CHUNKED_PREFILL if args.chunked_prefill else 0
+        print(json.dumps({"latency": run_latency(ws, bs, verbose=True, inflight=args.latency_inflight or None,
+                                                 flags=fl), "chunked_prefill": bool(args.chunked_prefill)}),
               flush=True)
         return
     if args.warmup < 3:
@@ -481,7 +486,7 @@ def main():
 
 
 # ------------------------------------------------------------------ latency: partial vs sequential
-def run_latency(workloads, batches, device=0, verbose=False, inflight=None):
+def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flags=0):
     """Request completion latency with tool partial execution vs sequential tool execution on
     the four workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool
     costs in both modes (the baseline is the same code with partial execution
@@ -501,7 +506,7 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None):
     Bmax = max(slots[w] for w in workloads)
     from inputs.vocab import synthetic_vocab
     eng = Engine(dm, synthetic_vocab(32000), max_slots=Bmax, max_pages_per_slot=max(pages_per.values()) + 2,
-                 device=device)
+                 device=device, flags=flags)
     tool_ids = {name: eng.register_tool(name, getattr(capi, kind), delims) for name, (kind, delims) in TOOLS.items()}
     out = {}
     for w in workloads:

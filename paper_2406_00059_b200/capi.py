@@ -20,6 +20,7 @@ SEG_FINAL, SEG_OVERFLOW, SEG_CANCELLED, SEG_OPEN, SEG_CLOSE = 1, 2, 4, 8, 16
 DELIM_NONE = 0xFFFF
 NO_TOKEN = 0xFFFFFFFF
 ENGINE_NO_GRAPH, ENGINE_DEBUG_LOGITS, ENGINE_SCAN_OFF, ENGINE_NO_PDL, ENGINE_NO_PERSISTENT = 1, 2, 4, 8, 16
+ENGINE_CHUNKED_PREFILL = 32
 
 c_i32, c_u32, c_u64, c_u16, c_f32, c_f64, c_sz, c_vp = (ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
                                                          ctypes.c_uint16, ctypes.c_float, ctypes.c_double,

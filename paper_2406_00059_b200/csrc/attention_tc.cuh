@@ -78,15 +78,14 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     __syncthreads();
     pdl_wait();
 
-    const SlotDev& slot = P.slots[b];
-    const int nkeys = slot.active ? min(slot.pos, slot.max_pos - 1) + 1 : 0;
+    const int nkeys = row_nkeys(P, b);
     const int nsplit = P.attn_splits;
     const int per = (((nkeys + nsplit - 1) / nsplit) + 63) / 64 * 64;
     const int k_begin = min(split * per, nkeys), k_end = min(nkeys, k_begin + per);
     const int pg_begin = k_begin / 16;
     const int n_pages = (k_end > k_begin) ? (k_end + 15) / 16 - pg_begin : 0;
     const int n_tiles = (n_pages + kAtcPagesPerStage - 1) / kAtcPagesPerStage;
-    const int32_t* pt = P.page_table + (size_t)b * P.max_pages;
+    const int32_t* pt = P.page_table + (size_t)row_slot_of(P, b) * P.max_pages;
 
     if (warp == kAtcWarps) {
         // ============ producer: TMA page blocks into the stage ring ============

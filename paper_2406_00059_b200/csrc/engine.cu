@@ -170,7 +170,17 @@ struct SlotHost {
     int32_t next_pos = 0;  // host's view of the position after the last fed/forced token
     bool final_seen = false;
     bool final_pending = false;  // round running (a FINAL will come)
+    int32_t round_pos0 = 0;      // device pos of the round's first input token
+    int32_t round_inputs = 0;    // input tokens the round feeds before generating (incl. cur_tok)
 };
+
+// A chunked-prefill job (NEXT-1): tokens fed at positions pos0, pos0+1, ... of a slot.
+struct PrefillJob {
+    int slot;
+    int32_t pos0;
+    std::vector<int32_t> toks;
+};
+constexpr int kPrefillRows = 256;  // rows per prefill pass (activation buffer capacity)
 
 struct Upload {
     void* dst;
@@ -284,6 +294,18 @@ struct cvy_engine {
     bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
     int attn_stages = 3;
     CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd]
+    // chunked prefill (NEXT-1): row tables and activation buffers of a prefill pass
+    float* d_px = nullptr;
+    void* d_pact = nullptr;
+    float* d_pq = nullptr;
+    void* d_po = nullptr;
+    void* d_ph = nullptr;
+    float* d_pssq = nullptr;
+    float* d_pattn_part = nullptr;
+    int32_t* d_prow = nullptr;      // [3][kPrefillRows]: slot, pos, token
+    std::vector<PrefillJob> prefill_pending;
+    std::map<int, Bucket> prefill_buckets;
+    uint64_t prefill_rows_total = 0;
     int32_t* d_pk_done = nullptr;   // persistent kernel: [L][5] phase-done counters
     int32_t* d_att_cnt = nullptr;   // persistent kernel: split attention segment tickets
     float* d_att_part2 = nullptr;   // persistent kernel: [num_sms][2][G*(hd+2)] partials
@@ -527,6 +549,17 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
         ALLOC(e->d_pk_pflag, sizeof(uint32_t) * 2 * (size_t)prop.multiProcessorCount);
         HALLOC(e->h_pk_err, e->d_pk_err, sizeof(int32_t) * (16 + 24 * (size_t)prop.multiProcessorCount));  // host-mapped: readable after a trap
     }
+    if ((ec->flags & CVY_ENGINE_CHUNKED_PREFILL) && e->bf16) {
+        const size_t R = kPrefillRows;
+        ALLOC(e->d_px, sizeof(float) * R * d);
+        ALLOC(e->d_pact, 2 * es * R * e->act_ld);
+        ALLOC(e->d_pq, sizeof(float) * R * H * hd);
+        ALLOC(e->d_po, 2 * es * R * e->act_ld);
+        ALLOC(e->d_ph, 2 * es * R * e->act_ld);
+        ALLOC(e->d_pssq, sizeof(float) * (size_t)(d / 128) * R);
+        ALLOC(e->d_pattn_part, sizeof(float) * R * Hkv * e->attn_splits_max * (H / Hkv) * (hd + 2));
+        ALLOC(e->d_prow, sizeof(int32_t) * 3 * R);
+    }
     e->max_patches = 4 * Bmax + 64;
     ALLOC(e->d_patches, sizeof(Patch) * e->max_patches);
     HALLOC(e->h_ring, e->dm_ring, sizeof(cvy_segment) * ec->ring_records);
@@ -624,7 +657,8 @@ void cvy_engine_destroy(cvy_engine* e) {
     void* dptrs[] = {e->d_trace, e->d_slots, e->d_page_table, e->d_in_buf, e->d_force_buf, e->d_rope, e->d_x, e->d_act, e->d_q,
                      e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches,
-                     e->d_pk_done, e->d_att_cnt, e->d_att_part2, e->d_pk_part, e->d_pk_pflag};
+                     e->d_pk_done, e->d_att_cnt, e->d_att_part2, e->d_pk_part, e->d_pk_pflag,
+                     e->d_px, e->d_pact, e->d_pq, e->d_po, e->d_ph, e->d_pssq, e->d_pattn_part, e->d_prow};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats, e->h_pk_err};
@@ -768,7 +802,16 @@ cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t
         if (cs != CVY_OK) return cs;
     }
     for (auto& u : ups) e->uploads.push_back(std::move(u));
-    if (r->prompt_len > 1) {
+    // chunked prefill (NEXT-1): all prompt tokens but the last run as one batched pass at the
+    // next step boundary; the slot then starts at the last prompt token
+    const bool prefill = (e->c.flags & CVY_ENGINE_CHUNKED_PREFILL) && e->d_prow && r->prompt_len > 1;
+    if (prefill) {
+        PrefillJob j;
+        j.slot = slot;
+        j.pos0 = (int32_t)r->synth_prefix_len;
+        j.toks.assign(r->prompt, r->prompt + r->prompt_len - 1);
+        e->prefill_pending.push_back(std::move(j));
+    } else if (r->prompt_len > 1) {
         Upload u;
         u.dst = e->d_in_buf + (size_t)slot * e->c.input_cap;
         u.data.resize((r->prompt_len - 1) * sizeof(int32_t));
@@ -788,10 +831,10 @@ cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t
     p.slot = slot;
     p.req_id = e->next_req++;
     p.tool = (e->c.flags & CVY_ENGINE_SCAN_OFF) ? -1 : r->tool_id;
-    p.pos = (int32_t)r->synth_prefix_len;
-    p.cur_tok = r->prompt[0];
+    p.pos = (int32_t)r->synth_prefix_len + (prefill ? (int32_t)r->prompt_len - 1 : 0);
+    p.cur_tok = prefill ? r->prompt[r->prompt_len - 1] : r->prompt[0];
     p.in_idx = 0;
-    p.in_len = (int32_t)r->prompt_len - 1;
+    p.in_len = prefill ? 0 : (int32_t)r->prompt_len - 1;
     p.max_new = (int32_t)r->max_new_tokens;
     p.force_len = (int32_t)r->forced_len;
     p.max_pos = sh.reserved;
@@ -801,6 +844,8 @@ cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t
     sh.state = 0;
     sh.final_pending = true;
     sh.next_pos = (int32_t)(r->synth_prefix_len + r->prompt_len + gen);
+    sh.round_pos0 = p.pos;
+    sh.round_inputs = 1 + p.in_len;
     e->slots[slot] = std::move(sh);
     e->req_slot[p.req_id] = slot;
     e->submitted_any = true;
@@ -829,7 +874,22 @@ cvy_status cvy_inject_observation(cvy_engine* e, uint64_t req_id, const int32_t*
     const int32_t need = sh.next_pos + 1 + (int32_t)n + (int32_t)gen + 1;
     if (!reserve_pages(e, sh, need, slot, ups)) return fail(CVY_E_FULL, "not enough KV pages for the next round");
     for (auto& u : ups) e->uploads.push_back(std::move(u));
-    if (n) {
+    // the round just parked: its last generated token is the next input (R19) at
+    // pos_end = round_pos0 + round_inputs + gen - 1
+    const uint32_t gen_done = e->h_status[slot].gen;
+    const bool prefill = (e->c.flags & CVY_ENGINE_CHUNKED_PREFILL) && e->d_prow && n >= 1 && gen_done >= 1 &&
+                         gen_done <= e->c.round_tokens;
+    int32_t pos_end = 0;
+    if (prefill) {
+        // prefill [last generated token, obs[0..n-2]]; the slot resumes at obs[n-1]
+        pos_end = sh.round_pos0 + sh.round_inputs + (int32_t)gen_done - 1;
+        PrefillJob j;
+        j.slot = slot;
+        j.pos0 = pos_end;
+        j.toks.push_back(e->h_tok_log[(size_t)slot * e->c.round_tokens + gen_done - 1]);
+        j.toks.insert(j.toks.end(), tokens, tokens + n - 1);
+        e->prefill_pending.push_back(std::move(j));
+    } else if (n) {
         Upload u;
         u.dst = e->d_in_buf + (size_t)slot * e->c.input_cap;
         u.data.resize(n * sizeof(int32_t));
@@ -848,7 +908,12 @@ cvy_status cvy_inject_observation(cvy_engine* e, uint64_t req_id, const int32_t*
     p.kind = PATCH_INJECT;
     p.slot = slot;
     p.req_id = req_id;
-    p.in_len = (int32_t)n;
+    p.in_len = prefill ? 0 : (int32_t)n;
+    if (prefill) {
+        p.set_pos = 1;
+        p.pos = pos_end + (int32_t)n;
+        p.cur_tok = tokens[n - 1];
+    }
     p.max_new = (int32_t)max_new_tokens;
     p.force_len = (int32_t)forced_len;
     p.max_pos = sh.reserved;
@@ -857,6 +922,13 @@ cvy_status cvy_inject_observation(cvy_engine* e, uint64_t req_id, const int32_t*
     sh.final_seen = false;
     sh.final_pending = true;
     sh.next_pos = sh.next_pos + 1 + (int32_t)n + (int32_t)gen;
+    if (prefill) {
+        sh.round_pos0 = pos_end + (int32_t)n;
+        sh.round_inputs = 1;
+    } else {
+        sh.round_pos0 = sh.round_pos0 + sh.round_inputs + (int32_t)gen_done - 1;
+        sh.round_inputs = 1 + (int32_t)n;
+    }
     return CVY_OK;
 }
 
@@ -1006,7 +1078,8 @@ StepParams base_params(cvy_engine* e, int Bp) {
 
 // plan one GEMM: W rows N per layer, K, epilogue
 bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int layer, int L_rows_total, const void* X,
-               EpiArgs epi, GemmPlan* out, std::string* why) {
+               EpiArgs epi, GemmPlan* out, std::string* why, int xcap = 0) {
+    if (xcap <= 0) xcap = (int)e->slots.size();  // activation buffer rows (planes are xcap rows apart)
     GemmPlan gp;
     std::memset(&gp, 0, sizeof(gp));
     const int Bp = bk.Bp;
@@ -1024,20 +1097,20 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub))
             return false;
         g.w_row0 = layer * N;
-        if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD) {
+        if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD && xcap == (int)e->slots.size()) {
             const int k = epi.kind == EPI_QKV ? 0 : epi.kind == EPI_SWIGLU ? 2 : (K == ::m_d(e) ? 1 : 3);
             g.trace = e->d_trace + (size_t)k * kTraceStride * e->num_sms;
         }
         g.part = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
-        g.x_plane_rows = (int32_t)e->slots.size();
+        g.x_plane_rows = (int32_t)xcap;
         if (!make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub),
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (weights) failed";
             return false;
         }
         const uint32_t xrows = g.merge ? (uint32_t)Bp : (uint32_t)g.mma_n;
-        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * e->slots.size()), (uint64_t)K, (uint64_t)e->act_ld, xrows,
+        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * xcap), (uint64_t)K, (uint64_t)e->act_ld, xrows,
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (activations) failed";
             return false;
@@ -1210,6 +1283,147 @@ struct KTimer {
     }
 };
 
+// Paged attention of one layer for every row of the bucket (+ the split-KV merge).
+cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt) {
+    cvy_status st;
+    const cvy_model_config& m = e->m;
+    const int Bp = bk.Bp;
+    const int G = m.n_heads / m.n_kv_heads;
+    const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
+    int layer = l;
+    void* aargs[] = {&bk.P, &layer};
+    if (e->attn_tc) {
+        void* targs[] = {&e->tm_kv, &bk.P, &layer};
+        const int nst = e->attn_stages;
+        const void* tf = m.head_dim == 128 ? (nst == 2 ? (const void*)attention_tc_kernel<128, 2>
+                                                        : nst == 4 ? (const void*)attention_tc_kernel<128, 4>
+                                                                   : (const void*)attention_tc_kernel<128, 3>)
+                                            : (nst == 2 ? (const void*)attention_tc_kernel<64, 2>
+                                                        : nst == 4 ? (const void*)attention_tc_kernel<64, 4>
+                                                                   : (const void*)attention_tc_kernel<64, 3>);
+        const int blk = kPageTokens * m.head_dim * 2;
+        const size_t tsmem = 1024 + (size_t)nst * kAtcPagesPerStage * 2 * blk + kAtcWarps * 8 * 16 * 2 +
+                             (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * nst * 8;
+        if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
+            CVY_OK)
+            return st;
+    } else {
+        const void* af = e->bf16 ? (const void*)attention_kernel<__nv_bfloat16> : (const void*)attention_kernel<float>;
+        if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAttnThreads), attn_smem, aargs,
+                           true)) != CVY_OK)
+            return st;
+    }
+    if (kt) kt->end();
+    if (bk.P.attn_splits > 1) {
+        void* margs[] = {&bk.P};
+        const void* mf =
+            e->bf16 ? (const void*)attention_merge_kernel<__nv_bfloat16> : (const void*)attention_merge_kernel<float>;
+        if (kt) kt->begin(3, l);
+        if ((st = launch_k(e, mf, dim3(m.n_kv_heads, Bp), dim3(128), 0, margs, true)) != CVY_OK) return st;
+        if (kt) kt->end();
+    }
+    return CVY_OK;
+}
+
+// ------------------------------------------------------------------ chunked prefill (NEXT-1)
+// A prefill bucket: the per-layer projection plans over the prefill activation buffers
+// (kPrefillRows rows) and a StepParams whose rows map to (slot, position, token).
+cvy_status build_prefill_bucket(cvy_engine* e, int Bp, Bucket** out) {
+    auto it = e->prefill_buckets.find(Bp);
+    if (it != e->prefill_buckets.end()) {
+        *out = &it->second;
+        return CVY_OK;
+    }
+    Bucket bk;
+    bk.Bp = Bp;
+    bk.P = base_params(e, Bp);
+    StepParams& P = bk.P;
+    P.Bmax = kPrefillRows;
+    P.act_plane = (int64_t)kPrefillRows * e->act_ld;
+    P.x = e->d_px;
+    P.act = e->d_pact;
+    P.q = e->d_pq;
+    P.o = e->d_po;
+    P.h = e->d_ph;
+    P.ssq = e->d_pssq;
+    P.attn_part = e->d_pattn_part;
+    P.dbg_logits = nullptr;
+    P.row_slot = e->d_prow;
+    P.row_pos = e->d_prow + kPrefillRows;
+    P.row_tok = e->d_prow + 2 * kPrefillRows;
+    const cvy_model_config& m = e->m;
+    const int L = m.n_layers, d = m.d_model, H = m.n_heads, Hkv = m.n_kv_heads, hd = m.head_dim, dff = m.d_ff;
+    const int Nqkv = (H + 2 * Hkv) * hd;
+    std::string why;
+    for (int l = 0; l < L; ++l) {
+        GemmPlan gp;
+        EpiArgs eq{EPI_QKV, l, Nqkv, nullptr};
+        if (!plan_gemm(e, bk, e->w.wqkv, Nqkv, d, l, L * Nqkv, e->d_pact, eq, &gp, &why, kPrefillRows))
+            return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+        EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d};
+        if (!plan_gemm(e, bk, e->w.wo, d, H * hd, l, L * d, e->d_po, eo, &gp, &why, kPrefillRows))
+            return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+        EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr};
+        if (!plan_gemm(e, bk, e->w.wgu, 2 * dff, d, l, L * 2 * dff, e->d_pact, eg, &gp, &why, kPrefillRows))
+            return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+        EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm};
+        if (!plan_gemm(e, bk, e->w.wd, d, dff, l, L * d, e->d_ph, ed, &gp, &why, kPrefillRows))
+            return fail(CVY_E_INVAL, why);
+        bk.plans.push_back(gp);
+    }
+    auto res = e->prefill_buckets.emplace(Bp, std::move(bk));
+    *out = &res.first->second;
+    return CVY_OK;
+}
+
+// Run the queued prefill jobs: rows (slot, pos, token) in passes of <= kPrefillRows, each
+// pass = embed + L x (QKV + RoPE + KV append, attention over keys [0, pos], O, gate/up, down);
+// no LM head (the slot resumes at its last prompt token in the next decode step).
+cvy_status enqueue_prefill(cvy_engine* e, const std::vector<PrefillJob>& jobs) {
+    std::vector<int32_t> rs, rp, rt;
+    for (const auto& j : jobs)
+        for (size_t i = 0; i < j.toks.size(); ++i) {
+            rs.push_back(j.slot);
+            rp.push_back(j.pos0 + (int32_t)i);
+            rt.push_back(j.toks[i]);
+        }
+    cvy_status st;
+    for (size_t r0 = 0; r0 < rs.size(); r0 += kPrefillRows) {
+        const int n = (int)std::min<size_t>(kPrefillRows, rs.size() - r0);
+        int Bp = 32;
+        while (Bp < n) Bp *= 2;
+        Bucket* bk = nullptr;
+        if ((st = build_prefill_bucket(e, Bp, &bk)) != CVY_OK) return st;
+        std::vector<int32_t> tab(3 * (size_t)kPrefillRows, 0);
+        for (int i = 0; i < kPrefillRows; ++i) tab[kPrefillRows + i] = -1;  // padding rows
+        for (int i = 0; i < n; ++i) {
+            tab[i] = rs[r0 + i];
+            tab[kPrefillRows + i] = rp[r0 + i];
+            tab[2 * kPrefillRows + i] = rt[r0 + i];
+        }
+        if ((st = check_cuda(e, cudaMemcpyAsync(e->d_prow, tab.data(), tab.size() * sizeof(int32_t),
+                                                cudaMemcpyHostToDevice, e->stream),
+                             "prefill rows")) != CVY_OK)
+            return st;
+        // (pageable source: cudaMemcpyAsync stages it before returning, as for the uploads)
+        void* args[] = {&bk->P};
+        if ((st = launch_k(e, (const void*)embed_kernel<__nv_bfloat16>, dim3(Bp), dim3(128), 0, args, true)) != CVY_OK)
+            return st;
+        size_t pi = 0;
+        for (int l = 0; l < e->m.n_layers; ++l) {
+            if ((st = launch_gemm(e, *bk, bk->plans[pi++])) != CVY_OK) return st;
+            if ((st = launch_attention(e, *bk, l, nullptr)) != CVY_OK) return st;
+            for (int k = 0; k < 3; ++k)
+                if ((st = launch_gemm(e, *bk, bk->plans[pi++])) != CVY_OK) return st;
+        }
+        e->prefill_rows_total += (uint64_t)n;
+    }
+    return CVY_OK;
+}
+
 cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
     cvy_status st;
     uint32_t launches = 0;
@@ -1256,48 +1470,14 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
         bk.launches = launches;
         return CVY_OK;
     }
-    const int G = m.n_heads / m.n_kv_heads;
-    const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
     size_t pi = 0;
     for (int l = 0; l < m.n_layers; ++l) {
         kt.begin(1, l);
         if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
         kt.end();
-        int layer = l;
-        void* aargs[] = {&bk.P, &layer};
         kt.begin(2, l);
-        if (e->attn_tc) {
-            void* targs[] = {&e->tm_kv, &bk.P, &layer};
-            const int nst = e->attn_stages;
-            const void* tf = m.head_dim == 128 ? (nst == 2 ? (const void*)attention_tc_kernel<128, 2>
-                                                            : nst == 4 ? (const void*)attention_tc_kernel<128, 4>
-                                                                       : (const void*)attention_tc_kernel<128, 3>)
-                                                : (nst == 2 ? (const void*)attention_tc_kernel<64, 2>
-                                                            : nst == 4 ? (const void*)attention_tc_kernel<64, 4>
-                                                                       : (const void*)attention_tc_kernel<64, 3>);
-            const int blk = kPageTokens * m.head_dim * 2;
-            const size_t tsmem = 1024 + (size_t)nst * kAtcPagesPerStage * 2 * blk + kAtcWarps * 8 * 16 * 2 +
-                                 (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * nst * 8;
-            if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
-                CVY_OK)
-                return st;
-        } else {
-            const void* af = e->bf16 ? (const void*)attention_kernel<__nv_bfloat16> : (const void*)attention_kernel<float>;
-            if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAttnThreads), attn_smem, aargs,
-                               true)) != CVY_OK)
-                return st;
-        }
-        kt.end();
-        launches += 2;
-        if (bk.P.attn_splits > 1) {
-            void* margs[] = {&bk.P};
-            const void* mf =
-                e->bf16 ? (const void*)attention_merge_kernel<__nv_bfloat16> : (const void*)attention_merge_kernel<float>;
-            kt.begin(3, l);
-            if ((st = launch_k(e, mf, dim3(m.n_kv_heads, Bp), dim3(128), 0, margs, true)) != CVY_OK) return st;
-            kt.end();
-            launches++;
-        }
+        if ((st = launch_attention(e, bk, l, &kt)) != CVY_OK) return st;
+        launches += bk.P.attn_splits > 1 ? 3 : 2;  // QKV + attention (+ merge)
         for (int k = 0; k < 3; ++k) {
             kt.begin(4 + k, l);
             if ((st = launch_gemm(e, bk, bk.plans[pi++])) != CVY_OK) return st;
@@ -1323,11 +1503,13 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
     cudaSetDevice(e->dev);
     std::vector<Patch> patches;
     std::vector<Upload> uploads;
+    std::vector<PrefillJob> prefills;
     int max_used = -1;
     {
         std::lock_guard<std::mutex> lk(e->mu);
         patches.swap(e->pending);
         uploads.swap(e->uploads);
+        prefills.swap(e->prefill_pending);
         for (int b = 0; b < (int)e->slots.size(); ++b)
             if (e->slots[b].used) max_used = b;
     }
@@ -1375,6 +1557,14 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
                                                      reinterpret_cast<SlotStatus*>(e->dm_status));
         st = check_cuda(e, cudaGetLastError(), "apply patches");
         if (st != CVY_OK) return st;
+    }
+    if (!prefills.empty()) {
+        // page tables are uploaded above; the pass writes the jobs' KV before this step reads it
+        cvy_status st = enqueue_prefill(e, prefills);
+        if (st != CVY_OK) {
+            e->dead = true;
+            return st;
+        }
     }
     Bucket* bk = nullptr;
     cvy_status st = build_bucket(e, Bp, &bk);

@@ -40,11 +40,21 @@ CVY_DEV void epilogue_prepare(const StepParams& P, const EpiArgs& E, EpiMeta& m,
     if (E.kind == EPI_QKV) {
         const size_t page_elems = (size_t)2 * P.Hkv * kPageTokens * P.hd;
         for (int b = et; b < P.Bp; b += kEpiThreads) {
-            const SlotDev& s = P.slots[b];
-            int pos = s.pos;
+            int pos, sb;
+            bool ok;
+            if (P.row_slot) {  // prefill row (NEXT-1): the host reserved its pages
+                pos = P.row_pos[b];
+                sb = P.row_slot[b];
+                ok = pos >= 0;
+            } else {
+                const SlotDev& s = P.slots[b];
+                pos = s.pos;
+                sb = b;
+                ok = s.active && pos < s.max_pos;
+            }
             long long off = -1;
-            if (s.active && pos < s.max_pos) {
-                const int page = P.page_table[(size_t)b * P.max_pages + pos / kPageTokens];
+            if (ok) {
+                const int page = P.page_table[(size_t)sb * P.max_pages + pos / kPageTokens];
                 off = (long long)((size_t)page * page_elems + (size_t)(pos % kPageTokens) * P.hd);
             }
             m.pos[b] = min(max(pos, 0), P.max_rope_pos - 1);

@@ -85,6 +85,10 @@ __global__ void apply_patches_kernel(SlotDev* slots, const Patch* patches, int n
                 status[p.slot].gen = 0;
                 break;
             case PATCH_INJECT:
+                if (p.set_pos) {  // observation prefilled (NEXT-1): resume at its last token
+                    s.pos = p.pos;
+                    s.cur_tok = p.cur_tok;
+                }
                 s.active = 1;
                 s.in_idx = 0;
                 s.in_len = p.in_len;
@@ -121,8 +125,13 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Step
     pdl_launch_dependents();
     pdl_wait();
     const int b = blockIdx.x;
-    const SlotDev& s = P.slots[b];
-    const int tok = s.active ? s.cur_tok : 0;
+    int tok;
+    if (P.row_tok) {
+        tok = P.row_pos[b] >= 0 ? P.row_tok[b] : 0;
+    } else {
+        const SlotDev& s = P.slots[b];
+        tok = s.active ? s.cur_tok : 0;
+    }
     const T* E = reinterpret_cast<const T*>(P.embed) + (size_t)tok * P.d;
     T* act = reinterpret_cast<T*>(P.act) + (size_t)b * P.act_ld;
     const float* nw = P.L > 0 ? P.attn_norm : P.final_norm;  // L == 0: straight to the LM head
@@ -164,10 +173,9 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
     float* alpha = lrow + kAttnMaxG;            // [G] rescale of this chunk
     float* red = alpha + kAttnMaxG;             // [4][G]
     pdl_wait();
-    const SlotDev& s = P.slots[b];
     const int nsplit = P.attn_splits;
     const int tid = threadIdx.x;
-    const int nkeys = s.active ? min(s.pos, s.max_pos - 1) + 1 : 0;
+    const int nkeys = row_nkeys(P, b);
     const int per = ((nkeys + nsplit - 1) / nsplit + kAttnThreads - 1) / kAttnThreads * kAttnThreads;
     const int k_begin = split * per, k_end = min(nkeys, k_begin + per);
     const float qscale = rsqrtf((float)hd) * 1.4426950408889634f;  // log2(e)/sqrt(hd)
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
     }
     __syncthreads();
     const T* kv = reinterpret_cast<const T*>(P.kv_pool);
-    const int32_t* pt = P.page_table + (size_t)b * P.max_pages;
+    const int32_t* pt = P.page_table + (size_t)row_slot_of(P, b) * P.max_pages;
     const size_t page_stride = (size_t)2 * P.Hkv * kPageTokens * hd;
     const size_t layer_base = (size_t)layer * P.n_pages * page_stride;
     const int nout = (G * hd + kAttnThreads - 1) / kAttnThreads;  // outputs per thread (<= 8)

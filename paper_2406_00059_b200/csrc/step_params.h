@@ -61,6 +61,8 @@ struct Patch {
     uint64_t req_id;
     int32_t tool, pos, cur_tok, in_len, in_idx, max_new, force_len, max_pos;
     uint32_t round, seq;
+    int32_t set_pos;   // INJECT: 1 = also set pos / cur_tok (the observation was prefilled)
+    int32_t pad_;
 };
 
 enum EpiKind : int32_t { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3, EPI_STORE = 4 };
@@ -119,7 +121,21 @@ struct StepParams {
     StepStats* stats;           // [16], mapped
     unsigned long long* step_ctr;  // device
     int32_t scan_off;
+    // Chunked prefill (NEXT-1): a prefill pass maps launch row r to (slot row_slot[r], position
+    // row_pos[r], input token row_tok[r]); row_pos < 0 marks a padding row.  Null in decode
+    // steps, where row r is slot r at its current position.
+    const int32_t* row_slot;
+    const int32_t* row_pos;
+    const int32_t* row_tok;
 };
+
+// keys attended by launch row r (its position + 1), 0 for idle slots / padding rows
+__host__ __device__ inline int row_nkeys(const StepParams& P, int r) {
+    if (P.row_slot) return P.row_pos[r] >= 0 ? P.row_pos[r] + 1 : 0;
+    const SlotDev& s = P.slots[r];
+    return s.active ? (s.pos < s.max_pos - 1 ? s.pos : s.max_pos - 1) + 1 : 0;
+}
+__host__ __device__ inline int row_slot_of(const StepParams& P, int r) { return P.row_slot ? P.row_slot[r] : r; }
 
 struct EpiArgs {
     int32_t kind;

@@ -432,3 +432,66 @@ def test_tool_registration_errors():
             eng.register_tool(*args)
         assert ei.value.status == status
     eng.close()
+
+
+# ------------------------------------------------------------------ NEXT-1: chunked prefill
+@pytest.mark.parametrize("which", ["tiny", "7b-L2"])
+def test_chunked_prefill_prompts_and_observations_match_oracle(which):
+    """CVY_ENGINE_CHUNKED_PREFILL: all prompt tokens but the last (and, after a FINAL, the last
+    generated token + all observation tokens but the last) run as one batched prefill pass;
+    the next decode step starts at the last input.  The oracle is fed the same tokens one by one
+    (forced decode, the plain definition); logits of every generating step within tolerance."""
+    if which == "tiny":
+        shape, vocab = TINY, BYTE_VOCAB
+    else:
+        shape, vocab = slice_of(MISTRAL_7B, L=2, name="7b-L2"), synthetic_vocab(32000)
+    V = shape.V
+    rng = random.Random(31)
+    B, seed, max_new = 5, 1010, 3
+    flags = capi.ENGINE_DEBUG_LOGITS | capi.ENGINE_CHUNKED_PREFILL
+    dm, eng = make_engine(shape, "bf16", vocab, B, seed, flags=flags, max_pages_per_slot=16)
+    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
+    prompts = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 2, 17, 40, 65)]
+    prefix = [0, 9, 0, 21, 3]
+    obs = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 5, 30, 2, 0)]
+    oreqs, rids = [], []
+    for i, p in enumerate(prompts):
+        r = oracle.Request(w, 256)
+        if prefix[i]:
+            r.synth_prefix(prefix[i], 40 + i)
+        for t in p[:-1]:
+            oracle.step([r], [t])
+        oreqs.append(r)
+        rids.append(eng.submit_request(p, max_new, synth_prefix_len=prefix[i], synth_seed=40 + i))
+    nxt = [p[-1] for p in prompts]
+    worst = 0.0
+    for rnd in range(2):
+        gens = [[] for _ in range(B)]
+        for t in range(max_new):
+            eng.step()
+            eng.sync()
+            ora = oracle.step(oreqs, nxt)
+            for i in range(B):
+                gl = eng.debug_logits(rids[i])
+                d = float(np.max(np.abs(gl.astype(np.float64) - ora[i])))
+                worst = max(worst, d)
+                assert d < 2e-2, (which, rnd, t, i, d)
+                g = eng.round_tokens(rids[i])[-1]
+                assert ora[i][g] >= ora[i].max() - 4e-2
+                gens[i].append(g)
+                nxt[i] = g
+        for _ in range(3):
+            eng.step()
+            eng.poll_segments()
+        eng.sync()
+        eng.poll_segments()
+        if rnd == 0:
+            for i in range(B):
+                # next round: last generated token, then the observation (R19)
+                seq = [gens[i][-1]] + obs[i]
+                for t in seq[:-1]:
+                    oracle.step([oreqs[i]], [t])
+                nxt[i] = seq[-1]
+                eng.inject_observation(rids[i], obs[i], max_new)
+    assert worst < 2e-2
+    eng.close()
