@@ -532,7 +532,9 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     ALLOC(e->d_step, sizeof(unsigned long long) * 2);
     // stream-K accumulators of shared tiles: rows padded to 256 per GEMM, Bmax columns
     const size_t max_rows = (size_t)std::max({(size_t)V, (size_t)2 * dff, (size_t)(H + 2 * Hkv) * hd, (size_t)d}) + 256;
-    ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * Bmax);
+    // (a chunked-prefill pass runs the same GEMMs over up to kPrefillRows rows)
+    const size_t acc_cols = (ec->flags & CVY_ENGINE_CHUNKED_PREFILL) ? std::max(Bmax, kPrefillRows) : (size_t)Bmax;
+    ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * acc_cols);
     ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
     e->pk_ok = e->bf16 && hd == 128 && (H / Hkv) <= 4 && H % Hkv == 0 && d % 128 == 0 && ((H + 2 * Hkv) * hd) % 128 == 0 &&
                (2 * dff) % 128 == 0 && (H * hd) % 64 == 0 && dff % 64 == 0 && !(ec->flags & CVY_ENGINE_NO_PERSISTENT);

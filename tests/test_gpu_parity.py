@@ -451,7 +451,8 @@ def test_chunked_prefill_prompts_and_observations_match_oracle(which):
     flags = capi.ENGINE_DEBUG_LOGITS | capi.ENGINE_CHUNKED_PREFILL
     dm, eng = make_engine(shape, "bf16", vocab, B, seed, flags=flags, max_pages_per_slot=16)
     w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
-    prompts = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 2, 17, 40, 65)]
+    # 1 + 16 + 39 + 150 (+ the 65-token prompt's 64) rows: a 256-row pass (unmerged stream-K GEMMs)
+    prompts = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 2, 17, 40, 151 if which == "tiny" else 65)]
     prefix = [0, 9, 0, 21, 3]
     obs = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 5, 30, 2, 0)]
     oreqs, rids = [], []
