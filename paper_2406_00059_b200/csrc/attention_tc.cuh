@@ -47,13 +47,20 @@ CVY_DEV uint32_t pack_bf16(float lo_elem, float hi_elem) {
 // 128B swizzle
 CVY_DEV uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
 
-template <int HD, int STAGES = kAtcStages>
+// PPS = pages per pipeline stage: 4 (each consumer warp takes one page of every stage) or 2
+// (warps 0-1 take the even stages, warps 2-3 the odd ones: half the shared memory per CTA, so
+// twice as many CTAs fit on an SM -- one wave for the decode grid -- with the same bytes in flight).
+template <int HD, int STAGES = kAtcStages, int PPS = kAtcPagesPerStage>
 __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_constant__ CUtensorMap tmKV,
                                                                    const __grid_constant__ StepParams P, int layer) {
     static_assert(HD == 64 || HD == 128, "head_dim");
+    static_assert(PPS == 4 || PPS == 2, "pages per stage");
+    // PPS == 2: stage t belongs to warp pair t & 1; an even ring makes every slot belong to one
+    // pair, so a pair's parity wait is never more than one phase ahead of the slot's barrier
+    static_assert(PPS == 4 || STAGES % 2 == 0, "PPS 2 needs an even number of stages");
     constexpr int HALVES = HD / 64;                      // 64-dim boxes per (page, K/V)
     constexpr int BLK = 16 * HD * 2;                     // bytes of one (page, K/V) block
-    constexpr int STAGE = kAtcPagesPerStage * 2 * BLK;   // K and V of 4 pages
+    constexpr int STAGE = PPS * 2 * BLK;                 // K and V of PPS pages
     constexpr int KSTEPS = HD / 16;
     extern __shared__ __align__(1024) uint8_t asm_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(asm_raw) + 1023) & ~uintptr_t(1023));
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
         tma_prefetch_desc(&tmKV);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], kAtcWarps);
+            mbar_init(&empty_bar[s], PPS);  // the PPS warps that consume the stage
         }
         fence_mbar_init();
     }
@@ -80,11 +87,11 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
 
     const int nkeys = row_nkeys(P, b);
     const int nsplit = P.attn_splits;
-    const int per = (((nkeys + nsplit - 1) / nsplit) + 63) / 64 * 64;
+    const int per = (((nkeys + nsplit - 1) / nsplit) + 16 * PPS - 1) / (16 * PPS) * (16 * PPS);
     const int k_begin = min(split * per, nkeys), k_end = min(nkeys, k_begin + per);
     const int pg_begin = k_begin / 16;
     const int n_pages = (k_end > k_begin) ? (k_end + 15) / 16 - pg_begin : 0;
-    const int n_tiles = (n_pages + kAtcPagesPerStage - 1) / kAtcPagesPerStage;
+    const int n_tiles = (n_pages + PPS - 1) / PPS;
     const int32_t* pt = P.page_table + (size_t)row_slot_of(P, b) * P.max_pages;
 
     if (warp == kAtcWarps) {
@@ -95,10 +102,10 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
                 const int st = t % STAGES;
                 const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
                 mbar_wait(&empty_bar[st], ph ^ 1u);
-                const int np = min(kAtcPagesPerStage, n_pages - t * kAtcPagesPerStage);
+                const int np = min(PPS, n_pages - t * PPS);
                 mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(np * 2 * BLK));
                 for (int p = 0; p < np; ++p) {
-                    const int page = pt[pg_begin + t * kAtcPagesPerStage + p];
+                    const int page = pt[pg_begin + t * PPS + p];
                     for (int c = 0; c < 2; ++c) {
                         const int row0 = ((((layer * P.n_pages + page) * 2 + c) * P.Hkv) + g) * 16;
                         for (int h = 0; h < HALVES; ++h)
@@ -148,12 +155,14 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     const uint32_t pw_addr = smem_u32(pw);
 
     for (int t = 0; t < n_tiles; ++t) {
+        if (PPS == 2 && (t & 1) != (warp >> 1)) continue;  // the other warp pair's stage
         const int st = t % STAGES;
         const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
-        const int pidx = t * kAtcPagesPerStage + warp;  // this warp's page in the split
+        const int wp = PPS == 4 ? warp : (warp & 1);    // this warp's page within the stage
+        const int pidx = t * PPS + wp;                  // this warp's page in the split
         if (pidx < n_pages) {
             mbar_wait(&full_bar[st], ph);
-            const uint32_t kbase = smem_u32(stages + (size_t)st * STAGE + (size_t)(warp * 2) * BLK);
+            const uint32_t kbase = smem_u32(stages + (size_t)st * STAGE + (size_t)(wp * 2) * BLK);
             const uint32_t vbase = kbase + BLK;
             // ---- S^T = K . [q_hi|q_lo]^T
             float s[2][4];  // [key block of 8 cols? no: one n8 block]; s[0] keys grp / grp+8

@@ -292,7 +292,10 @@ struct cvy_engine {
     uint32_t last_launches = 0;
     std::vector<uint8_t> vlen_host;
     bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
-    int attn_stages = 3;
+    int attn_stages = 2;
+    int attn_pps = 2;           // KV pages per attention stage: 2 x 2 stages = 32 KB of ring per CTA,
+                                // 6 CTAs per SM, so the decode grid (Hkv x B) runs in one wave
+                                // (measured at B=64: attention -3..6% vs 4 pages x 3 stages)
     CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd]
     // chunked prefill (NEXT-1): row tables and activation buffers of a prefill pass
     float* d_px = nullptr;
@@ -619,11 +622,15 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
             cvy_engine_destroy(e);
             return fail(CVY_E_CUDA, "KV tensor map encode failed");
         }
-        e->attn_stages = 3;
-        if (const char* as = getenv("CVY_ATTN_STAGES")) e->attn_stages = std::max(2, std::min(4, atoi(as)));
+        e->attn_stages = 2;
+        if (const char* as = getenv("CVY_ATTN_STAGES")) e->attn_stages = std::max(2, std::min(6, atoi(as)));
+        if (const char* ap = getenv("CVY_ATTN_PPS")) e->attn_pps = atoi(ap) == 2 ? 2 : 4;
         for (const void* f : {(const void*)attention_tc_kernel<128, 2>, (const void*)attention_tc_kernel<128, 3>,
                               (const void*)attention_tc_kernel<128, 4>, (const void*)attention_tc_kernel<64, 2>,
-                              (const void*)attention_tc_kernel<64, 3>, (const void*)attention_tc_kernel<64, 4>})
+                              (const void*)attention_tc_kernel<64, 3>, (const void*)attention_tc_kernel<64, 4>,
+                              (const void*)attention_tc_kernel<128, 2, 2>, (const void*)attention_tc_kernel<128, 4, 2>,
+                              (const void*)attention_tc_kernel<128, 6, 2>, (const void*)attention_tc_kernel<64, 2, 2>,
+                              (const void*)attention_tc_kernel<64, 4, 2>, (const void*)attention_tc_kernel<64, 6, 2>})
             cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     }
     // kernel attributes
@@ -1296,15 +1303,25 @@ cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt) {
     void* aargs[] = {&bk.P, &layer};
     if (e->attn_tc) {
         void* targs[] = {&e->tm_kv, &bk.P, &layer};
-        const int nst = e->attn_stages;
-        const void* tf = m.head_dim == 128 ? (nst == 2 ? (const void*)attention_tc_kernel<128, 2>
-                                                        : nst == 4 ? (const void*)attention_tc_kernel<128, 4>
-                                                                   : (const void*)attention_tc_kernel<128, 3>)
-                                            : (nst == 2 ? (const void*)attention_tc_kernel<64, 2>
-                                                        : nst == 4 ? (const void*)attention_tc_kernel<64, 4>
-                                                                   : (const void*)attention_tc_kernel<64, 3>);
+        const int pps = e->attn_pps;
+        const int nst = pps == 2 ? (e->attn_stages <= 2 ? 2 : e->attn_stages >= 6 ? 6 : 4) : e->attn_stages;
+        const void* tf;
+        if (pps == 2)
+            tf = m.head_dim == 128 ? (nst <= 2 ? (const void*)attention_tc_kernel<128, 2, 2>
+                                                : nst >= 6 ? (const void*)attention_tc_kernel<128, 6, 2>
+                                                           : (const void*)attention_tc_kernel<128, 4, 2>)
+                                    : (nst <= 2 ? (const void*)attention_tc_kernel<64, 2, 2>
+                                                : nst >= 6 ? (const void*)attention_tc_kernel<64, 6, 2>
+                                                           : (const void*)attention_tc_kernel<64, 4, 2>);
+        else
+            tf = m.head_dim == 128 ? (nst == 2 ? (const void*)attention_tc_kernel<128, 2>
+                                                : nst == 4 ? (const void*)attention_tc_kernel<128, 4>
+                                                           : (const void*)attention_tc_kernel<128, 3>)
+                                    : (nst == 2 ? (const void*)attention_tc_kernel<64, 2>
+                                                : nst == 4 ? (const void*)attention_tc_kernel<64, 4>
+                                                           : (const void*)attention_tc_kernel<64, 3>);
         const int blk = kPageTokens * m.head_dim * 2;
-        const size_t tsmem = 1024 + (size_t)nst * kAtcPagesPerStage * 2 * blk + kAtcWarps * 8 * 16 * 2 +
+        const size_t tsmem = 1024 + (size_t)nst * pps * 2 * blk + kAtcWarps * 8 * 16 * 2 +
                              (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * nst * 8;
         if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
             CVY_OK)
