@@ -1236,8 +1236,6 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
         K.trace_layer = e->trace_layer;
         K.trace_phase = 1;
         if (const char* v = getenv("CVY_PK_TRACE_PHASE")) K.trace_phase = atoi(v);
-        K.dbg = 0;
-        if (const char* v = getenv("CVY_PK_DBG")) K.dbg = atoi(v);
         bk.pk_smem = PkSmem::total(K.w_stages, K.x_stages, K.x_slot);
         int nb = 0;
         if (ok && K.w_stages >= 2 && bk.pk_smem <= 232448 &&

@@ -83,7 +83,6 @@ struct PkParams {
     unsigned long long* trace;  // [grid][kPkTraceStride] %globaltimer stamps of trace_layer, or null
     int32_t trace_layer;
     int32_t trace_phase;  // GEMM index (0..3) whose epilogue gets detailed stamps [5,6,7,13,14]
-    int32_t dbg;          // measurement knobs (CVY_PK_DBG): 1 = attention consumers skip all math
 };
 
 struct PkSmem {
@@ -592,117 +591,6 @@ CVY_DEV void pk_att_page(PkAttRun& R, uint32_t kbase, uint32_t vbase, uint16_t* 
     __syncwarp();
 }
 
-// two 16-key pages (a, b) of K and V (hd 128) in shared memory -> online-softmax update of the
-// run.  The two pages' QK^T chains and PV products are interleaved (independent MMA chains),
-// which doubles the work per latency-bound step of the single-page version.  has_b = false
-// skips page b entirely (its shared memory is not read: it may hold stale bytes).
-CVY_DEV void pk_att_pages2(PkAttRun& R, uint32_t ka, uint32_t kb, bool has_b, uint16_t* pw, int key_a, int key_b,
-                           int nkeys, int G, int lane) {
-    constexpr int KSTEPS = 8;
-    const int grp = lane >> 2, tig = lane & 3;
-    const int h0 = 2 * (tig & 1);
-    const uint32_t va = ka + 4096, vb = kb + 4096;
-    float aa[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int ks = 0; ks < KSTEPS; ++ks) {
-        const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
-        const int dchunk = ks * 2 + (lane >> 4);
-        const uint32_t off = (dchunk >> 3) * 2048 + sw128(r, dchunk & 7);
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(ka + off, a0, a1, a2, a3);
-        mma_bf16_16816(aa, a0, a1, a2, a3, R.qb[ks][0], R.qb[ks][1]);
-        if (has_b) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4(kb + off, b0, b1, b2, b3);
-            mma_bf16_16816(ab, b0, b1, b2, b3, R.qb[ks][0], R.qb[ks][1]);
-        }
-    }
-    // scores: [page][key half][head j]; hi + lo column halves summed
-    float s[2][2][2];
-    s[0][0][0] = aa[0] + __shfl_xor_sync(0xffffffffu, aa[0], 2);
-    s[0][0][1] = aa[1] + __shfl_xor_sync(0xffffffffu, aa[1], 2);
-    s[0][1][0] = aa[2] + __shfl_xor_sync(0xffffffffu, aa[2], 2);
-    s[0][1][1] = aa[3] + __shfl_xor_sync(0xffffffffu, aa[3], 2);
-    s[1][0][0] = ab[0] + __shfl_xor_sync(0xffffffffu, ab[0], 2);
-    s[1][0][1] = ab[1] + __shfl_xor_sync(0xffffffffu, ab[1], 2);
-    s[1][1][0] = ab[2] + __shfl_xor_sync(0xffffffffu, ab[2], 2);
-    s[1][1][1] = ab[3] + __shfl_xor_sync(0xffffffffu, ab[3], 2);
-    {
-        const int k0 = key_a + grp, k1 = key_b + grp;
-        const bool ok[2][2] = {{k0 < nkeys, k0 + 8 < nkeys}, {has_b && k1 < nkeys, has_b && k1 + 8 < nkeys}};
-#pragma unroll
-        for (int pg = 0; pg < 2; ++pg)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    if (!ok[pg][hh] || h0 + j >= G) s[pg][hh][j] = -INFINITY;
-    }
-    float p[2][2][2];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        float mx = fmaxf(fmaxf(s[0][0][j], s[0][1][j]), fmaxf(s[1][0][j], s[1][1][j]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-        const float mnew = fmaxf(R.m_run[j], mx);
-        const bool none = (mnew == -INFINITY);
-        const float alpha = none ? 1.f : exp2f(R.m_run[j] - mnew);
-#pragma unroll
-        for (int pg = 0; pg < 2; ++pg)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) p[pg][hh][j] = none ? 0.f : exp2f(s[pg][hh][j] - mnew);
-        float ps = (p[0][0][j] + p[0][1][j]) + (p[1][0][j] + p[1][1][j]);
-        ps += __shfl_xor_sync(0xffffffffu, ps, 4);
-        ps += __shfl_xor_sync(0xffffffffu, ps, 8);
-        ps += __shfl_xor_sync(0xffffffffu, ps, 16);
-        R.l_run[j] = R.l_run[j] * alpha + ps;
-        R.m_run[j] = mnew;
-#pragma unroll
-        for (int i = 0; i < KSTEPS; ++i) {
-            R.o[i][j] *= alpha;
-            R.o[i][2 + j] *= alpha;
-        }
-    }
-    // P^T -> shared memory as [col n][32 keys] bf16 (n < 4: hi of head n, n >= 4: lo)
-    __syncwarp();
-#pragma unroll
-    for (int pg = 0; pg < 2; ++pg)
-#pragma unroll
-        for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const float x = p[pg][hh][j];
-                const __nv_bfloat16 hi = __float2bfloat16_rn(x);
-                const __nv_bfloat16 val = (tig < 2) ? hi : __float2bfloat16_rn(x - __bfloat162float(hi));
-                const int n = (tig < 2 ? 0 : 4) + h0 + j;
-                pw[n * 32 + pg * 16 + grp + hh * 8] = *reinterpret_cast<const uint16_t*>(&val);
-            }
-    __syncwarp();
-    const uint32_t pw_addr = smem_u32(pw);
-    uint32_t pa0, pa1, pb0, pb1;
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(pa0) : "r"(pw_addr + (uint32_t)((grp * 32 + tig * 2) * 2)));
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(pa1) : "r"(pw_addr + (uint32_t)((grp * 32 + tig * 2 + 8) * 2)));
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(pb0) : "r"(pw_addr + (uint32_t)((grp * 32 + 16 + tig * 2) * 2)));
-    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(pb1) : "r"(pw_addr + (uint32_t)((grp * 32 + 16 + tig * 2 + 8) * 2)));
-#pragma unroll
-    for (int i = 0; i < KSTEPS; ++i) {
-        const int mtx = lane >> 3, r = lane & 7;
-        const int key = r + (mtx >> 1) * 8;
-        const int dchunk = i * 2 + (mtx & 1);
-        const uint32_t off = (dchunk >> 3) * 2048 + sw128(key, dchunk & 7);
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(va + off, a0, a1, a2, a3);
-        mma_bf16_16816(R.o[i], a0, a1, a2, a3, pa0, pa1);
-        if (has_b) {
-            uint32_t b0, b1, b2, b3;
-            ldsm_x4_t(vb + off, b0, b1, b2, b3);
-            mma_bf16_16816(R.o[i], b0, b1, b2, b3, pb0, pb1);
-        }
-    }
-    __syncwarp();
-}
-
 // One layer's attention over this CTA's units [u0, u1) on the 8 attention warps (aw = 0..7,
 // at = 0..255).  Unit = 8 KV pages of one (slot, kv head); warp aw takes page aw of the unit,
 // which sits in D-ring use xcnt + aw / ppslot; each warp releases its slot itself.
@@ -723,7 +611,7 @@ CVY_DEV void pk_attention_phase(const StepParams& P, const PkParams& K, long lon
         pk_att_decode(att_pre, att_nch, Bp, (int)u, b, g, chunk);
         const int nchb = att_nch[b];
         const int seg_s = att_pre[b] + g * nchb, seg_e = seg_s + nchb;
-        if ((u == u0 || chunk == 0) && !(K.dbg & 1)) {
+        if (u == u0 || chunk == 0) {
             run_s = (int)u;
             const unsigned long long ta = atr ? gtimer() : 0;
             pk_att_load_q(P, R, b, g, lane);
@@ -742,7 +630,7 @@ CVY_DEV void pk_attention_phase(const StepParams& P, const PkParams& K, long lon
                     (pidx < npg ? 0x510 : 0x511) | (int)(min(use, 0x7FFFFu) << 12));
         const unsigned long long tp = atr ? gtimer() : 0;
         if (atr) t_wait += tp - tw;
-        if (pidx < npg && !(K.dbg & 1)) {
+        if (pidx < npg) {
             const uint32_t kbase = smem_u32(xring + (size_t)s * K.x_slot + (size_t)(aw % ppslot) * 8192);
             pk_att_page(R, kbase, kbase + 4096, pw, pidx * 16, nkeys, G, lane);
         }
@@ -750,7 +638,7 @@ CVY_DEV void pk_attention_phase(const StepParams& P, const PkParams& K, long lon
         __syncwarp();
         if (lane == 0) mbar_arrive(&xempty[s]);
         xcnt += (uint32_t)K.att_su;
-        if ((u == u1 - 1 || chunk == nchb - 1) && !(K.dbg & 1)) {
+        if (u == u1 - 1 || chunk == nchb - 1) {
             const unsigned long long tf = atr ? gtimer() : 0;
             pk_att_finish(P, K, R, comb, flags, b, g, seg_s, seg_e, run_s, (int)u + 1, U, at, aw, lane);
             if (atr) t_fin += gtimer() - tf;
