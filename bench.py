@@ -42,7 +42,7 @@ def load_peaks():
 
 
 # ------------------------------------------------------------------ workload
-def codegen_workload(B: int, gen_tokens: int, seed: int = 2001):
+def codegen_workload(B: int, gen_tokens: int, seed: int = 2001, prefix_min: int = 128, prefix_spread: int = 400):
     """Per request: synthetic prefix length, synth seed, forced token stream (teacher forcing
     of codegen scripts)."""
     from inputs.vocab import Tokenizer, synthetic_vocab
@@ -52,7 +52,7 @@ def codegen_workload(B: int, gen_tokens: int, seed: int = 2001):
     rng = random.Random(seed)
     reqs = []
     for b in range(B):
-        prefix = 128 + rng.randrange(0, 400)
+        prefix = prefix_min + (rng.randrange(0, prefix_spread) if prefix_spread > 0 else 0)
         ids = []
         while len(ids) < gen_tokens:
             ids += tok.encode(codegen_script(rng, 40))
@@ -224,10 +224,14 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def workload_config(B, ctx_mean):
+def workload_config(B, ctx_mean, prefix_min=128, prefix_spread=400):
     return {"workload": "codegen (BASELINE.json configs[1]): Mistral-7B-shape random-init, "
-                        "teacher-forced Python-script streams, code-interpreter tool '\\n' (partial mode)",
-            "batch_per_gpu": B, "kv_prefix": "128+U(0,400) synthetic tokens", "ctx_mean": ctx_mean,
+                        "teacher-forced Python-script streams, code-interpreter tool '\\n' (partial mode)"
+                        if (B, prefix_min, prefix_spread) == (64, 128, 400) else
+                        f"decode step at batch {B}, synthetic KV prefixes {prefix_min}+U(0,{prefix_spread}) "
+                        "(Mistral-7B shape, codegen streams; SURVEY.md 8(d) config points)",
+            "batch_per_gpu": B, "kv_prefix": f"{prefix_min}+U(0,{prefix_spread}) synthetic tokens",
+            "ctx_mean": ctx_mean,
             "l2": "no flush: inputs > L2 (14.2 GB weights + KV streamed per step)"}
 
 
@@ -252,7 +256,7 @@ def run_ours(args):
     B = args.batch
     W, K = args.warmup, args.steps
     gen = W + K + 8
-    vocab, reqs = codegen_workload(B, gen)
+    vocab, reqs = codegen_workload(B, gen, prefix_min=args.prefix_min, prefix_spread=args.prefix_spread)
     max_ctx = max(r["prefix"] for r in reqs) + gen + 64
     pages_per_slot = (max_ctx + 15) // 16 + 1
     n_pages = B * pages_per_slot + 64
@@ -394,7 +398,7 @@ def run_ours(args):
                              f"synthetic prefixes), {secs:.1f} s of CPU work"}
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "bf16", "data": "synthetic", "config": workload_config(B, ctx_mean),
+                "dtype": "bf16", "data": "synthetic", "config": workload_config(B, ctx_mean, args.prefix_min, args.prefix_spread),
                 "tokens_per_s_per_gpu": value / world, "roofline": roofline, "step_roofline": step_roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(perf.launches_per_step) * K,
                 "clocks": clk, "wall_s_timed": wall, "segments_polled": nseg[0],
@@ -455,6 +459,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--scan-off", action="store_true", help="trigger scan disabled (overhead A/B)")
+    ap.add_argument("--prefix-min", type=int, default=128, help="synthetic KV prefix: min tokens")
+    ap.add_argument("--prefix-spread", type=int, default=400, help="synthetic KV prefix: + U(0, spread)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--latency-only", default="", help="comma list of workloads: run only the latency A/B")

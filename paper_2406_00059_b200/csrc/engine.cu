@@ -92,21 +92,31 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
                  bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0) {
     g.N = N;
     g.K = K;
-    g.merge = Bp <= 128;
-    g.bk = Bp >= 512 ? 32 : 64;
+    // batches above 128 columns run as nbt tiles of 128 on grid.y, each with the merged
+    // (hi, lo) N = 256 pipeline (measured: the unmerged Bp = 256 layout, 4x more activation
+    // than weight bytes per stage and 2 stages, ran gate/up at 1.7 TB/s)
+    g.nbt = Bp > 128 ? Bp / 128 : 1;
+    g.bq = Bp / g.nbt;
+    if (getenv("CVY_GEMM_NO_BATCH_TILES")) {
+        g.nbt = 1;
+        g.bq = Bp;
+    }
+    const int Bq = g.bq;
+    g.merge = Bq <= 128;
+    g.bk = Bq >= 512 ? 32 : 64;
     // wide GEMMs (gate/up, LM head): 256-row tiles, one per CTA, no reduction; narrow ones
     // (QKV, O, down): 128-row tiles with K split over a 2..4-CTA cluster (DSMEM reduction)
     g.nsub = (g.merge && N >= 8192) ? 2 : 1;
     if (const char* ns = getenv("CVY_GEMM_NSUB")) g.nsub = std::max(1, std::min(2, atoi(ns)));
     if (nsub_override > 0) g.nsub = nsub_override;
     if (g.merge) {
-        g.mma_n = 2 * Bp;
+        g.mma_n = 2 * Bq;
         g.nbh = 1;
-        g.cols_per_sub = 2 * Bp;
+        g.cols_per_sub = 2 * Bq;
     } else {
-        g.mma_n = std::min(Bp, 256);
-        g.nbh = Bp / g.mma_n;
-        g.cols_per_sub = Bp;
+        g.mma_n = std::min(Bq, 256);
+        g.nbh = Bq / g.mma_n;
+        g.cols_per_sub = Bq;
     }
     if (g.bk == 32 || !g.merge) g.nsub = 1;
     if (g.nsub * g.cols_per_sub > 512) {
@@ -117,7 +127,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     g.tmem_cols = pow2_at_least((uint32_t)(g.acc_stages * g.nsub * g.cols_per_sub));
     g.tiles = (N + 128 * g.nsub - 1) / (128 * g.nsub);
     g.kblocks = K / g.bk;
-    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bp, 2, g.bk);
+    const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bq, 2, g.bk);
     const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
     int stages = std::min(12, (int)((232448 - fixed) / stage));
     if (stages < 2) {
@@ -128,14 +138,14 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     *smem = (size_t)stages * stage + fixed;
     // split mode: tiles <= SMs (one tile, or one cluster of S CTAs per tile)
     g.split = 0;
-    if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk) {
+    if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk && (g.nbt == 1 || !allow_kernel_split)) {
         int S = 1;
         // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
         while (allow_kernel_split && S < 4 && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
         if (S == 3 && !getenv("CVY_GEMM_ALLOW_S3")) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
         if (g.tiles <= num_sms) g.split = S;
         // the DSMEM staging of the partial must fit in the pipeline smem
-        if (g.split > 1 && (size_t)g.nsub * Bp * 512 > (size_t)stages * stage) g.split = 0;
+        if (g.split > 1 && (size_t)g.nsub * Bq * 512 > (size_t)stages * stage) g.split = 0;
     }
     // L2 look-ahead: ~256 KB of weights per CTA beyond the smem ring (bounded by L2 capacity)
     g.l2_prefetch = 0;  // measured: no gain (mainloops already stream at 5.6-6.8 TB/s once unblocked)
@@ -143,8 +153,9 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     if (g.split > 0) {
         *grid = g.tiles * g.split;
     } else {
+        // stream-K: the nbt batch tiles share the SMs (each streams 1/grid of the weights)
         const long long T = (long long)g.tiles * g.kblocks;
-        *grid = (int)std::min<long long>(num_sms, T);
+        *grid = (int)std::min<long long>(std::max(1, num_sms / g.nbt), T);
     }
     return true;
 }
@@ -1118,7 +1129,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
             *why = "cuTensorMapEncodeTiled (weights) failed";
             return false;
         }
-        const uint32_t xrows = g.merge ? (uint32_t)Bp : (uint32_t)g.mma_n;
+        const uint32_t xrows = g.merge ? (uint32_t)g.bq : (uint32_t)g.mma_n;
         if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * xcap), (uint64_t)K, (uint64_t)e->act_ld, xrows,
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (activations) failed";
@@ -1253,8 +1264,8 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
 cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
     if (e->bf16) {
         void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g, &gp.tmN};
-        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind), dim3(gp.grid),
-                        dim3(kGemmThreads), gp.smem, args, true, gp.g.split > 1 ? gp.g.split : 1);
+        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind),
+                        dim3(gp.grid, gp.g.nbt), dim3(kGemmThreads), gp.smem, args, true, gp.g.split > 1 ? gp.g.split : 1);
     }
     const float* W = (const float*)gp.W;
     const float* X = (const float*)gp.X;
@@ -1959,15 +1970,15 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     g.epi.store_out = Ytmp;
     CUDA_TRY(cudaMalloc(&g.part, sizeof(float) * (size_t)g.tiles * g.nsub * 128 * Bp));
     CUDA_TRY(cudaMemset(g.part, 0, sizeof(float) * (size_t)g.tiles * g.nsub * 128 * Bp));
-    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (g.tiles + 1)));
-    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (g.tiles + 1)));
+    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (g.tiles * g.nbt + 1)));
+    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (g.tiles * g.nbt + 1)));
     // X as the (hi, lo) pair the engine uses: hi = X (exact bf16), lo = 0, padded to Bp rows
     void* Xp = nullptr;
     CUDA_TRY(cudaMalloc(&Xp, (size_t)2 * Bp * K * 2));
     CUDA_TRY(cudaMemset(Xp, 0, (size_t)2 * Bp * K * 2));
     CUDA_TRY(cudaMemcpy(Xp, X, (size_t)B * K * 2, cudaMemcpyDeviceToDevice));
     CUtensorMap tmW, tmX;
-    const uint32_t xrows = g.merge ? (uint32_t)Bp : (uint32_t)g.mma_n;
+    const uint32_t xrows = g.merge ? (uint32_t)g.bq : (uint32_t)g.mma_n;
     if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub), (uint32_t)g.bk) ||
         !make_tmap(&tmX, Xp, (uint64_t)(2 * Bp), (uint64_t)K, (uint64_t)K, xrows, (uint32_t)g.bk))
         return fail(CVY_E_CUDA, "tensor map encode failed");
@@ -1975,7 +1986,7 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     void* args[] = {&tmW, &tmX, &P, &g, &tmW};
     cudaLaunchConfig_t lc;
     std::memset(&lc, 0, sizeof(lc));
-    lc.gridDim = dim3(grid);
+    lc.gridDim = dim3(grid, g.nbt);
     lc.blockDim = dim3(kGemmThreads);
     lc.dynamicSmemBytes = smem;
     cudaLaunchAttribute la[1];

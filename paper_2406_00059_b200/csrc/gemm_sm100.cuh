@@ -35,7 +35,11 @@ struct GemmTC {
     int32_t K;
     int32_t nsub;       // 128-row sub-tiles per tile (must equal the kernel's NSUB)
     int32_t mma_n;      // UMMA N of one MMA
-    int32_t nbh;        // batch halves (Bp / mma_n) when the planes are not merged
+    int32_t nbh;        // batch halves (bq / mma_n) when the planes are not merged
+    int32_t bq;         // batch columns of one CTA (= Bp, or 128 when the batch is tiled)
+    int32_t nbt;        // batch tiles (grid.y): Bp = nbt * bq; each CTA row of the grid runs the
+                        // merged 128-column pipeline on its batch tile (CTAs sharing a weight
+                        // tile read it through L2)
     int32_t tiles;
     int32_t kblocks;    // K / bk
     int32_t bk;         // K elements per pipeline stage: 64 (128B swizzle) or 32 (64B swizzle)
@@ -133,16 +137,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int KSTEPS = BK / 16;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    const int Bp = P.Bp;
+    const int Bp = G.bq;                              // this CTA's batch columns
+    const int cbase = (int)blockIdx.y * G.bq;         // first batch column of this CTA
     const uint32_t XB = (uint32_t)Bp * ROW;           // one activation plane per stage
     const uint32_t stage_bytes = WB + 2u * XB;
     uint8_t* fixed = smem + (size_t)G.stages * stage_bytes;
     float* esm = reinterpret_cast<float*>(fixed);
     EpiMeta meta;
     meta.kvoff = reinterpret_cast<long long*>(esm + 128 * kEsmLd + 4);
-    meta.scale = reinterpret_cast<float*>(meta.kvoff + Bp);
-    meta.pos = reinterpret_cast<int*>(meta.scale + Bp);
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta.pos + Bp + 2);
+    meta.scale = reinterpret_cast<float*>(meta.kvoff + P.Bp);
+    meta.pos = reinterpret_cast<int*>(meta.scale + P.Bp);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta.pos + P.Bp + 2);
     uint64_t* empty_bar = full_bar + G.stages;
     uint64_t* tfull_bar = empty_bar + G.stages;
     uint64_t* tempty_bar = tfull_bar + 2;
@@ -184,7 +189,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
-    unsigned long long* tr = G.trace ? G.trace + (size_t)blockIdx.x * kTraceStride : nullptr;
+    unsigned long long* tr = (G.trace && blockIdx.y == 0) ? G.trace + (size_t)blockIdx.x * kTraceStride : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = gtimer();
 
     if (warp == 4) {
@@ -217,7 +222,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int pl = 0; pl < 2; ++pl)
                     for (int h = 0; h < xh; ++h)
                         tma_load_2d(sx + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[i], kb * BK,
-                                    pl * G.x_plane_rows + h * xrows, pol_x);
+                                    pl * G.x_plane_rows + cbase + h * xrows, pol_x);
             }
             int stage = pre % G.stages;
             uint32_t phase = (pre == G.stages) ? 1u : 0u;
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int pl = 0; pl < 2; ++pl)
                     for (int h = 0; h < xh; ++h)
                         tma_load_2d(sw + WB + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[stage], kb * BK,
-                                    pl * G.x_plane_rows + h * xrows, pol_x);
+                                    pl * G.x_plane_rows + cbase + h * xrows, pol_x);
                 if (++stage == G.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -240,7 +245,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         // non-split: warm L2 with the next GEMM's first k-blocks right behind our own stream
         __syncwarp();
-        if (G.split <= 1) prefetch_next_gemm(G, &tmN, lane);
+        if (G.split <= 1 && blockIdx.y == 0) prefetch_next_gemm(G, &tmN, lane);
     } else if (warp == 5) {
         // ===================== MMA issuer =====================
         const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)G.mma_n);
@@ -372,7 +377,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
                         }
-                        if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
+                        if (!(G.dbg & 8))
+                            epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, et);
                     }
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
@@ -381,7 +387,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 // Shared tile: add this CTA's partial into the tile's fp32 accumulator with L2
                 // vector reductions (no return, nobody waits), take an arrival ticket; the last
                 // arriver reads the completed sum, re-zeroes it, and runs the epilogue.
-                float* acc = G.part + (size_t)tile * rows * Bp;
+                float* acc = G.part + ((size_t)tile * G.nbt + blockIdx.y) * rows * Bp;
+                int32_t* ticket = G.tile_cnt + (size_t)tile * G.nbt + blockIdx.y;
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
                         float v[32];
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mbar_arrive(&tempty_bar[as]);
                 __threadfence();
                 epi_sync();
-                if (et == 0) flags[0] = (atomicAdd(&G.tile_cnt[tile], 1) == c_last - c_first) && !(G.dbg & 4);
+                if (et == 0) flags[0] = (atomicAdd(ticket, 1) == c_last - c_first) && !(G.dbg & 4);
                 epi_sync();
                 if (flags[0]) {
                     __threadfence();
@@ -418,16 +425,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             }
 #pragma unroll
                             for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));
-                            if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, et);
+                            if (!(G.dbg & 8))
+                                epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, et);
                         }
-                    if (et == 0) G.tile_cnt[tile] = 0;
+                    if (et == 0) *ticket = 0;
                     did_epi = true;
                 }
             }
             if (EPI == EPI_LMHEAD && did_epi) {
                 __threadfence();
                 epi_sync();
-                if (et == 0) flags[1] = (atomicAdd(P.lm_done, 1) == G.tiles - 1);
+                if (et == 0) flags[1] = (atomicAdd(P.lm_done, 1) == G.tiles * G.nbt - 1);
                 epi_sync();
                 if (flags[1]) sample_scan_publish(P, et, reinterpret_cast<int*>(esm));
             }
@@ -442,7 +450,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // the S partials in rank order (deterministic), then runs the epilogue on them
         cluster_sync_all();
         if (tr && threadIdx.x == 0) tr[6] = gtimer();  // partials staged cluster-wide
-        if (warp == 4) prefetch_next_gemm(G, &tmN, lane);  // overlaps the reduce below
+        if (warp == 4 && blockIdx.y == 0) prefetch_next_gemm(G, &tmN, lane);  // overlaps the reduce below
         if (warp < 4) {
             const int et = threadIdx.x;
             const int units = NSUB * (Bp / 16);
@@ -476,7 +484,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
                 const int s = u / (Bp / 16), cb = (u % (Bp / 16)) * 16;
                 if (tr && et == 0 && u == crank) tr[8] = gtimer();
-                if (!(G.dbg & 8)) epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cb, v, esm, meta, threadIdx.x, 16);
+                if (!(G.dbg & 8))
+                    epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, threadIdx.x, 16);
                 if (tr && et == 0 && u == crank) tr[9] = gtimer();
             }
         }
