@@ -95,7 +95,9 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     // batches above 128 columns run as nbt tiles of 128 on grid.y, each with the merged
     // (hi, lo) N = 256 pipeline (measured: the unmerged Bp = 256 layout, 4x more activation
     // than weight bytes per stage and 2 stages, ran gate/up at 1.7 TB/s)
-    g.nbt = Bp > 128 ? Bp / 128 : 1;
+    int bq_max = 128;
+    if (const char* v = getenv("CVY_GEMM_BQ")) bq_max = std::max(32, std::min(128, atoi(v)));  // A/B knob
+    g.nbt = Bp > bq_max ? Bp / bq_max : 1;
     g.bq = Bp / g.nbt;
     if (getenv("CVY_GEMM_NO_BATCH_TILES")) {
         g.nbt = 1;
