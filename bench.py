@@ -388,6 +388,10 @@ def run_ours(args):
         eng.release_request(rid)
     e2e = run_e2e(eng, reqs, tool, B)
     eng.close()
+    # whole-job e2e at N GPUs: all ranks' generated tokens / the slowest rank's wall time
+    e2e_ms, e2e_tok, _ = reduce_over_ranks(e2e.pop("_dt_s") * 1e3, e2e.pop("_ntok"), [0.0], device="cuda")
+    e2e["per_rank_value"] = e2e["value"]
+    e2e["value"] = e2e_tok / (e2e_ms / 1000.0)
 
     if rank == 0:
         cpu = None
@@ -436,7 +440,7 @@ def run_e2e(eng, reqs, tool, B):
         eng.release_request(i)
     h2d = B * (prompt_len + G) * 4 + B * 64 * 4  # prompt + forced tokens + page-table entries
     d2h = nrec * 40 + nbytes + ntok * 4
-    return {"value": ntok / dt, "unit": "tokens/s", "h2d_bytes_per_step": h2d / steps,
+    return {"value": ntok / dt, "_dt_s": dt, "_ntok": ntok, "unit": "tokens/s", "h2d_bytes_per_step": h2d / steps,
             "d2h_bytes_per_step": d2h / steps, "steps": steps, "requests": B, "generated_per_request": G,
             "prompt_tokens": prompt_len, "includes": "submit (host prompts + forced streams), chunked prefill "
                                                      "(CVY_ENGINE_CHUNKED_PREFILL), decode, segment polling, "
