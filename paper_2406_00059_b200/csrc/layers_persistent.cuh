@@ -1000,7 +1000,6 @@ __global__ void __launch_bounds__(kPkThreads, 1)
         // ===================== WG0: epilogue / attention warps 0-3 =====================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n" ::: "memory");
         const int et = threadIdx.x;
-        const int G = P.H / Hkv;
         long long u0, u1;
         pk_att_range(att_pre, att_nch, Bp, U, nseg, cta, Gc, u0, u1);
         uint32_t xcnt = 0, acnt = 0, red_ph = 0;
