@@ -108,7 +108,10 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     g.bk = Bq >= 512 ? 32 : 64;
     // wide GEMMs (gate/up, LM head): 256-row tiles, one per CTA, no reduction; narrow ones
     // (QKV, O, down): 128-row tiles with K split over a 2..4-CTA cluster (DSMEM reduction)
-    g.nsub = (g.merge && N >= 8192) ? 2 : 1;
+    // 256-row tiles halve the activation bytes per weight byte; worth it down to the QKV
+    // width (6144 rows: 24 tiles x 4-CTA clusters; measured QKV 0.896 -> 0.836 ms/step at B=64),
+    // not for the 4096-row O / down GEMMs (16 tiles: too few CTAs)
+    g.nsub = (g.merge && N >= 6144) ? 2 : 1;
     if (const char* ns = getenv("CVY_GEMM_NSUB")) g.nsub = std::max(1, std::min(2, atoi(ns)));
     if (nsub_override > 0) g.nsub = nsub_override;
     if (g.merge) {
