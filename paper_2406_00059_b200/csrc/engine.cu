@@ -196,7 +196,7 @@ struct PrefillJob {
     int32_t pos0;
     std::vector<int32_t> toks;
 };
-constexpr int kPrefillRows = 256;  // rows per prefill pass (activation buffer capacity)
+constexpr int kPrefillRows = 512;  // rows per prefill pass (activation buffer capacity)
 
 struct Upload {
     void* dst;
