@@ -2,17 +2,18 @@
 //
 // Y^T[n][b] = sum_k W[n][k] * X[b][k]  (swap-AB: the weight rows are the UMMA M=128 side,
 // the padded batch is the UMMA N side), bf16 inputs, fp32 accumulation in TMEM.  X is the
-// (hi, lo) bf16 pair of the activation: for Bp <= 128 both planes
-// form ONE B operand of N = 2*Bp rows (TMEM columns [0,Bp) = W.x_hi, [Bp,2Bp) = W.x_lo,
-// summed in the epilogue); above that the two planes are separate MMAs into the same D.
+// (hi, lo) bf16 pair of the activation: both planes form ONE B
+// operand of N = 2*bq rows (TMEM columns [0,bq) = W.x_hi, [bq,2bq) = W.x_lo, summed in the
+// epilogue).  Batches above 128 run as Bp/128 batch tiles of bq = 128 columns on grid.y.
 //
-// Work split: stream-K over (tile, k-block) iterations -- one persistent CTA per SM, each
-// owning a contiguous iteration range, so every SM streams the same weight bytes (the
-// kernel is HBM-bound for Bp <= ~200).  A tile finished by one CTA is epilogued from TMEM;
-// a tile shared by several CTAs is reduced with fp32 vector reductions into an L2-resident
-// accumulator; an arrival ticket elects the last contributor, which reads the sum, re-zeroes
-// it and runs the epilogue.  No CTA ever waits on another (fp32 summation order -- and thus
-// the last bits of the result -- varies run to run).
+// Work split (chosen per GEMM by the engine):
+//  * whole tiles (split = 1): one CTA per 128- or 256-row tile (gate/up, LM head);
+//  * cluster split-K (split = S in 2..4): tile = blockIdx.x / S, its K range split over the S
+//    CTAs of a thread-block cluster; partials are staged in the idle pipeline smem and
+//    reduce-scattered through DSMEM in rank order (deterministic) -- QKV, O, down;
+//  * stream-K (split = 0, batch tiles / forced): contiguous (tile, k-block) ranges per CTA;
+//    shared tiles are summed with fp32 red.add into an L2 accumulator and the last arriving
+//    contributor (ticket) runs the epilogue (summation order varies run to run).
 //
 // Warp roles (192 threads): warps 0-3 epilogue (TMEM lanes 0-127), warp 4 TMA producer,
 // warp 5 MMA issuer (one lane; descriptors precomputed, loops unrolled) and TMEM owner.
