@@ -369,6 +369,21 @@ def run_ours(args):
     step_bytes = step_alg_bytes(shape, [c + K / 2 for c in ctx_start])
     step_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (max_ms / K / 1000.0) / 1e9,
                  "frac": step_bytes / (max_ms / K / 1000.0) / 1e9 / hbm}
+    # phase roofline: t_min = sum over phases of max(bytes / HBM, flops / TC);
+    # the projections' flops count the (hi, lo) activation pair twice
+    tc = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])) * 1e12
+    ctx_now = [c + K / 2 for c in ctx_start]
+    proj_bytes = 2.0 * shape.n_params_streamed
+    proj_flops = 2.0 * shape.n_params_streamed * B * 2
+    kv_tok = shape.kv_bytes_per_token
+    att_bytes = sum(c + 1 for c in ctx_now) * kv_tok + B * kv_tok
+    att_flops = 4.0 * shape.L * shape.H * shape.hd * sum(c + 1 for c in ctx_now)
+    t_proj = max(proj_bytes / (hbm * 1e9), proj_flops / tc)
+    t_att = max(att_bytes / (hbm * 1e9), att_flops / tc)
+    t_meas = max_ms / K / 1000.0
+    step_roof["phase_roofline"] = {"t_min_ms": (t_proj + t_att) * 1e3, "frac": (t_proj + t_att) / t_meas,
+                                   "projections": "tensor" if proj_flops / tc > proj_bytes / (hbm * 1e9) else "hbm",
+                                   "tc_peak_tflops": tc / 1e12}
 
     # end-to-end through the C ABI with host buffers: release, then a fresh batch whose
     # prompts and forced streams come from host memory; timed until every FINAL is polled and
