@@ -244,8 +244,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for the multi-rank path on a single-GPU box: CVY_DIST_BACKEND=gloo (reductions
+    # on host tensors) and CVY_SAME_GPU=1 (every rank on device 0); the driver's runs use NCCL,
+    # one GPU per rank
+    backend = os.environ.get("CVY_DIST_BACKEND", "nccl")
+    if os.environ.get("CVY_SAME_GPU") == "1":
+        local = 0
+    red_dev = "cuda" if backend == "nccl" else None
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     torch.cuda.set_device(local)
 
     from inputs.configs import MISTRAL_7B
@@ -306,7 +313,7 @@ def run_ours(args):
     dev_ms = ev0.elapsed_time(ev1)
     perf = eng.perf()
     max_ms, total_tokens, rank_stats = reduce_over_ranks(dev_ms, B * K, [float(rank), dev_ms, float(B * K)],
-                                                         device="cuda")
+                                                         device=red_dev)
     value = total_tokens / (max_ms / 1000.0)
     ctx_mean = float(np.mean([c + K / 2 for c in ctx_start]))
 
@@ -404,7 +411,7 @@ def run_ours(args):
     e2e = run_e2e(eng, reqs, tool, B)
     eng.close()
     # whole-job e2e at N GPUs: all ranks' generated tokens / the slowest rank's wall time
-    e2e_ms, e2e_tok, _ = reduce_over_ranks(e2e.pop("_dt_s") * 1e3, e2e.pop("_ntok"), [0.0], device="cuda")
+    e2e_ms, e2e_tok, _ = reduce_over_ranks(e2e.pop("_dt_s") * 1e3, e2e.pop("_ntok"), [0.0], device=red_dev)
     e2e["per_rank_value"] = e2e["value"]
     e2e["value"] = e2e_tok / (e2e_ms / 1000.0)
 
