@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "attention_tc.cuh"
 #include "layers_persistent.cuh"
+#include "attention_pk.cuh"
 #include "step_params.h"
 
 using namespace cvy;
@@ -309,6 +310,7 @@ struct cvy_engine {
     std::vector<uint8_t> vlen_host;
     bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
     int attn_stages = 2;
+    bool attn_pk = false;       // persistent attention kernel (CVY_ATTN_PERSISTENT=1, attention_pk.cuh)
     int attn_pps = 2;           // KV pages per attention stage: 2 x 2 stages = 32 KB of ring per CTA,
                                 // 6 CTAs per SM, so the decode grid (Hkv x B) runs in one wave
                                 // (measured at B=64: attention -3..6% vs 4 pages x 3 stages)
@@ -641,6 +643,10 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
         e->attn_stages = 2;
         if (const char* as = getenv("CVY_ATTN_STAGES")) e->attn_stages = std::max(2, std::min(6, atoi(as)));
         if (const char* ap = getenv("CVY_ATTN_PPS")) e->attn_pps = atoi(ap) == 2 ? 2 : 4;
+        if (const char* apk = getenv("CVY_ATTN_PERSISTENT"))
+            e->attn_pk = atoi(apk) != 0 && hd == 128 && (H / Hkv) <= 4;
+        if (e->attn_pk)
+            cudaFuncSetAttribute(attention_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ap_smem_bytes(3));
         for (const void* f : {(const void*)attention_tc_kernel<128, 2>, (const void*)attention_tc_kernel<128, 3>,
                               (const void*)attention_tc_kernel<128, 4>, (const void*)attention_tc_kernel<64, 2>,
                               (const void*)attention_tc_kernel<64, 3>, (const void*)attention_tc_kernel<64, 4>,
@@ -1315,6 +1321,15 @@ cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt) {
     const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
     int layer = l;
     void* aargs[] = {&bk.P, &layer};
+    if (e->attn_pk && bk.P.row_slot == nullptr && Bp <= kApMaxRows) {
+        int nst = 3;
+        void* pargs[] = {&e->tm_kv, &bk.P, &layer, &nst};
+        if ((st = launch_k(e, (const void*)attention_persistent_kernel, dim3(e->num_sms), dim3((kApConsumers + 1) * 32),
+                           ap_smem_bytes(nst), pargs, true)) != CVY_OK)
+            return st;
+        if (kt) kt->end();
+        return CVY_OK;
+    }
     if (e->attn_tc) {
         void* targs[] = {&e->tm_kv, &bk.P, &layer};
         const int pps = e->attn_pps;

@@ -516,7 +516,8 @@ CVY_DEV void pk_att_page(PkAttRun& R, uint32_t kbase, uint32_t vbase, uint16_t* 
     constexpr int KSTEPS = 8;
     const int grp = lane >> 2, tig = lane & 3;
     const int h0 = 2 * (tig & 1);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    // two independent accumulator chains (even / odd k-steps) halve the dependent MMA latency
+    float acc[4] = {0.f, 0.f, 0.f, 0.f}, acc2[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int ks = 0; ks < KSTEPS; ++ks) {
         const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
@@ -524,8 +525,10 @@ CVY_DEV void pk_att_page(PkAttRun& R, uint32_t kbase, uint32_t vbase, uint16_t* 
         const uint32_t addr = kbase + (dchunk >> 3) * 2048 + sw128(r, dchunk & 7);
         uint32_t a0, a1, a2, a3;
         ldsm_x4(addr, a0, a1, a2, a3);
-        mma_bf16_16816(acc, a0, a1, a2, a3, R.qb[ks][0], R.qb[ks][1]);
+        mma_bf16_16816((ks & 1) ? acc2 : acc, a0, a1, a2, a3, R.qb[ks][0], R.qb[ks][1]);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] += acc2[u];
     float s[2][2];
     s[0][0] = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 2);
     s[0][1] = acc[1] + __shfl_xor_sync(0xffffffffu, acc[1], 2);
