@@ -32,13 +32,48 @@ METRIC = "decode tokens/s/GPU + HBM roofline %; request latency, partial vs sequ
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
 
+def _flatten(d, pre=""):
+    out = {}
+    if isinstance(d, dict):
+        for k, v in d.items():
+            out.update(_flatten(v, f"{pre}.{k}".lower() if pre else str(k).lower()))
+    elif isinstance(d, (int, float)) and not isinstance(d, bool):
+        out[pre] = float(d)
+    return out
+
+
+def parse_peaks(d):
+    """HBM GB/s and dense bf16 TF/s from a driver-written MEASURED_PEAKS.json of unknown key
+    naming: the sustained figure is preferred (the dominant kernel is timed inside a long step),
+    TB/s and GFLOP/s are normalised; a figure that cannot be found keeps the fallback."""
+    flat = _flatten(d)
+
+    def pick(must, unit_fix):
+        cands = [(k, v) for k, v in flat.items() if any(m in k for m in must) and v > 0]
+        if not cands:
+            return None
+        cands.sort(key=lambda kv: (0 if "sustain" in kv[0] else 1 if "burst" not in kv[0] else 2, kv[0]))
+        return unit_fix(cands[0][1])
+
+    hbm = pick(("hbm", "copy", "dram"), lambda v: v * 1000.0 if v < 100 else v)
+    tc = pick(("bf16",), lambda v: v / 1000.0 if v > 20000 else (v * 1000.0 if v < 20 else v))
+    out = dict(PEAKS_FALLBACK)
+    if hbm:
+        out["hbm_gbs"] = hbm
+    if tc:
+        out["bf16_tflops"] = tc
+    return out, ("measured" if hbm else "fallback")
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
-        return d, "measured"
-    return PEAKS_FALLBACK, "fallback"
+        try:
+            with open(p) as f:
+                return parse_peaks(json.load(f))
+        except (OSError, ValueError):
+            pass
+    return dict(PEAKS_FALLBACK), "fallback"
 
 
 # ------------------------------------------------------------------ workload

@@ -115,9 +115,12 @@ enum {
     CVY_ENGINE_NO_PDL = 8,       /* no programmatic dependent launch between kernels        */
     CVY_ENGINE_NO_PERSISTENT = 16, /* one kernel per GEMM / attention instead of the
                                      persistent all-layers kernel (A/B and parity)          */
-    CVY_ENGINE_CHUNKED_PREFILL = 32 /* prompt and observation tokens (all but the last) run
+    CVY_ENGINE_CHUNKED_PREFILL = 32, /* prompt and observation tokens (all but the last) run
                                      as one batched prefill pass at the next step boundary
                                      instead of one token per decode step (NEXT-1)           */
+    CVY_ENGINE_TILED_WEIGHTS = 64 /* wqkv / wo / wgu / wd are tile-major (packed by
+                                     cvy_pack_weights_tiled); bf16 only, excludes the
+                                     persistent all-layers kernel                            */
 };
 
 typedef struct {
@@ -169,6 +172,19 @@ cvy_status cvy_weight_sizes_for(const cvy_model_config* m, uint32_t n_pages, cvy
  * (uniform, std 0.02; norms 1.0) on the given device.  Synchronous.  Zeroes nothing else. */
 cvy_status cvy_init_synthetic_weights(const cvy_model_config* m, const cvy_weights* w,
                                       uint64_t seed, int32_t device);
+
+/* Repack wqkv, wo, wgu and wd IN PLACE from the row-major layouts above into tile-major
+ * order, for an engine created with CVY_ENGINE_TILED_WEIGHTS.  Each [L*R][K] matrix (R rows
+ * per layer, K columns) becomes [L*R/128][K/64][128][64]: element (r, k) moves to
+ *   ((r / 128) * (K / 64) + k / 64) * 8192 + (r % 128) * 64 + k % 64,
+ * so every 128-row x 64-column weight tile a projection GEMM stage loads is 16 contiguous KB
+ * (one DRAM-friendly TMA box instead of 128 B from each of 128 rows; DESIGN.md §7.2 "Weight
+ * layout").  The weights are the same values (a permutation of their bytes); the GEMMs
+ * (the projections of the decode step) compute the same products.
+ * bf16 only; every R % 128 == 0 and K % 64 == 0, else CVY_E_INVAL and nothing is touched.
+ * Uses a device scratch buffer of one layer's largest matrix.  Synchronous.  Not idempotent:
+ * call once per weight set. */
+cvy_status cvy_pack_weights_tiled(const cvy_model_config* m, const cvy_weights* w, int32_t device);
 
 /* Create / destroy.  vocab_bytes [V][16] and vocab_lens [V] give the byte string of every
  * token id (<= 16 bytes; specials have length 0) and are copied. */

@@ -21,6 +21,7 @@ DELIM_NONE = 0xFFFF
 NO_TOKEN = 0xFFFFFFFF
 ENGINE_NO_GRAPH, ENGINE_DEBUG_LOGITS, ENGINE_SCAN_OFF, ENGINE_NO_PDL, ENGINE_NO_PERSISTENT = 1, 2, 4, 8, 16
 ENGINE_CHUNKED_PREFILL = 32
+ENGINE_TILED_WEIGHTS = 64
 
 c_i32, c_u32, c_u64, c_u16, c_f32, c_f64, c_sz, c_vp = (ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
                                                          ctypes.c_uint16, ctypes.c_float, ctypes.c_double,
@@ -93,6 +94,7 @@ PROTOTYPES = {
     "cvy_last_error": (ctypes.c_char_p, []),
     "cvy_weight_sizes_for": (c_i32, [ctypes.POINTER(ModelConfig), c_u32, ctypes.POINTER(WeightSizes)]),
     "cvy_init_synthetic_weights": (c_i32, [ctypes.POINTER(ModelConfig), ctypes.POINTER(Weights), c_u64, c_i32]),
+    "cvy_pack_weights_tiled": (c_i32, [ctypes.POINTER(ModelConfig), ctypes.POINTER(Weights), c_i32]),
     "cvy_engine_create": (c_i32, [ctypes.POINTER(ModelConfig), ctypes.POINTER(EngineConfig), ctypes.POINTER(Weights),
                                   ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(c_vp)]),
     "cvy_engine_destroy": (None, [c_vp]),

@@ -335,6 +335,7 @@ struct cvy_engine {
     int32_t* d_pk_err = nullptr;    // device alias of h_pk_err
     int32_t* h_pk_err = nullptr;    // first timed-out wait of the persistent kernel (0: none)
     bool pk_ok = false;             // model shape supported by the persistent kernel
+    bool w_tiled = false;           // projection weights packed tile-major (CVY_ENGINE_TILED_WEIGHTS)
     unsigned long long* d_trace = nullptr;  // test hook: GEMM CTA timestamps of one layer
     int trace_layer = -1;
     bool timing = false;        // launch the timed graph variant
@@ -468,6 +469,65 @@ cvy_status cvy_init_synthetic_weights(const cvy_model_config* m, const cvy_weigh
     return CVY_OK;
 }
 
+// Tile-major packing of the projection weights (DESIGN.md §7.2 "Weight layout").
+bool tiled_shape_ok(const cvy_model_config* m, std::string* why) {
+    const int64_t d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim, dff = m->d_ff;
+    if (m->dtype != CVY_DTYPE_BF16) {
+        *why = "tile-major weights are bf16 only";
+        return false;
+    }
+    if (((H + 2 * Hkv) * hd) % 128 || d % 128 || (2 * dff) % 128 || d % 64 || (H * hd) % 64 || dff % 64) {
+        *why = "tile-major weights need every projection's rows % 128 == 0 and columns % 64 == 0";
+        return false;
+    }
+    return true;
+}
+
+// dst[((r / 128) * (K / 64) + k / 64) * 8192 + (r % 128) * 64 + k % 64] = src[r * K + k] for one
+// [R][K] bf16 block (R % 128 == 0); 16 bytes per thread step.
+__global__ void pack_tiled_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t R, int64_t K) {
+    const int64_t n = R * K / 8, kc = K / 8, KB = K / 64;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / kc, k = (i % kc) * 8;
+        dst[(((r / 128) * KB + k / 64) * 8192 + (r % 128) * 64 + k % 64) / 8] = src[i];
+    }
+}
+
+cvy_status cvy_pack_weights_tiled(const cvy_model_config* m, const cvy_weights* w, int32_t device) {
+    std::string why;
+    if (!model_ok(m, &why) || !w) return fail(CVY_E_INVAL, why.empty() ? "null weights" : why);
+    if (!w->wqkv || !w->wo || !w->wgu || !w->wd) return fail(CVY_E_INVAL, "null weight pointer");
+    if (!tiled_shape_ok(m, &why)) return fail(CVY_E_INVAL, why);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(CVY_E_CUDA, "no CUDA device");
+    CUDA_TRY(cudaSetDevice(device));
+    const int64_t L = m->n_layers, d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim,
+                  dff = m->d_ff;
+    const int64_t R[4] = {(H + 2 * Hkv) * hd, d, 2 * dff, d}, K[4] = {d, H * hd, d, dff};
+    // the pack rewrites the caller's buffers (documented in conveyor.h); cvy_weights holds them const
+    void* base[4] = {const_cast<void*>(w->wqkv), const_cast<void*>(w->wo), const_cast<void*>(w->wgu),
+                     const_cast<void*>(w->wd)};
+    size_t tmp_bytes = 0;
+    for (int q = 0; q < 4; ++q) tmp_bytes = std::max(tmp_bytes, (size_t)(R[q] * K[q] * 2));
+    void* tmp = nullptr;
+    CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
+    cudaError_t err = cudaSuccess;
+    // one layer at a time through a scratch copy: a layer's tiles occupy exactly its own bytes
+    for (int q = 0; q < 4 && err == cudaSuccess; ++q)
+        for (int64_t l = 0; l < L && err == cudaSuccess; ++l) {
+            uint8_t* blk = (uint8_t*)base[q] + (size_t)l * R[q] * K[q] * 2;
+            err = cudaMemcpy(tmp, blk, (size_t)R[q] * K[q] * 2, cudaMemcpyDeviceToDevice);
+            if (err == cudaSuccess) {
+                pack_tiled_kernel<<<1184, 256>>>((uint4*)blk, (const uint4*)tmp, R[q], K[q]);
+                err = cudaGetLastError();
+            }
+        }
+    if (err == cudaSuccess) err = cudaDeviceSynchronize();
+    cudaFree(tmp);
+    if (err != cudaSuccess) return fail(CVY_E_CUDA, cudaGetErrorString(err));
+    return CVY_OK;
+}
+
 void cvy_engine_destroy(cvy_engine* e);
 
 cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config* ec, const cvy_weights* w,
@@ -493,7 +553,10 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     if (prop.major != 10) return fail(CVY_E_CUDA, "libconveyor is built for sm_100a (B200) only");
     CUDA_TRY(cudaSetDevice(ec->device));
 
+    if ((ec->flags & CVY_ENGINE_TILED_WEIGHTS) && !tiled_shape_ok(m, &why)) return fail(CVY_E_INVAL, why);
+
     cvy_engine* e = new cvy_engine();
+    e->w_tiled = (ec->flags & CVY_ENGINE_TILED_WEIGHTS) != 0;
     e->m = *m;
     e->c = *ec;
     e->w = *w;
@@ -558,7 +621,8 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * acc_cols);
     ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
     e->pk_ok = e->bf16 && hd == 128 && (H / Hkv) <= 4 && H % Hkv == 0 && d % 128 == 0 && ((H + 2 * Hkv) * hd) % 128 == 0 &&
-               (2 * dff) % 128 == 0 && (H * hd) % 64 == 0 && dff % 64 == 0 && !(ec->flags & CVY_ENGINE_NO_PERSISTENT);
+               (2 * dff) % 128 == 0 && (H * hd) % 64 == 0 && dff % 64 == 0 && !(ec->flags & CVY_ENGINE_NO_PERSISTENT) &&
+               !(ec->flags & CVY_ENGINE_TILED_WEIGHTS);  // the persistent kernel reads row-major weights
     // opt-in until it beats the one-kernel-per-op path (DESIGN.md §7 "Persistent layer kernel")
     {
         const char* pe = getenv("CVY_PERSISTENT");
@@ -1135,8 +1199,16 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         g.part = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
         g.x_plane_rows = (int32_t)xcap;
-        if (!make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub),
-                       (uint32_t)g.bk)) {
+        g.wtiled = e->w_tiled && (Wbase == e->w.wqkv || Wbase == e->w.wo || Wbase == e->w.wgu || Wbase == e->w.wd);
+        if (g.wtiled && g.bk != 64) {
+            *why = "tile-major weights need 64-element k-blocks (batch tiles of <= 128 columns)";
+            return false;
+        }
+        if (g.wtiled) g.l2_prefetch = 0;
+        // tile-major: a [rows * K / 64][64] view, box = one 128-row x 64-column tile (16 KB)
+        if (!(g.wtiled ? make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total * K / 64, 64, 64, 128, 64)
+                       : make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K,
+                                   (uint32_t)(128 * g.nsub), (uint32_t)g.bk))) {
             *why = "cuTensorMapEncodeTiled (weights) failed";
             return false;
         }
@@ -1209,7 +1281,7 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
             nx.w_row0 = b.g.w_row0;
             nx.grid = b.grid;
             nx.bk = b.g.bk;
-            nx.blocks = std::max(0, pf_kb * 1024 / (nx.rows_per_tile * nx.bk * 2));
+            nx.blocks = b.g.wtiled ? 0 : std::max(0, pf_kb * 1024 / (nx.rows_per_tile * nx.bk * 2));
             a.tmN = b.tmW;
         }
     }

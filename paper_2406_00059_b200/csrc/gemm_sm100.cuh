@@ -52,6 +52,9 @@ struct GemmTC {
     int32_t split;      // 0: stream-K over all CTAs; S >= 1: tile = blockIdx/S, K split over the S
                         //    CTAs of a thread-block cluster, reduced through DSMEM
     int32_t w_row0;     // first row of this layer's matrix in the weight tensor map
+    int32_t wtiled;     // 1: weights packed tile-major [rows/128][K/64][128][64] (cvy_pack_weights_tiled):
+                        //    every 128-row x 64-column box is 16 contiguous KB (row-major boxes
+                        //    read 128 B from each of 128 rows; DESIGN.md §7.2 "Weight layout")
     int32_t x_plane_rows;  // row offset of the lo plane in the activation tensor map
     float* part;        // [tiles][nsub*128][Bp] fp32 accumulators of shared tiles (zero between uses)
     int32_t* tile_cnt;  // [tiles] arrival tickets (zero between uses; reset by the last arriver)
@@ -110,6 +113,21 @@ CVY_DEV void prefetch_next_gemm(const GemmTC& G, const CUtensorMap* tmN, int lan
         for (long long i = a0; i < a1; ++i, ++j)
             if ((j & 31) == lane)
                 tma_prefetch_l2_2d(tmN, (int)(i % nx.kblocks) * nx.bk, nx.w_row0 + (int)(i / nx.kblocks) * nx.rows_per_tile);
+    }
+}
+
+// Weight k-block kb of row tile `tile` (128 * nsub rows) into the stage's weight slot.
+template <int NSUB, int BK>
+CVY_DEV void load_w_tile(void* dst, const CUtensorMap* tmW, uint64_t* bar, const GemmTC& G, int tile, int kb,
+                         uint64_t pol) {
+    if (!G.wtiled) {
+        tma_load_2d(dst, tmW, bar, kb * BK, G.w_row0 + tile * 128 * NSUB, pol);
+    } else {
+#pragma unroll
+        for (int s = 0; s < NSUB; ++s) {
+            const int rt = G.w_row0 / 128 + tile * NSUB + s;
+            tma_load_2d(static_cast<uint8_t*>(dst) + s * 16384, tmW, bar, 0, (rt * G.kblocks + kb) * 128, pol);
+        }
     }
 }
 
@@ -209,12 +227,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const long long it = it0 + i;
                 const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
                 mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
-                tma_load_2d(smem + (size_t)i * stage_bytes, &tmW, &full_bar[i], kb * BK, G.w_row0 + tile * rows_per_tile,
-                            pol_w);
+                load_w_tile<NSUB, BK>(smem + (size_t)i * stage_bytes, &tmW, &full_bar[i], G, tile, kb, pol_w);
             }
             // deeper look-ahead into L2 while the previous kernel drains (HBM would idle otherwise)
             const long long pf_end = min(it1, it0 + pre + (long long)G.l2_prefetch);
-            for (long long it = it0 + pre; it < pf_end; ++it)
+            for (long long it = it0 + pre; it < pf_end && !G.wtiled; ++it)
                 tma_prefetch_l2_2d(&tmW, (int)(it % G.kblocks) * BK, G.w_row0 + (int)(it / G.kblocks) * rows_per_tile);
             pdl_wait();
             for (int i = 0; i < pre; ++i) {
@@ -232,7 +249,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
                 uint8_t* sw = smem + (size_t)stage * stage_bytes;
                 mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
-                tma_load_2d(sw, &tmW, &full_bar[stage], kb * BK, G.w_row0 + tile * rows_per_tile, pol_w);
+                load_w_tile<NSUB, BK>(sw, &tmW, &full_bar[stage], G, tile, kb, pol_w);
                 for (int pl = 0; pl < 2; ++pl)
                     for (int h = 0; h < xh; ++h)
                         tma_load_2d(sw + WB + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[stage], kb * BK,

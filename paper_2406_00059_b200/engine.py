@@ -22,10 +22,26 @@ def model_config(shape, dtype: str = "bf16") -> capi.ModelConfig:
                             capi.DTYPE_BF16 if dtype == "bf16" else capi.DTYPE_FP32)
 
 
-class DeviceModel:
-    """Weights + KV pool as torch CUDA tensors (borrowed by the engine)."""
+def tiled_default(shape, dtype: str) -> bool:
+    """Tile-major projection weights (CVY_ENGINE_TILED_WEIGHTS) unless the shape cannot be
+    tiled, the persistent all-layers kernel (row-major weights) is requested, or
+    CVY_TILED_WEIGHTS=0."""
+    import os
+    if dtype != "bf16" or os.environ.get("CVY_TILED_WEIGHTS", "1") == "0":
+        return False
+    if os.environ.get("CVY_PERSISTENT", "0") not in ("", "0"):
+        return False
+    rows = [(shape.H + 2 * shape.Hkv) * shape.hd, shape.d, 2 * shape.dff]
+    cols = [shape.d, shape.H * shape.hd, shape.dff]
+    return all(r % 128 == 0 for r in rows) and all(c % 64 == 0 for c in cols)
 
-    def __init__(self, shape, dtype: str, n_pages: int, seed: int, device: int = 0):
+
+class DeviceModel:
+    """Weights + KV pool as torch CUDA tensors (borrowed by the engine).  `tiled`: pack the
+    projection weights tile-major (cvy_pack_weights_tiled); engines over this model get
+    CVY_ENGINE_TILED_WEIGHTS automatically."""
+
+    def __init__(self, shape, dtype: str, n_pages: int, seed: int, device: int = 0, tiled: bool | None = None):
         import torch
         self.shape = shape
         self.n_pages = n_pages
@@ -41,6 +57,9 @@ class DeviceModel:
         self.tensors["kv_pool"].zero_()
         self.w = capi.Weights(*[self.tensors[n].data_ptr() for n, _ in capi.Weights._fields_])
         check(capi.lib().cvy_init_synthetic_weights(ctypes.byref(self.cfg), ctypes.byref(self.w), seed, device))
+        self.tiled = tiled_default(shape, dtype) if tiled is None else bool(tiled)
+        if self.tiled:
+            check(capi.lib().cvy_pack_weights_tiled(ctypes.byref(self.cfg), ctypes.byref(self.w), device))
 
     def tensor(self, name):
         return self.tensors[name]
@@ -74,6 +93,8 @@ class Engine:
             ring_records = 1
             while ring_records < 64 * max_slots:
                 ring_records <<= 1
+        if getattr(model, "tiled", False):
+            flags |= capi.ENGINE_TILED_WEIGHTS
         self.ecfg = capi.EngineConfig(max_slots, n_pages if n_pages is not None else model.n_pages, max_pages_per_slot,
                                       ring_records, round_bytes, round_tokens, input_cap, forced_cap, device, flags)
         h = ctypes.c_void_p()

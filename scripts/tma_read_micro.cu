@@ -122,6 +122,64 @@ __global__ void __launch_bounds__(64, 1) rd_bulk(const uint8_t* src, size_t byte
     }
 }
 
+// GEMM-shaped stream: per stage, 2 boxes of 128 rows x 64 cols (32 KB, this CTA's weight rows,
+// k-block kb) + 1 box of 128 rows of a shared 128-row x K "activation" matrix (16 KB, the same
+// for every CTA at the same kb).  rot != 0 starts CTA c at k-block (c * rot) % KB.
+__global__ void __launch_bounds__(64, 1) rd_gemmlike(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
+                                                      int KB, int stages, int rot, int with_x, int layout,
+                                                      unsigned long long* sink) {
+    extern __shared__ __align__(1024) uint8_t raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[16], empty[16];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int SB = 48 * 1024;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int i = 0; i < KB; ++i) {
+                const int kb = (i + blockIdx.x * rot) % KB;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_arrive_expect_tx(&full[s], with_x ? SB : 32768);
+                uint8_t* d = ring + (size_t)s * SB;
+                if (layout == 0) {  // row-major [N][K]: 128 rows x 128 B per box
+                    tma_load_2d(d, &tw, &full[s], kb * 64, blockIdx.x * 256, pol);
+                    tma_load_2d(d + 16384, &tw, &full[s], kb * 64, blockIdx.x * 256 + 128, pol);
+                } else if (layout == 1) {  // row-major, one 128-row sub x two adjacent k-blocks
+                    const int sub = i & 1, kp = (i >> 1) * 2;
+                    tma_load_2d(d, &tw, &full[s], kp * 64, blockIdx.x * 256 + sub * 128, pol);
+                    tma_load_2d(d + 16384, &tw, &full[s], kp * 64 + 64, blockIdx.x * 256 + sub * 128, pol);
+                } else {  // tile-major [N/128][K/64][128][64]: each box is 16 contiguous KB
+                    tma_load_2d(d, &tw, &full[s], 0, ((blockIdx.x * 2 + 0) * KB + kb) * 128, pol);
+                    tma_load_2d(d + 16384, &tw, &full[s], 0, ((blockIdx.x * 2 + 1) * KB + kb) * 128, pol);
+                }
+                if (with_x) tma_load_2d(d + 32768, &tx, &full[s], kb * 64, 0, policy_evict_last());
+                if (++s == stages) { s = 0; ph ^= 1u; }
+            }
+        }
+    } else if (lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        unsigned long long acc = 0;
+        for (int i = 0; i < KB; ++i) {
+            mbar_wait(&full[s], ph);
+            acc += *reinterpret_cast<volatile uint32_t*>(ring + (size_t)s * SB);
+            mbar_arrive(&empty[s]);
+            if (++s == stages) { s = 0; ph ^= 1u; }
+        }
+        if (acc == 0x123456789ull) *sink = acc;
+    }
+}
+
 __global__ void rd_ldg(const int4* src, size_t n16, unsigned long long* sink) {
     unsigned long long acc = 0;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -189,6 +247,63 @@ int main() {
                 snprintf(name, sizeof name, "tma box%dx64 %dx%dKB%s", br, st, c[1], sc ? " scatter" : "");
                 timeit(name, [&] { rd_tma<<<nsm, 64, smem>>>(tm, (uint32_t)(rows / 16), br, st, sb, sc, sink); });
             }
+        }
+    }
+    // per-SM ceiling: the same stream on fewer CTAs (one per SM)
+    {
+        CUtensorMap tm;
+        cuuint64_t gdim[2] = {128, rows}, gstride[1] = {256};
+        cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+        enc()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const int cfg[][2] = {{3, 64}, {6, 32}, {12, 16}};
+        for (auto& c : cfg) {
+            const int st = c[0], sb = c[1] * 1024;
+            const size_t smem = (size_t)st * sb + 1024;
+            cudaFuncSetAttribute(rd_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            for (int grid : {148, 128, 112, 96, 74}) {
+                char name[96];
+                snprintf(name, sizeof name, "tma box128x64 %dx%dKB grid %d", st, c[1], grid);
+                timeit(name, [&] { rd_tma<<<grid, 64, smem>>>(tm, (uint32_t)(rows / 16), 128, st, sb, 0, sink); });
+            }
+        }
+    }
+    // gate/up-shaped: 112 CTAs x 256 weight rows x K = 4096 (bf16) = 235 MB, + shared X (128 x 4096)
+    {
+        const int K = 4096, KB = K / 64, NR = 28672;
+        CUtensorMap tw, tx;
+        cuuint64_t gw[2] = {(cuuint64_t)K, (cuuint64_t)NR}, sw[1] = {(cuuint64_t)K * 2};
+        cuuint64_t gx[2] = {(cuuint64_t)K, 128}, sx[1] = {(cuuint64_t)K * 2};
+        cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+        enc()(&tw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gw, sw, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CUtensorMap tt;  // tile-major view of the same bytes: rows of 64 elements
+        cuuint64_t gt[2] = {64, (cuuint64_t)NR * K / 64}, st_[1] = {128};
+        enc()(&tt, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, gt, st_, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        enc()(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf + (size_t)NR * K * 2, gx, sx, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        const size_t wbytes = (size_t)NR * K * 2;
+        for (int st : {3, 4}) {
+            const size_t smem = (size_t)st * 48 * 1024 + 1024;
+            cudaFuncSetAttribute(rd_gemmlike, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            for (int lay = 0; lay < 3; ++lay)
+            for (int wx = 0; wx < 2; ++wx)
+                for (int rot : {0, 1}) {
+                    if (!wx && rot) continue;
+                    const int reps = 10;
+                    rd_gemmlike<<<112, 64, smem>>>(lay == 2 ? tt : tw, tx, KB, st, rot, wx, lay, sink);
+                    cudaDeviceSynchronize();
+                    cudaEventRecord(e0);
+                    for (int r = 0; r < reps; ++r) rd_gemmlike<<<112, 64, smem>>>(lay == 2 ? tt : tw, tx, KB, st, rot, wx, lay, sink);
+                    cudaEventRecord(e1);
+                    cudaError_t err = cudaEventSynchronize(e1);
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    printf("gemmlike 112 CTAs layout %d %d x 48KB x=%d rot=%d: %.1f us/launch, weights %.1f GB/s  %s\n",
+                           lay, st, wx, rot, ms * 1e3 / reps, wbytes * reps / (ms * 1e-3) / 1e9, cudaGetErrorString(err));
+                }
         }
     }
     const int chunks[] = {4096, 8192, 16384};

@@ -71,6 +71,21 @@ def test_no_gpu_fails_loudly(lib):
     assert lib.cvy_debug_gemm(None, None, None, 128, 64, 4, 1, 0, None) == capi.CVY_E_INVAL
 
 
+def test_pack_weights_tiled_rejects_before_touching_memory(lib):
+    """cvy_pack_weights_tiled validates dtype and shape before any device work (no GPU needed):
+    fp32 and projections whose rows are not multiples of 128 are CVY_E_INVAL."""
+    from inputs.configs import ModelShape
+    w = capi.Weights(*([1] * 10))
+    cfg = model_config(TINY, "fp32")
+    assert lib.cvy_pack_weights_tiled(ctypes.byref(cfg), ctypes.byref(w), 0) == capi.CVY_E_INVAL
+    assert b"bf16" in lib.cvy_last_error()
+    odd = ModelShape("odd", L=1, d=128, H=4, Hkv=1, hd=32, dff=384, V=256, eps=1e-5, rope_base=1e4, eos=-1)  # 192 QKV rows
+    cfg = model_config(odd, "bf16")
+    assert lib.cvy_pack_weights_tiled(ctypes.byref(cfg), ctypes.byref(w), 0) == capi.CVY_E_INVAL
+    assert b"% 128" in lib.cvy_last_error()
+    assert lib.cvy_pack_weights_tiled(ctypes.byref(cfg), None, 0) == capi.CVY_E_INVAL
+
+
 def test_null_engine_calls_are_errors(lib):
     assert lib.cvy_step(None, None) == capi.CVY_E_INVAL
     assert lib.cvy_cancel_request(None, 1) == capi.CVY_E_INVAL

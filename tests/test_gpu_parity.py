@@ -81,6 +81,40 @@ def test_7b_two_layer_slice_bf16(persistent, monkeypatch):
     assert d < 2e-2
 
 
+def test_pack_weights_tiled_is_the_tile_permutation():
+    """cvy_pack_weights_tiled moves element (r, k) of every [L*R][K] projection matrix to
+    ((r/128)*(K/64) + k/64)*8192 + (r%128)*64 + k%64 (conveyor.h): bit-exact against the
+    row-major weights viewed as [L*R/128][128][K/64][64] and transposed on the middle axes."""
+    import torch
+    from paper_2406_00059_b200.engine import DeviceModel
+    ensure_built()
+    sh = slice_of(MISTRAL_7B, L=2, name="7b-L2")
+    row = DeviceModel(sh, "bf16", 16, seed=7, tiled=False)
+    til = DeviceModel(sh, "bf16", 16, seed=7, tiled=True)
+    mats = {"wqkv": ((sh.H + 2 * sh.Hkv) * sh.hd, sh.d), "wo": (sh.d, sh.H * sh.hd), "wgu": (2 * sh.dff, sh.d),
+            "wd": (sh.d, sh.dff)}
+    for name, (R, K) in mats.items():
+        n = sh.L * R * K * 2
+        a = row.tensor(name)[:n].view(torch.int16).view(sh.L * R // 128, 128, K // 64, 64)
+        b = til.tensor(name)[:n].view(torch.int16).view(sh.L * R // 128, K // 64, 128, 64)
+        assert torch.equal(a.permute(0, 2, 1, 3).contiguous(), b), name
+    for name in ("embed", "lm_head", "final_norm", "attn_norm", "mlp_norm"):
+        assert torch.equal(row.tensor(name), til.tensor(name)), name
+
+
+@pytest.mark.parametrize("tiled", ["1", "0"])
+def test_7b_two_layer_slice_weight_layouts(tiled, monkeypatch):
+    """The projection GEMMs over tile-major (CVY_ENGINE_TILED_WEIGHTS) and row-major weights."""
+    monkeypatch.setenv("CVY_PERSISTENT", "0")
+    monkeypatch.setenv("CVY_TILED_WEIGHTS", tiled)
+    shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
+    vocab = synthetic_vocab(32000)
+    prompts = [[1, 300, 5000], [1, 77], [1, 31999, 2000, 12]]
+    d, _ = free_running_parity(shape, "bf16", vocab, prompts, max_new=3, seed=1003, tol=2e-2, prefix=40,
+                               synth_seeds=[11, 12, 13])
+    assert d < 2e-2
+
+
 def set_mode(monkeypatch, mode):
     """mode "1": persistent all-layers kernel; "0": one kernel per op; "attn": one kernel per op
     with the persistent attention kernel (attention_pk.cuh; hd 128, G <= 4, else attention_tc)."""

@@ -201,3 +201,16 @@ def test_refill_admits_waiting_requests_and_partial_aborts_free_slots_sooner():
         assert peak <= 2
         spans[mode] = max(lg.t_done for lg in logs) - t0
     assert spans[capi.MODE_PARTIAL] < spans[capi.MODE_SEQUENTIAL]
+
+
+def test_bench_peak_parsing_units_and_preference():
+    """bench.parse_peaks reads a driver-written MEASURED_PEAKS.json of unknown key naming:
+    sustained over burst, TB/s -> GB/s, GFLOP/s -> TF/s, and the fallback when nothing matches."""
+    import bench
+    p, src = bench.parse_peaks({"hbm_copy_gbs": {"burst": 7300.0, "sustained": 6900.0},
+                                "bf16_dense_tflops": {"burst": 1650.0, "sustained": 1380.0}})
+    assert src == "measured" and p == {"hbm_gbs": 6900.0, "bf16_tflops": 1380.0}
+    p, src = bench.parse_peaks({"hbm_tbs": 6.54, "cublas_bf16_gflops": 1648400.0})
+    assert src == "measured" and p["hbm_gbs"] == 6540.0 and abs(p["bf16_tflops"] - 1648.4) < 1e-9
+    p, src = bench.parse_peaks({"unrelated": 1, "flag": True})
+    assert src == "fallback" and p == bench.PEAKS_FALLBACK
