@@ -1198,6 +1198,9 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         }
         g.part = e->d_gemm_acc;
         g.tile_cnt = e->d_tile_cnt;
+        // measurement knob (wrong results): the gate/up epilogue's debug bits (GemmTC::dbg)
+        if (const char* dg = getenv("CVY_GEMM_DBG_GU"))
+            if (epi.kind == EPI_SWIGLU) g.dbg = atoi(dg);
         g.x_plane_rows = (int32_t)xcap;
         g.wtiled = e->w_tiled && (Wbase == e->w.wqkv || Wbase == e->w.wo || Wbase == e->w.wgu || Wbase == e->w.wd);
         if (g.wtiled && g.bk != 64) {

@@ -238,7 +238,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                     for (int r = 0; r < 16; ++r) {
                         const float g = esm[(part * 16 + r) * kEsmLd + col];
                         const float u = esm[(64 + part * 16 + r) * kEsmLd + col];
-                        a[r] = g / (1.f + __expf(-g)) * u;
+                        a[r] = __fdividef(g, 1.f + __expf(-g)) * u;  // silu(g) u; 1 + e^-g >= 1
                     }
                     store_act_row16<T>(reinterpret_cast<T*>(P.h) + (size_t)(cb + col) * P.act_ld + j0,
                                        (size_t)P.act_plane, a);

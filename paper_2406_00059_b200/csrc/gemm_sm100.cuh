@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr uint32_t WB = NSUB * 128u * ROW;        // weight bytes per stage
     constexpr int KSTEPS = BK / 16;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // aligned by an offset from smem_raw (not a uintptr round trip), so the compiler keeps the
+    // shared state space and the epilogue's exchange / metadata accesses compile to LDS / STS
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int Bp = G.bq;                              // this CTA's batch columns
     const int cbase = (int)blockIdx.y * G.bq;         // first batch column of this CTA
     const uint32_t XB = (uint32_t)Bp * ROW;           // one activation plane per stage
