@@ -39,14 +39,15 @@ __global__ void __launch_bounds__((kApConsumers + 1) * 32, 1)
                                 int layer, int nstages) {
     constexpr int HD = 128;
     extern __shared__ __align__(1024) uint8_t ap_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ap_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = ap_raw + ((1024u - (smem_u32(ap_raw) & 1023u)) & 1023u);  // keeps the shared state space
     uint8_t* ring = sm;
     uint16_t* pbuf = reinterpret_cast<uint16_t*>(ring + (size_t)nstages * kApStage);
     float* comb = reinterpret_cast<float*>(pbuf + kApConsumers * 128);
     int* nch = reinterpret_cast<int*>(comb + kApWarps * (8 + 4 * HD));
     int* pre = nch + kApMaxRows;        // [kApMaxRows + 1]
     int* nkeys = pre + kApMaxRows + 1;  // [kApMaxRows]
-    uint64_t* full = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(nkeys + kApMaxRows) + 15) & ~uintptr_t(15));
+    uint8_t* bars = reinterpret_cast<uint8_t*>(nkeys + kApMaxRows);
+    uint64_t* full = reinterpret_cast<uint64_t*>(bars + ((16u - (smem_u32(bars) & 15u)) & 15u));
     uint64_t* empty = full + nstages;
 
     pdl_launch_dependents();

@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     constexpr int STAGE = PPS * 2 * BLK;                 // K and V of PPS pages
     constexpr int KSTEPS = HD / 16;
     extern __shared__ __align__(1024) uint8_t asm_raw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(asm_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sm = asm_raw + ((1024u - (smem_u32(asm_raw) & 1023u)) & 1023u);  // keeps the shared state space
     uint8_t* stages = sm;
     uint16_t* pbuf = reinterpret_cast<uint16_t*>(sm + STAGES * STAGE);  // [warp][8][16] bf16
     float* comb = reinterpret_cast<float*>(pbuf + kAtcWarps * 8 * 16);      // [warp][4 m, 4 l, 4*HD O]

@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(kPkThreads, 1)
                              const __grid_constant__ CUtensorMap tmXh, const __grid_constant__ CUtensorMap tmKV,
                              const __grid_constant__ StepParams P, const __grid_constant__ PkParams K) {
     extern __shared__ __align__(1024) uint8_t pk_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(pk_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = pk_raw + ((1024u - (smem_u32(pk_raw) & 1023u)) & 1023u);  // keeps the shared state space
     const int SW = K.w_stages, SX = K.x_stages;
     uint8_t* wring = smem;
     uint8_t* xring = wring + (size_t)SW * kPkWStage;
