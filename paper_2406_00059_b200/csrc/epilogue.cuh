@@ -121,12 +121,15 @@ template <typename T> CVY_DEV void store_act_row32(T* dst, size_t plane, const f
 template <typename T> CVY_DEV void store_act_row16(T* dst, size_t plane, const float* w) { store_act_rows<T, 16>(dst, plane, w); }
 
 // One 32-column chunk of one 128-row sub-tile.  n0 = first global row of the sub-tile.
-template <typename T, int KIND = -1>
+// W = columns in v (32, or 16 for the split-K reduce-scatter units): the per-row loops run W
+// iterations (instruction latency is what bounds an epilogue).
+template <typename T, int KIND = -1, int W = 32>
 CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int cb, float* v, float* esm,
-                            const EpiMeta& M, int et, int width = 32) {
+                            const EpiMeta& M, int et) {
+    static_assert(W == 16 || W == 32, "chunk width");
     const float* s_scale = M.scale;
     const int n = n0 + et;
-    const int ncols = min(width, P.Bp - cb);
+    const int ncols = min(W, P.Bp - cb);
     switch (KIND >= 0 ? KIND : E.kind) {
         case EPI_QKV: {
             const int hd = P.hd, half = hd >> 1;
@@ -137,23 +140,23 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
             // all global inputs first (RoPE cos/sin of every column), then compute, then store
             float2 cs[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < W; ++i)
                 cs[i] = (rot && i < ncols) ? __ldg(&P.rope[(size_t)M.pos[cb + i] * half + j]) : make_float2(1.f, 0.f);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= s_scale[cb + i];
+            for (int i = 0; i < W; ++i) v[i] *= s_scale[cb + i];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = v[i];
+            for (int i = 0; i < W; ++i) esm[et * kEsmLd + i] = v[i];
             epi_sync();
             const int partner = et ^ half;
             float out[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
+            for (int i = 0; i < W; ++i) {
                 const float pv = esm[partner * kEsmLd + i];
                 out[i] = dim < half ? (v[i] * cs[i].x - pv * cs[i].y) : (v[i] * cs[i].x + pv * cs[i].y);
             }
             epi_sync();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = out[i];
+            for (int i = 0; i < W; ++i) esm[et * kEsmLd + i] = out[i];
             epi_sync();
             // transposed stores: thread -> (column b, 32 consecutive rows), 16-byte vectors
             {
@@ -185,25 +188,29 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
         case EPI_RESID: {
             // v: this thread's row (n0 + et) for 32 columns -> esm; then thread -> (column b,
             // 32 consecutive rows): x += v, act = x * w_norm (hi, lo), sum of squares
+            const int col = et >> 2, part = et & 3;
+            const int r0 = n0 + part * 32;
+            const bool ok = col < ncols && r0 < E.N;
+            const int b = cb + col;
+            // the residual and norm-weight loads do not depend on the exchange: issue them first
+            // so their latency hides behind the exchange stores and barrier
+            float xv[32], wn[32];
+            if (ok) {
+                const float4* xs = reinterpret_cast<const float4*>(P.x + (size_t)b * P.d + r0);
+                const float4* ws = reinterpret_cast<const float4*>(E.norm_w + r0);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = v[i];
+                for (int q = 0; q < 8; ++q) {
+                    const float4 a = xs[q], w4 = __ldg(ws + q);
+                    xv[4 * q] = a.x; xv[4 * q + 1] = a.y; xv[4 * q + 2] = a.z; xv[4 * q + 3] = a.w;
+                    wn[4 * q] = w4.x; wn[4 * q + 1] = w4.y; wn[4 * q + 2] = w4.z; wn[4 * q + 3] = w4.w;
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < W; ++i) esm[et * kEsmLd + i] = v[i];
             epi_sync();
             {
-                const int col = et >> 2, part = et & 3;
-                const int r0 = n0 + part * 32;
-                const bool ok = col < ncols && r0 < E.N;
-                const int b = cb + col;
                 float ss = 0.f;
                 if (ok) {
-                    float xv[32], wn[32];
-                    const float4* xs = reinterpret_cast<const float4*>(P.x + (size_t)b * P.d + r0);
-                    const float4* ws = reinterpret_cast<const float4*>(E.norm_w + r0);
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        const float4 a = xs[q], w4 = __ldg(ws + q);
-                        xv[4 * q] = a.x; xv[4 * q + 1] = a.y; xv[4 * q + 2] = a.z; xv[4 * q + 3] = a.w;
-                        wn[4 * q] = w4.x; wn[4 * q + 1] = w4.y; wn[4 * q + 2] = w4.z; wn[4 * q + 3] = w4.w;
-                    }
 #pragma unroll
                     for (int r = 0; r < 32; ++r) {
                         xv[r] += esm[(part * 32 + r) * kEsmLd + col];
@@ -227,7 +234,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
         case EPI_SWIGLU: {
             // sub-tile rows 0..63: gate rows j0..j0+63; rows 64..127: up rows j0..j0+63
 #pragma unroll
-            for (int i = 0; i < 32; ++i) esm[et * kEsmLd + i] = v[i] * s_scale[cb + i];
+            for (int i = 0; i < W; ++i) esm[et * kEsmLd + i] = v[i] * s_scale[cb + i];
             epi_sync();
             {
                 const int col = et >> 2, part = et & 3;   // part -> 16 consecutive j

@@ -476,14 +476,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int units = NSUB * (Bp / 16);
             const int tile = blockIdx.x / G.split;
             const uint32_t base = smem_u32(smem);
-            for (int u = crank; u < units; u += G.split) {
-                float v[32];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0.f;
-                const uint32_t off = (uint32_t)(((size_t)u * 512 + et) * 16);
-                // all S*4 remote loads in flight at once (DSMEM round trips are ~200 cycles),
-                // then the sum in rank order
-                float4 t4[4][4];
+            // all S*4 remote loads of a unit in flight at once (DSMEM round trips are ~200
+            // cycles), then the sum in rank order; the next unit's loads are issued before this
+            // unit's epilogue so their latency overlaps it
+            float4 t4[4][4];
+            auto issue = [&](int uu) {
+                const uint32_t off = (uint32_t)(((size_t)uu * 512 + et) * 16);
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                     if (r < G.split) {
@@ -491,6 +489,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                         for (int q = 0; q < 4; ++q) t4[r][q] = ld_dsmem_f4(a + 2048u * q);
                     }
+            };
+            if (crank < units) issue(crank);
+            for (int u = crank; u < units; u += G.split) {
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0.f;
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                     if (r < G.split) {
@@ -502,10 +506,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             v[4 * q + 3] += t4[r][q].w;
                         }
                     }
+                if (u + G.split < units) issue(u + G.split);
                 const int s = u / (Bp / 16), cb = (u % (Bp / 16)) * 16;
                 if (tr && et == 0 && u == crank) tr[8] = gtimer();
                 if (!(G.dbg & 8))
-                    epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, threadIdx.x, 16);
+                    epilogue_chunk<T, EPI, 16>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, threadIdx.x);
                 if (tr && et == 0 && u == crank) tr[9] = gtimer();
             }
         }
