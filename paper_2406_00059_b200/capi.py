@@ -7,7 +7,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libconveyor.so")
+LIB_PATH = os.environ.get("CVY_LIB_PATH") or os.path.join(HERE, "libconveyor.so")  # override: A/B builds
 
 CVY_OK, CVY_E_INVAL, CVY_E_NOMEM, CVY_E_FULL, CVY_E_AGAIN = 0, -1, -2, -3, -4
 CVY_E_NOTFOUND, CVY_E_STATE, CVY_E_DUP, CVY_E_CUDA, CVY_E_NCCL = -5, -6, -7, -8, -9

@@ -82,6 +82,27 @@ template <> CVY_DEV void store_row32<__nv_bfloat16>(__nv_bfloat16* dst, const fl
                           *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
     }
 }
+// NR (16 or 32) consecutive rows of one column, 16-byte vectors
+template <typename T, int NR> CVY_DEV void store_rows(T* dst, const float* w);
+template <> CVY_DEV void store_rows<float, 32>(float* dst, const float* w) { store_row32<float>(dst, w); }
+template <> CVY_DEV void store_rows<__nv_bfloat16, 32>(__nv_bfloat16* dst, const float* w) { store_row32<__nv_bfloat16>(dst, w); }
+template <> CVY_DEV void store_rows<float, 16>(float* dst, const float* w) {
+    float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+}
+template <> CVY_DEV void store_rows<__nv_bfloat16, 16>(__nv_bfloat16* dst, const float* w) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(w[8 * q], w[8 * q + 1]);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(w[8 * q + 2], w[8 * q + 3]);
+        __nv_bfloat162 p2 = __floats2bfloat162_rn(w[8 * q + 4], w[8 * q + 5]);
+        __nv_bfloat162 p3 = __floats2bfloat162_rn(w[8 * q + 6], w[8 * q + 7]);
+        d[q] = make_uint4(*reinterpret_cast<uint32_t*>(&p0), *reinterpret_cast<uint32_t*>(&p1),
+                          *reinterpret_cast<uint32_t*>(&p2), *reinterpret_cast<uint32_t*>(&p3));
+    }
+}
 // (hi, lo) activation planes of a run of N consecutive rows (N = 16 or 32)
 template <typename T, int NR> CVY_DEV void store_act_rows(T* dst, size_t plane, const float* w);
 template <> CVY_DEV void store_act_rows<float, 32>(float* dst, size_t, const float* w) { store_row32<float>(dst, w); }
@@ -158,19 +179,21 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
 #pragma unroll
             for (int i = 0; i < W; ++i) esm[et * kEsmLd + i] = out[i];
             epi_sync();
-            // transposed stores: thread -> (column b, 32 consecutive rows), 16-byte vectors
+            // transposed stores: thread -> (column b, RP = W consecutive rows), 16-byte vectors;
+            // 128 / RP threads per column, so every epilogue thread works at W = 16 too
             {
-                const int col = et >> 2, part = et & 3;
-                const int r0 = n0 + part * 32;
+                constexpr int RP = W, NPART = 128 / W;
+                const int col = et / NPART, part = et % NPART;
+                const int r0 = n0 + part * RP;
                 if (col < ncols && r0 < E.N) {
                     const int b = cb + col;
-                    float w[32];
+                    float w[RP];
 #pragma unroll
-                    for (int r = 0; r < 32; ++r) w[r] = esm[(part * 32 + r) * kEsmLd + col];
+                    for (int r = 0; r < RP; ++r) w[r] = esm[(part * RP + r) * kEsmLd + col];
                     if (r0 < P.H * hd) {
                         float4* dq = reinterpret_cast<float4*>(P.q + (size_t)b * (P.H * hd) + r0);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) dq[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+                        for (int q = 0; q < RP / 4; ++q) dq[q] = make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
                     } else if (M.kvoff[b] >= 0) {
                         const int c = r0 >= qk_rows ? 1 : 0;
                         const int rel = r0 - P.H * hd - c * P.Hkv * hd;
@@ -178,7 +201,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                         T* kv = reinterpret_cast<T*>(P.kv_pool) +
                                 (size_t)E.layer * P.n_pages * (size_t)(2 * P.Hkv * kPageTokens * hd) + M.kvoff[b] +
                                 (size_t)(c * P.Hkv + g) * (kPageTokens * hd) + e;
-                        store_row32<T>(kv, w);
+                        store_rows<T, RP>(kv, w);
                     }
                 }
             }
@@ -188,18 +211,20 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
         case EPI_RESID: {
             // v: this thread's row (n0 + et) for 32 columns -> esm; then thread -> (column b,
             // 32 consecutive rows): x += v, act = x * w_norm (hi, lo), sum of squares
-            const int col = et >> 2, part = et & 3;
-            const int r0 = n0 + part * 32;
+            // transposed: thread -> (column b, RP = W consecutive rows), 128 / RP threads per column
+            constexpr int RP = W, NPART = 128 / W;
+            const int col = et / NPART, part = et % NPART;
+            const int r0 = n0 + part * RP;
             const bool ok = col < ncols && r0 < E.N;
             const int b = cb + col;
             // the residual and norm-weight loads do not depend on the exchange: issue them first
             // so their latency hides behind the exchange stores and barrier
-            float xv[32], wn[32];
+            float xv[RP], wn[RP];
             if (ok) {
                 const float4* xs = reinterpret_cast<const float4*>(P.x + (size_t)b * P.d + r0);
                 const float4* ws = reinterpret_cast<const float4*>(E.norm_w + r0);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
+                for (int q = 0; q < RP / 4; ++q) {
                     const float4 a = xs[q], w4 = __ldg(ws + q);
                     xv[4 * q] = a.x; xv[4 * q + 1] = a.y; xv[4 * q + 2] = a.z; xv[4 * q + 3] = a.w;
                     wn[4 * q] = w4.x; wn[4 * q + 1] = w4.y; wn[4 * q + 2] = w4.z; wn[4 * q + 3] = w4.w;
@@ -212,20 +237,21 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                 float ss = 0.f;
                 if (ok) {
 #pragma unroll
-                    for (int r = 0; r < 32; ++r) {
-                        xv[r] += esm[(part * 32 + r) * kEsmLd + col];
+                    for (int r = 0; r < RP; ++r) {
+                        xv[r] += esm[(part * RP + r) * kEsmLd + col];
                         ss += xv[r] * xv[r];
                     }
                     float4* xd = reinterpret_cast<float4*>(P.x + (size_t)b * P.d + r0);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) xd[q] = make_float4(xv[4 * q], xv[4 * q + 1], xv[4 * q + 2], xv[4 * q + 3]);
+                    for (int q = 0; q < RP / 4; ++q) xd[q] = make_float4(xv[4 * q], xv[4 * q + 1], xv[4 * q + 2], xv[4 * q + 3]);
 #pragma unroll
-                    for (int r = 0; r < 32; ++r) wn[r] *= xv[r];
-                    store_act_row32<T>(reinterpret_cast<T*>(P.act) + (size_t)b * P.act_ld + r0, (size_t)P.act_plane, wn);
+                    for (int r = 0; r < RP; ++r) wn[r] *= xv[r];
+                    store_act_rows<T, RP>(reinterpret_cast<T*>(P.act) + (size_t)b * P.act_ld + r0, (size_t)P.act_plane, wn);
                 }
-                // the 4 threads of a column are lanes 4c..4c+3 of one warp
-                ss += __shfl_xor_sync(0xffffffffu, ss, 1);
-                ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+                // the NPART threads of a column are consecutive lanes of one warp; the partial
+                // sums over the 128-row block combine in a fixed order
+#pragma unroll
+                for (int o = 1; o < NPART; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
                 if (ok && part == 0) P.ssq[(size_t)(n0 / 128) * P.Bmax + b] = ss;
             }
             epi_sync();
