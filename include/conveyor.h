@@ -173,8 +173,9 @@ cvy_status cvy_weight_sizes_for(const cvy_model_config* m, uint32_t n_pages, cvy
 cvy_status cvy_init_synthetic_weights(const cvy_model_config* m, const cvy_weights* w,
                                       uint64_t seed, int32_t device);
 
-/* Repack wqkv, wo, wgu and wd IN PLACE from the row-major layouts above into tile-major
- * order, for an engine created with CVY_ENGINE_TILED_WEIGHTS.  Each [L*R][K] matrix (R rows
+/* Repack wqkv, wo, wgu and wd -- and lm_head when vocab % 128 == 0 -- IN PLACE from the
+ * row-major layouts above into tile-major order, for an engine created with
+ * CVY_ENGINE_TILED_WEIGHTS (which reads lm_head tile-major under the same vocab rule).  Each [L*R][K] matrix (R rows
  * per layer, K columns) becomes [L*R/128][K/64][128][64]: element (r, k) moves to
  *   ((r / 128) * (K / 64) + k / 64) * 8192 + (r % 128) * 64 + k % 64,
  * so every 128-row x 64-column weight tile a projection GEMM stage loads is 16 contiguous KB

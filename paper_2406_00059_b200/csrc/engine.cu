@@ -483,6 +483,9 @@ bool tiled_shape_ok(const cvy_model_config* m, std::string* why) {
     return true;
 }
 
+// The LM head joins the tile-major packing when its rows split into 128-row tiles.
+bool lm_head_tiled(const cvy_model_config* m) { return m->vocab % 128 == 0 && m->d_model % 64 == 0; }
+
 // dst[((r / 128) * (K / 64) + k / 64) * 8192 + (r % 128) * 64 + k % 64] = src[r * K + k] for one
 // [R][K] bf16 block (R % 128 == 0); 16 bytes per thread step.
 __global__ void pack_tiled_kernel(uint4* __restrict__ dst, const uint4* __restrict__ src, int64_t R, int64_t K) {
@@ -503,18 +506,22 @@ cvy_status cvy_pack_weights_tiled(const cvy_model_config* m, const cvy_weights* 
     CUDA_TRY(cudaSetDevice(device));
     const int64_t L = m->n_layers, d = m->d_model, H = m->n_heads, Hkv = m->n_kv_heads, hd = m->head_dim,
                   dff = m->d_ff;
-    const int64_t R[4] = {(H + 2 * Hkv) * hd, d, 2 * dff, d}, K[4] = {d, H * hd, d, dff};
+    // the LM head [V][d] is packed too when V % 128 == 0 (lm_head_tiled(); one "layer")
+    const int nq = lm_head_tiled(m) ? 5 : 4;
+    const int64_t R[5] = {(H + 2 * Hkv) * hd, d, 2 * dff, d, (int64_t)m->vocab}, K[5] = {d, H * hd, d, dff, d};
+    const int64_t Lq[5] = {L, L, L, L, 1};
     // the pack rewrites the caller's buffers (documented in conveyor.h); cvy_weights holds them const
-    void* base[4] = {const_cast<void*>(w->wqkv), const_cast<void*>(w->wo), const_cast<void*>(w->wgu),
-                     const_cast<void*>(w->wd)};
+    void* base[5] = {const_cast<void*>(w->wqkv), const_cast<void*>(w->wo), const_cast<void*>(w->wgu),
+                     const_cast<void*>(w->wd), const_cast<void*>(w->lm_head)};
+    if (nq == 5 && !w->lm_head) return fail(CVY_E_INVAL, "null weight pointer");
     size_t tmp_bytes = 0;
-    for (int q = 0; q < 4; ++q) tmp_bytes = std::max(tmp_bytes, (size_t)(R[q] * K[q] * 2));
+    for (int q = 0; q < nq; ++q) tmp_bytes = std::max(tmp_bytes, (size_t)(R[q] * K[q] * 2));
     void* tmp = nullptr;
     CUDA_TRY(cudaMalloc(&tmp, tmp_bytes));
     cudaError_t err = cudaSuccess;
     // one layer at a time through a scratch copy: a layer's tiles occupy exactly its own bytes
-    for (int q = 0; q < 4 && err == cudaSuccess; ++q)
-        for (int64_t l = 0; l < L && err == cudaSuccess; ++l) {
+    for (int q = 0; q < nq && err == cudaSuccess; ++q)
+        for (int64_t l = 0; l < Lq[q] && err == cudaSuccess; ++l) {
             uint8_t* blk = (uint8_t*)base[q] + (size_t)l * R[q] * K[q] * 2;
             err = cudaMemcpy(tmp, blk, (size_t)R[q] * K[q] * 2, cudaMemcpyDeviceToDevice);
             if (err == cudaSuccess) {
@@ -1202,7 +1209,8 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         if (const char* dg = getenv("CVY_GEMM_DBG_GU"))
             if (epi.kind == EPI_SWIGLU) g.dbg = atoi(dg);
         g.x_plane_rows = (int32_t)xcap;
-        g.wtiled = e->w_tiled && (Wbase == e->w.wqkv || Wbase == e->w.wo || Wbase == e->w.wgu || Wbase == e->w.wd);
+        g.wtiled = e->w_tiled && (Wbase == e->w.wqkv || Wbase == e->w.wo || Wbase == e->w.wgu || Wbase == e->w.wd ||
+                                  (Wbase == e->w.lm_head && lm_head_tiled(&e->m)));
         if (g.wtiled && g.bk != 64) {
             *why = "tile-major weights need 64-element k-blocks (batch tiles of <= 128 columns)";
             return false;
