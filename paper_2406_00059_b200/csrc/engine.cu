@@ -147,11 +147,16 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk && (g.nbt == 1 || !allow_kernel_split)) {
         int S = 1;
         // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
-        while (allow_kernel_split && S < 4 && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
+        while (allow_kernel_split && S < kMaxSplit && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
         if (S == 3 && !getenv("CVY_GEMM_ALLOW_S3")) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
         if (g.tiles <= num_sms) g.split = S;
         // the DSMEM staging of the partial must fit in the pipeline smem
         if (g.split > 1 && (size_t)g.nsub * Bq * 512 > (size_t)stages * stage) g.split = 0;
+        // the kernel's reduce-scatter sums at most kMaxSplit ranks (gemm_sm100.cuh, t4[kMaxSplit])
+        if (g.split > kMaxSplit) {
+            *why = "cluster split-K wider than the kernel's reduce-scatter";
+            return false;
+        }
     }
     // L2 look-ahead: ~256 KB of weights per CTA beyond the smem ring (bounded by L2 capacity)
     g.l2_prefetch = 0;  // measured: no gain (mainloops already stream at 5.6-6.8 TB/s once unblocked)

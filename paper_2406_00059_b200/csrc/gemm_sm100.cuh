@@ -31,6 +31,8 @@ struct GemmNext {
     int32_t blocks;  // k-blocks prefetched per next-kernel CTA (0: off)
 };
 
+constexpr int kMaxSplit = 4;  // cluster split-K ranks the DSMEM reduce-scatter sums (t4[kMaxSplit])
+
 struct GemmTC {
     int32_t N;          // weight rows of this GEMM (one layer)
     int32_t K;
@@ -479,11 +481,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             // all S*4 remote loads of a unit in flight at once (DSMEM round trips are ~200
             // cycles), then the sum in rank order; the next unit's loads are issued before this
             // unit's epilogue so their latency overlaps it
-            float4 t4[4][4];
+            float4 t4[kMaxSplit][4];
             auto issue = [&](int uu) {
                 const uint32_t off = (uint32_t)(((size_t)uu * 512 + et) * 16);
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
+                for (int r = 0; r < kMaxSplit; ++r)
                     if (r < G.split) {
                         const uint32_t a = mapa_shared(base + off, (uint32_t)r);
 #pragma unroll
@@ -496,7 +498,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = 0.f;
 #pragma unroll
-                for (int r = 0; r < 4; ++r)
+                for (int r = 0; r < kMaxSplit; ++r)
                     if (r < G.split) {
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {

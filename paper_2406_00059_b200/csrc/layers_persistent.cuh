@@ -491,10 +491,12 @@ CVY_DEV void pk_att_load_q(const StepParams& P, PkAttRun& R, int b, int g, int l
     for (int ks = 0; ks < KSTEPS; ++ks) {
         float v[4];
         const int d0 = ks * 16 + tig * 2;
-        v[0] = qrow[d0];
-        v[1] = qrow[d0 + 1];
-        v[2] = qrow[d0 + 8];
-        v[3] = qrow[d0 + 9];
+        const float2 qa = *reinterpret_cast<const float2*>(qrow + d0);      // 8-byte aligned (d0 even)
+        const float2 qc = *reinterpret_cast<const float2*>(qrow + d0 + 8);
+        v[0] = qa.x;
+        v[1] = qa.y;
+        v[2] = qc.x;
+        v[3] = qc.y;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const float x = valid ? v[u] * qs : 0.f;
