@@ -184,7 +184,8 @@ cvy_status cvy_init_synthetic_weights(const cvy_model_config* m, const cvy_weigh
  * (the projections of the decode step) compute the same products.
  * bf16 only; every R % 128 == 0 and K % 64 == 0, else CVY_E_INVAL and nothing is touched.
  * Uses a device scratch buffer of one layer's largest matrix.  Synchronous.  Not idempotent:
- * call once per weight set. */
+ * call once per weight set.  On CVY_E_CUDA the matrices may be partly packed: regenerate them
+ * (cvy_init_synthetic_weights) before use. */
 cvy_status cvy_pack_weights_tiled(const cvy_model_config* m, const cvy_weights* w, int32_t device);
 
 /* Create / destroy.  vocab_bytes [V][16] and vocab_lens [V] give the byte string of every
