@@ -400,6 +400,7 @@ bool model_ok(const cvy_model_config* m, std::string* why) {
     if (m->head_dim != 32 && m->head_dim != 64 && m->head_dim != 128) { *why = "head_dim must be 32, 64 or 128"; return false; }
     if (m->d_model % 128 || (m->n_heads * m->head_dim) % 128 || m->d_ff % 64) { *why = "d_model, H*hd must be multiples of 128, d_ff of 64"; return false; }
     if (m->n_heads % m->n_kv_heads || m->n_heads / m->n_kv_heads > kAttnMaxG) { *why = "n_heads / n_kv_heads must be an integer <= 8"; return false; }
+    if (m->d_model > 8192) { *why = "d_model must be <= 8192 (embedding kernel's per-block sums)"; return false; }
     if (m->dtype != CVY_DTYPE_BF16 && m->dtype != CVY_DTYPE_FP32) { *why = "bad dtype"; return false; }
     if (m->dtype == CVY_DTYPE_FP32 && std::max(m->d_model, std::max(m->d_ff, m->n_heads * m->head_dim)) > 1024) {
         *why = "fp32 parity path supports K <= 1024 only";

@@ -135,20 +135,33 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Step
     const T* E = reinterpret_cast<const T*>(P.embed) + (size_t)tok * P.d;
     T* act = reinterpret_cast<T*>(P.act) + (size_t)b * P.act_ld;
     const float* nw = P.L > 0 ? P.attn_norm : P.final_norm;  // L == 0: straight to the LM head
-    __shared__ float red[4];
-    for (int blk = 0; blk < P.d / 128; ++blk) {
-        const int i = blk * 128 + threadIdx.x;
-        float v = DT<T>::to_f(E[i]);
-        P.x[(size_t)b * P.d + i] = v;
-        DT<T>::store_act(act + i, (size_t)P.act_plane, v * nw[i]);
-        float sq = v * v;
+    // thread t owns element blk * 128 + t of every 128-block; the embedding row is read with all
+    // loads in flight (it comes from HBM: a dependent load per block made this a latency chain),
+    // and the per-block sums of squares keep their reduction tree (warp xor, then 4 warps)
+    constexpr int kMaxBlk = 64;  // d <= 8192
+    __shared__ float red[kMaxBlk][4];
+    const int nblk = P.d / 128;
+    for (int blk0 = 0; blk0 < nblk; blk0 += 16) {
+        float v[16];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-        __syncthreads();
-        if (threadIdx.x == 0) P.ssq[(size_t)blk * P.Bmax + b] = (red[0] + red[1]) + (red[2] + red[3]);
-        __syncthreads();
+        for (int j = 0; j < 16; ++j)
+            v[j] = blk0 + j < nblk ? DT<T>::to_f(E[(blk0 + j) * 128 + threadIdx.x]) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int blk = blk0 + j;
+            if (blk >= nblk) break;
+            const int i = blk * 128 + threadIdx.x;
+            P.x[(size_t)b * P.d + i] = v[j];
+            DT<T>::store_act(act + i, (size_t)P.act_plane, v[j] * nw[i]);
+            float sq = v[j] * v[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            if ((threadIdx.x & 31) == 0 && blk < kMaxBlk) red[blk][threadIdx.x >> 5] = sq;
+        }
     }
+    __syncthreads();
+    for (int blk = threadIdx.x; blk < nblk && blk < kMaxBlk; blk += blockDim.x)
+        P.ssq[(size_t)blk * P.Bmax + b] = (red[blk][0] + red[blk][1]) + (red[blk][2] + red[blk][3]);
 }
 
 // ------------------------------------------------------------------ paged GQA decode attention
