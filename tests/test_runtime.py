@@ -214,3 +214,17 @@ def test_bench_peak_parsing_units_and_preference():
     assert src == "measured" and p["hbm_gbs"] == 6540.0 and abs(p["bf16_tflops"] - 1648.4) < 1e-9
     p, src = bench.parse_peaks({"unrelated": 1, "flag": True})
     assert src == "fallback" and p == bench.PEAKS_FALLBACK
+
+
+def test_bench_algorithmic_bytes_match_survey_counts():
+    """The roofline numerator (bench.step_alg_bytes) against SURVEY.md §8(d)'s independent count
+    for the 7B shape: 7,110,393,856 streamed parameters (bf16: 14.22 GB; the embedding is a
+    gather) + sum over slots of (ctx + 1) x 128 KiB of KV read + 128 KiB of KV written per slot."""
+    import bench
+    from inputs.configs import MISTRAL_7B
+    assert MISTRAL_7B.n_params_streamed == 7_110_393_856
+    kv_tok = 2 * MISTRAL_7B.L * MISTRAL_7B.Hkv * MISTRAL_7B.hd * 2
+    assert kv_tok == 128 * 1024
+    ctx = [128 + 7 * i for i in range(64)]
+    want = 2 * 7_110_393_856 + sum(c + 1 for c in ctx) * kv_tok + len(ctx) * kv_tok
+    assert bench.step_alg_bytes(MISTRAL_7B, ctx) == want
