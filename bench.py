@@ -230,7 +230,8 @@ def time_oracle(shape, reqs, budget_s: float, seed: int, n_req: int | None = Non
         toks += n_req
         steps += 1
         i += n_req
-        if t_total >= budget_s or (max_steps and steps >= max_steps):
+        # budget_s <= 0: no time budget (exactly max_steps steps, as the reference arm needs)
+        if (budget_s > 0 and t_total >= budget_s) or (max_steps and steps >= max_steps):
             break
     return toks, t_total, oracle.num_threads(), n_req, steps
 

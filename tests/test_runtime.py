@@ -228,3 +228,15 @@ def test_bench_algorithmic_bytes_match_survey_counts():
     ctx = [128 + 7 * i for i in range(64)]
     want = 2 * 7_110_393_856 + sum(c + 1 for c in ctx) * kv_tok + len(ctx) * kv_tok
     assert bench.step_alg_bytes(MISTRAL_7B, ctx) == want
+
+
+def test_time_oracle_runs_exactly_the_requested_steps():
+    """bench.time_oracle with no time budget runs exactly max_steps steps (the reference arm
+    reports steps and ms_per_step from it), and with a budget stops once the budget is spent."""
+    import bench
+    from inputs.configs import TINY
+    reqs = [{"prefix": 5 + i, "seed": 100 + i} for i in range(4)]
+    toks, t, _, n, steps = bench.time_oracle(TINY, reqs, 0.0, 7, n_req=2, max_steps=3)
+    assert (steps, n, toks) == (3, 2, 6) and t > 0
+    toks, t, _, n, steps = bench.time_oracle(TINY, reqs, 1e-9, 7, n_req=1, max_steps=50)
+    assert steps == 1 and toks == 1
