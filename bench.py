@@ -208,7 +208,7 @@ def time_oracle(shape, reqs, budget_s: float, seed: int, n_req: int | None = Non
     requests (their synthetic prefixes, first input token).  The sample size is calibrated
     so the total lands near budget_s.  Returns (tokens, seconds, threads, n_req, steps)."""
     import oracle
-    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False, cache=False)
+    w = oracle.Weights(shape, seed, bf16=True, cache=False)
 
     def one_step(sample):
         ors = []

@@ -44,7 +44,7 @@ def lib():
         L = ctypes.CDLL(_LIB_PATH)
         vp, i32, u64, dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint64, ctypes.c_double
         L.orc_weights_create.restype = vp
-        L.orc_weights_create.argtypes = [ctypes.POINTER(_Model), u64, i32, i32, i32]
+        L.orc_weights_create.argtypes = [ctypes.POINTER(_Model), u64, i32, i32]
         L.orc_weights_destroy.argtypes = [vp]
         L.orc_req_create.restype = vp
         L.orc_req_create.argtypes = [vp, i32]
@@ -101,18 +101,17 @@ def tid_lm_head(L: int) -> int:
 
 
 class Weights:
-    """Random-init weights (counter hash), fp32 or bf16 values; act_bf16 selects the bf16
-    storage-point contract (R4) for activations."""
+    """Random-init weights (counter hash), fp32 or bf16 values.  Activations are exact (fp64);
+    a bf16 model rounds only its KV cache to bf16 on append."""
 
-    def __init__(self, shape, seed: int, bf16: bool, act_bf16: bool, cache: bool | None = None):
+    def __init__(self, shape, seed: int, bf16: bool, cache: bool | None = None):
         self.shape = shape
         self.bf16 = bf16
-        self.act_bf16 = act_bf16
         m = _Model(shape.L, shape.d, shape.H, shape.Hkv, shape.hd, shape.dff, shape.V,
                    shape.eps, shape.rope_base)
         if cache is None:
             cache = shape.n_params_streamed < 200_000_000
-        self._h = lib().orc_weights_create(ctypes.byref(m), seed, int(bf16), int(act_bf16), int(cache))
+        self._h = lib().orc_weights_create(ctypes.byref(m), seed, int(bf16), int(cache))
 
     def tensor(self, tid: int, rows: int, cols: int) -> np.ndarray:
         out = np.empty((rows, cols), dtype=np.float64)

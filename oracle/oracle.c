@@ -82,7 +82,6 @@ typedef struct {
     orc_model m;
     uint64_t seed;
     int wbf16;     /* 1: weights are bf16 values, 0: fp32 values                  */
-    int act_bf16;  /* 1: bf16 storage points (R4), 0: exact             */
     int cache_weights;
     double** wcache; /* [1+8L+1] dense weight arrays when cached, else NULL       */
 } orc_weights;
@@ -112,13 +111,11 @@ static void tensor_shape(const orc_model* m, uint64_t tid, int* rows, int* cols)
 
 static double weight_a(void) { return 0.02 * sqrt(3.0); }
 
-orc_weights* orc_weights_create(const orc_model* m, uint64_t seed, int wbf16, int act_bf16,
-                                int cache_weights) {
+orc_weights* orc_weights_create(const orc_model* m, uint64_t seed, int wbf16, int cache_weights) {
     orc_weights* w = (orc_weights*)calloc(1, sizeof(orc_weights));
     w->m = *m;
     w->seed = seed;
     w->wbf16 = wbf16;
-    w->act_bf16 = act_bf16;
     w->cache_weights = cache_weights;
     if (cache_weights) {
         int n = 2 + 8 * m->L;
@@ -234,17 +231,13 @@ static void rope(double* a, int hd, int pos, double base) {
     }
 }
 
-/* RMSNorm input for the next GEMM.  Exact mode: u = x * rsqrt(mean(x^2)+eps) * w, scale 1.
- * bf16 mode (R4): u = bf16(x * w) and the scalar rsqrt(mean(x^2)+eps) is applied
- * to the GEMM output (identical in exact arithmetic). w (norm weight) is 1.0 (R3). */
+/* RMSNorm input for the next GEMM: u = x * rsqrt(mean(x^2)+eps) * w, w (norm weight) = 1.0
+ * (R3).  Returns the scale applied afterwards to the GEMM output (1: none; the activations
+ * are exact). */
 static double rms_input(const orc_weights* w, const double* x, int d, double* u) {
     double ms = 0.0;
     for (int i = 0; i < d; ++i) ms += x[i] * x[i];
     double s = 1.0 / sqrt(ms / (double)d + w->m.eps);
-    if (w->act_bf16) {
-        for (int i = 0; i < d; ++i) u[i] = bf16_round(x[i] * 1.0);
-        return s;
-    }
     for (int i = 0; i < d; ++i) u[i] = x[i] * s * 1.0;
     return 1.0;
 }
@@ -335,8 +328,6 @@ int orc_step(orc_req* const* reqs, int n, const int32_t* tok, double* logits) {
                     double p = s[t] / den;
                     for (int e = 0; e < hd; ++e) oj[e] += p * vt[e];
                 }
-                if (w->act_bf16)
-                    for (int e = 0; e < hd; ++e) oj[e] = bf16_round(oj[e]);
             }
             free(s);
         }
@@ -352,7 +343,7 @@ int orc_step(orc_req* const* reqs, int n, const int32_t* tok, double* logits) {
         for (int i = 0; i < n; ++i)
             for (int e = 0; e < dff; ++e) {
                 double a = silu(g[i][e] * sc[i]) * (up[i][e] * sc[i]);
-                u[i][e] = w->act_bf16 ? bf16_round(a) : a;
+                u[i][e] = a;
             }
         matvec(w, tensor_id(l, W_D), d, dff, n, u, y);
         for (int i = 0; i < n; ++i)

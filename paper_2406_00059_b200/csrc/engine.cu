@@ -97,7 +97,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     // (hi, lo) N = 256 pipeline (measured: the unmerged Bp = 256 layout, 4x more activation
     // than weight bytes per stage and 2 stages, ran gate/up at 1.7 TB/s)
     int bq_max = 128;
-    if (const char* v = getenv("CVY_GEMM_BQ")) bq_max = std::max(32, std::min(128, atoi(v)));  // A/B knob
+    if (const char* v = getenv("CVY_GEMM_BQ")) bq_max = std::max(32, std::min(256, atoi(v)));  // A/B knob
     g.nbt = Bp > bq_max ? Bp / bq_max : 1;
     g.bq = Bp / g.nbt;
     if (getenv("CVY_GEMM_NO_BATCH_TILES")) {
@@ -107,6 +107,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     const int Bq = g.bq;
     g.merge = Bq <= 128;
     g.bk = Bq >= 512 ? 32 : 64;
+    if (const char* v = getenv("CVY_GEMM_BK")) g.bk = (atoi(v) == 32 && !g.merge) ? 32 : 64;  // A/B knob
     // wide GEMMs (gate/up, LM head): 256-row tiles, one per CTA, no reduction; narrow ones
     // (QKV, O, down): 128-row tiles with K split over a 2..4-CTA cluster (DSMEM reduction)
     // 256-row tiles halve the activation bytes per weight byte; worth it down to the QKV
@@ -124,7 +125,9 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         g.nbh = Bq / g.mma_n;
         g.cols_per_sub = Bq;
     }
-    if (g.bk == 32 || !g.merge) g.nsub = 1;
+    // unmerged (Bq > 128): hi and lo accumulate into the same TMEM columns; two 128-row
+    // sub-tiles fill all 512 columns at Bq = 256 (one accumulator stage)
+    if (!g.merge && !(nsub_override == 2 || getenv("CVY_GEMM_NSUB"))) g.nsub = 1;
     if (g.nsub * g.cols_per_sub > 512) {
         *why = "accumulator exceeds TMEM";
         return false;
@@ -164,9 +167,14 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     if (g.split > 0) {
         *grid = g.tiles * g.split;
     } else {
-        // stream-K: the nbt batch tiles share the SMs (each streams 1/grid of the weights)
+        // stream-K: the nbt batch tiles share the SMs (each streams 1/grid of the weights).
+        // When every (tile, batch tile) fits one wave, whole tiles instead: no shared tile, so no
+        // L2 partial fix-up in the kernel's tail (measured at B = 512)
         const long long T = (long long)g.tiles * g.kblocks;
         *grid = (int)std::min<long long>(std::max(1, num_sms / g.nbt), T);
+        int whole = 1;
+        if (const char* v = getenv("CVY_GEMM_WHOLE")) whole = atoi(v);
+        if (whole && g.nbt > 1 && g.tiles * g.nbt <= num_sms) *grid = g.tiles;
     }
     return true;
 }
@@ -194,6 +202,15 @@ struct SlotHost {
     bool final_pending = false;  // round running (a FINAL will come)
     int32_t round_pos0 = 0;      // device pos of the round's first input token
     int32_t round_inputs = 0;    // input tokens the round feeds before generating (incl. cur_tok)
+    bool cancel_pending = false; // a CANCEL patch is queued for the running round (de-duplication)
+};
+
+// A synthetic KV prefix to write before the slot's first step (queued by submit, run by
+// cvy_step on the engine stream after the page-table uploads, never during a graph capture).
+struct SynthJob {
+    int slot;
+    uint32_t len;
+    uint64_t seed;
 };
 
 // A chunked-prefill job (NEXT-1): tokens fed at positions pos0, pos0+1, ... of a slot.
@@ -231,6 +248,11 @@ struct Bucket {
     std::vector<cudaEvent_t> kev;
     std::vector<std::pair<int, int>> kinfo;  // (kind, layer) per launch
     uint32_t launches = 0;
+    // batch-split overlap: two half-batch chains on two streams, so one half's
+    // HBM-bound attention runs beside the other half's tensor-bound projections
+    bool ov = false;
+    StepParams PH[2];
+    std::vector<GemmPlan> hplans[2];  // per chain: 4 GEMMs per layer (QKV, O, gate/up, down)
     // persistent layer kernel (layers_persistent.cuh): all L layers in one launch
     bool pk = false;
     CUtensorMap pk_w[4], pk_x[3];
@@ -249,6 +271,17 @@ struct cvy_engine {
     int dev = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t stream_b = nullptr;   // second chain of the batch-split overlap
+    cudaStream_t cur = nullptr;        // stream launch_k enqueues on (stream or stream_b)
+    int cur_prio = 0;                  // launch priority attribute (0: none)
+    cudaEvent_t ov_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fork / join / attention order
+    int prio_hi = 0, prio_lo = 0;      // device stream-priority range (greatest, least)
+    bool ov_ok = false;                // batch-split overlap enabled for buckets >= 256
+    int ov_gemm_sms = 0;               // CTA budget of one overlapped GEMM (its share of the SMs)
+    int ov_prio = 1;                   // 1: GEMMs at high launch priority, 2: attention, 0: none
+    bool ov_serial_attn = true;        // the two chains' attention launches run one after the other
+    float* d_gemm_acc2 = nullptr;      // stream-K scratch of chain 1 (chain 0 uses d_gemm_acc)
+    int32_t* d_tile_cnt2 = nullptr;
     bool dead = false;
     bool bf16 = true;
     int act_ld = 0;
@@ -296,6 +329,7 @@ struct cvy_engine {
     std::mutex mu;
     std::vector<Patch> pending;
     std::vector<Upload> uploads;
+    std::vector<SynthJob> synth_pending;
     std::vector<SlotHost> slots;
     std::vector<int32_t> free_pages;
     std::vector<ToolDev> tools;
@@ -633,6 +667,18 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     const size_t acc_cols = (ec->flags & CVY_ENGINE_CHUNKED_PREFILL) ? std::max(Bmax, kPrefillRows) : (size_t)Bmax;
     ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * acc_cols);
     ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
+    // batch-split overlap: bf16, buckets of >= 256 slots; CVY_OVERLAP=0 disables
+    e->ov_ok = false;  // opt-in: measured slower at C4
+    if (const char* v = getenv("CVY_OVERLAP"))
+        e->ov_ok = e->bf16 && Bmax >= 256 && (hd == 64 || hd == 128) && (H / Hkv) <= 4 && atoi(v) != 0;
+    e->ov_gemm_sms = prop.multiProcessorCount / 2;
+    if (const char* v = getenv("CVY_OV_GEMM_SMS")) e->ov_gemm_sms = std::max(8, std::min(prop.multiProcessorCount, atoi(v)));
+    if (const char* v = getenv("CVY_OV_PRIO")) e->ov_prio = atoi(v);
+    if (const char* v = getenv("CVY_OV_SERIAL_ATTN")) e->ov_serial_attn = atoi(v) != 0;
+    if (e->ov_ok) {
+        ALLOC(e->d_gemm_acc2, sizeof(float) * max_rows * (size_t)Bmax);
+        ALLOC(e->d_tile_cnt2, sizeof(int32_t) * 8192);
+    }
     e->pk_ok = e->bf16 && hd == 128 && (H / Hkv) <= 4 && H % Hkv == 0 && d % 128 == 0 && ((H + 2 * Hkv) * hd) % 128 == 0 &&
                (2 * dff) % 128 == 0 && (H * hd) % 64 == 0 && dff % 64 == 0 && !(ec->flags & CVY_ENGINE_NO_PERSISTENT) &&
                !(ec->flags & CVY_ENGINE_TILED_WEIGHTS);  // the persistent kernel reads row-major weights
@@ -696,10 +742,18 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
             cvy_engine_destroy(e);
             return fail(CVY_E_INVAL, "vocab entry longer than 16 bytes");
         }
-    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&e->stream_b, cudaStreamNonBlocking) != cudaSuccess) {
         cvy_engine_destroy(e);
         return fail(CVY_E_CUDA, "stream create");
     }
+    e->cur = e->stream;
+    cudaDeviceGetStreamPriorityRange(&e->prio_lo, &e->prio_hi);
+    for (auto& ev : e->ov_ev)
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+            cvy_engine_destroy(e);
+            return fail(CVY_E_CUDA, "event create");
+        }
     e->slots.resize(Bmax);
     for (int p = (int)ec->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
     if (const char* tl = getenv("CVY_GEMM_TRACE_LAYER")) {
@@ -749,6 +803,7 @@ void cvy_engine_destroy(cvy_engine* e) {
     if (!e) return;
     cudaSetDevice(e->dev);
     if (e->stream) cudaStreamSynchronize(e->stream);
+    if (e->stream_b) cudaStreamSynchronize(e->stream_b);
     for (auto& kv : e->buckets) {
         if (kv.second.graph) cudaGraphExecDestroy(kv.second.graph);
         if (kv.second.graph_timed) cudaGraphExecDestroy(kv.second.graph_timed);
@@ -766,12 +821,16 @@ void cvy_engine_destroy(cvy_engine* e) {
                      e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches,
                      e->d_pk_done, e->d_att_cnt, e->d_att_part2, e->d_pk_part, e->d_pk_pflag,
-                     e->d_px, e->d_pact, e->d_pq, e->d_po, e->d_ph, e->d_pssq, e->d_pattn_part, e->d_prow};
+                     e->d_px, e->d_pact, e->d_pq, e->d_po, e->d_ph, e->d_pssq, e->d_pattn_part, e->d_prow,
+                     e->d_gemm_acc2, e->d_tile_cnt2};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats, e->h_pk_err};
     for (void* p : hptrs)
         if (p) cudaFreeHost(p);
+    for (auto& ev : e->ov_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->stream_b) cudaStreamDestroy(e->stream_b);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -891,24 +950,9 @@ cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t
         for (int32_t p : sh.pages) e->free_pages.push_back(p);
         return fail(CVY_E_FULL, "not enough KV pages");
     }
-    // synthetic prefix is written at submit time (synchronously on the engine stream)
-    if (r->synth_prefix_len) {
-        int32_t* d_pages = e->d_page_table + (size_t)slot * e->c.max_pages_per_slot;
-        for (auto& u : ups) cudaMemcpyAsync(u.dst, u.data.data(), u.data.size(), cudaMemcpyHostToDevice, e->stream);
-        ups.clear();
-        const int64_t n = (int64_t)e->m.n_layers * r->synth_prefix_len * 2 * e->m.n_kv_heads * e->m.head_dim;
-        const int blocks = (int)std::min<int64_t>(4096, (n + 255) / 256);
-        if (e->bf16)
-            synth_prefix_kernel<__nv_bfloat16><<<blocks, 256, 0, e->stream>>>(
-                (__nv_bfloat16*)e->w.kv_pool, d_pages, (int)e->c.n_pages, e->m.n_layers, e->m.n_kv_heads,
-                e->m.head_dim, (int)r->synth_prefix_len, r->synth_seed);
-        else
-            synth_prefix_kernel<float><<<blocks, 256, 0, e->stream>>>(
-                (float*)e->w.kv_pool, d_pages, (int)e->c.n_pages, e->m.n_layers, e->m.n_kv_heads, e->m.head_dim,
-                (int)r->synth_prefix_len, r->synth_seed);
-        cvy_status cs = check_cuda(e, cudaGetLastError(), "synth prefix");
-        if (cs != CVY_OK) return cs;
-    }
+    // the synthetic prefix is written by cvy_step (after this slot's page-table upload, before
+    // its first step), so submit never touches the stream a step graph may be capturing on
+    if (r->synth_prefix_len) e->synth_pending.push_back(SynthJob{slot, r->synth_prefix_len, r->synth_seed});
     for (auto& u : ups) e->uploads.push_back(std::move(u));
     // chunked prefill (NEXT-1): all prompt tokens but the last run as one batched pass at the
     // next step boundary; the slot then starts at the last prompt token
@@ -1029,6 +1073,7 @@ cvy_status cvy_inject_observation(cvy_engine* e, uint64_t req_id, const int32_t*
     sh.state = 0;
     sh.final_seen = false;
     sh.final_pending = true;
+    sh.cancel_pending = false;
     sh.next_pos = sh.next_pos + 1 + (int32_t)n + (int32_t)gen;
     if (prefill) {
         sh.round_pos0 = pos_end + (int32_t)n;
@@ -1046,7 +1091,8 @@ cvy_status cvy_cancel_request(cvy_engine* e, uint64_t req_id) {
     auto it = e->req_slot.find(req_id);
     if (it == e->req_slot.end()) return fail(CVY_E_NOTFOUND, "unknown request");
     SlotHost& sh = e->slots[it->second];
-    if (sh.state != 0) return CVY_OK;  // idempotent: parked or already cancelled
+    if (sh.state != 0 || sh.cancel_pending) return CVY_OK;  // idempotent: parked, cancelled or queued
+    sh.cancel_pending = true;
     Patch p;
     std::memset(&p, 0, sizeof(p));
     p.kind = PATCH_CANCEL;
@@ -1096,9 +1142,14 @@ cvy_status launch_k(cvy_engine* e, const void* func, dim3 grid, dim3 block, size
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
-    cfg.stream = e->stream;
-    cudaLaunchAttribute attr[2];
+    cfg.stream = e->cur ? e->cur : e->stream;
+    cudaLaunchAttribute attr[3];
     int na = 0;
+    if (e->cur_prio != 0) {
+        attr[na].id = cudaLaunchAttributePriority;
+        attr[na].val.priority = e->cur_prio;
+        ++na;
+    }
     if (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL) && !e->capturing_timed) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
@@ -1184,13 +1235,24 @@ StepParams base_params(cvy_engine* e, int Bp) {
     return P;
 }
 
+// Options of a half-batch plan (batch-split overlap): its padded batch, its CTA budget, its own
+// stream-K scratch, and the rows of the activation tensor map left after the row offset of X.
+struct PlanOpts {
+    int Bp = 0;
+    int sms = 0;
+    float* part = nullptr;
+    int32_t* tile_cnt = nullptr;
+    int64_t x_rows = 0;
+};
+
 // plan one GEMM: W rows N per layer, K, epilogue
 bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int layer, int L_rows_total, const void* X,
-               EpiArgs epi, GemmPlan* out, std::string* why, int xcap = 0) {
+               EpiArgs epi, GemmPlan* out, std::string* why, int xcap = 0, const PlanOpts* po = nullptr) {
     if (xcap <= 0) xcap = (int)e->slots.size();  // activation buffer rows (planes are xcap rows apart)
     GemmPlan gp;
     std::memset(&gp, 0, sizeof(gp));
-    const int Bp = bk.Bp;
+    const int Bp = (po && po->Bp) ? po->Bp : bk.Bp;
+    const int sms = (po && po->sms) ? po->sms : e->num_sms;
     gp.W = Wbase;
     gp.X = X;
     gp.w_row0 = (int64_t)layer * N;
@@ -1202,15 +1264,15 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         // gate/up: optionally stream-K over every SM instead of 112 whole 256-row tiles (A/B knob)
         const bool gu_sk = epi.kind == EPI_SWIGLU && getenv("CVY_GU_STREAMK") && atoi(getenv("CVY_GU_STREAMK")) != 0;
         const int gu_nsub = (epi.kind == EPI_SWIGLU && getenv("CVY_GU_NSUB")) ? atoi(getenv("CVY_GU_NSUB")) : 0;
-        if (!gemm_config(g, N, K, Bp, e->num_sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub))
+        if (!gemm_config(g, N, K, Bp, sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub))
             return false;
         g.w_row0 = layer * N;
         if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD && xcap == (int)e->slots.size()) {
             const int k = epi.kind == EPI_QKV ? 0 : epi.kind == EPI_SWIGLU ? 2 : (K == ::m_d(e) ? 1 : 3);
             g.trace = e->d_trace + (size_t)k * kTraceStride * e->num_sms;
         }
-        g.part = e->d_gemm_acc;
-        g.tile_cnt = e->d_tile_cnt;
+        g.part = (po && po->part) ? po->part : e->d_gemm_acc;
+        g.tile_cnt = (po && po->tile_cnt) ? po->tile_cnt : e->d_tile_cnt;
         // measurement knob (wrong results): the gate/up epilogue's debug bits (GemmTC::dbg)
         if (const char* dg = getenv("CVY_GEMM_DBG_GU"))
             if (epi.kind == EPI_SWIGLU) g.dbg = atoi(dg);
@@ -1230,7 +1292,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
             return false;
         }
         const uint32_t xrows = g.merge ? (uint32_t)g.bq : (uint32_t)g.mma_n;
-        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * xcap), (uint64_t)K, (uint64_t)e->act_ld, xrows,
+        if (!make_tmap(&gp.tmX, X, (uint64_t)((po && po->x_rows) ? po->x_rows : 2 * xcap), (uint64_t)K, (uint64_t)e->act_ld, xrows,
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (activations) failed";
             return false;
@@ -1280,6 +1342,59 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
         EpiArgs el{EPI_LMHEAD, 0, V, nullptr};
         if (!plan_gemm(e, bk, e->w.lm_head, V, d, 0, V, e->d_act, el, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
+    }
+    // batch-split overlap: chain k owns slots [k*Bp/2, (k+1)*Bp/2); its
+    // StepParams are the full ones with every per-slot pointer advanced by k*Bp/2 rows, so the
+    // unchanged kernels see a batch of Bp/2 slots.  Each chain's GEMMs get their own stream-K
+    // scratch and a budget of ov_gemm_sms CTAs; the rest of the SMs run the other chain's attention.
+    if (e->ov_ok && Bp >= 256 && !bk.P.row_slot) {
+        const int Bh = Bp / 2;
+        const size_t es = dtype_size(m.dtype);
+        bool ok = true;
+        for (int k = 0; k < 2 && ok; ++k) {
+            const size_t r0 = (size_t)k * Bh;
+            StepParams Q = bk.P;
+            Q.Bp = Bh;
+            Q.slots = bk.P.slots + r0;
+            Q.page_table = bk.P.page_table + r0 * bk.P.max_pages;
+            Q.in_buf = bk.P.in_buf + r0 * bk.P.input_cap;
+            Q.force_buf = bk.P.force_buf + r0 * bk.P.forced_cap;
+            Q.x = bk.P.x + r0 * d;
+            Q.act = (uint8_t*)bk.P.act + r0 * e->act_ld * es;
+            Q.o = (uint8_t*)bk.P.o + r0 * e->act_ld * es;
+            Q.h = (uint8_t*)bk.P.h + r0 * e->act_ld * es;
+            Q.q = bk.P.q + r0 * H * hd;
+            Q.ssq = bk.P.ssq + r0;
+            Q.am_keys = bk.P.am_keys + r0;
+            Q.dbg_logits = bk.P.dbg_logits ? bk.P.dbg_logits + r0 * V : nullptr;
+            Q.attn_splits = 1;
+            Q.attn_part = bk.P.attn_part + r0 * Hkv * (m.n_heads / Hkv) * (hd + 2);
+            bk.PH[k] = Q;
+            PlanOpts po;
+            po.Bp = Bh;
+            po.sms = e->ov_gemm_sms;
+            po.part = k == 0 ? e->d_gemm_acc : e->d_gemm_acc2;
+            po.tile_cnt = k == 0 ? e->d_tile_cnt : e->d_tile_cnt2;
+            po.x_rows = (int64_t)2 * e->slots.size() - (int64_t)r0;
+            const size_t xoff = r0 * e->act_ld * es;
+            for (int l = 0; l < L && ok; ++l) {
+                GemmPlan gp;
+                EpiArgs eq{EPI_QKV, l, Nqkv, nullptr};
+                ok = ok && plan_gemm(e, bk, e->w.wqkv, Nqkv, d, l, L * Nqkv, (uint8_t*)e->d_act + xoff, eq, &gp, &why, 0, &po);
+                bk.hplans[k].push_back(gp);
+                EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d};
+                ok = ok && plan_gemm(e, bk, e->w.wo, d, H * hd, l, L * d, (uint8_t*)e->d_o + xoff, eo, &gp, &why, 0, &po);
+                bk.hplans[k].push_back(gp);
+                EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr};
+                ok = ok && plan_gemm(e, bk, e->w.wgu, 2 * dff, d, l, L * 2 * dff, (uint8_t*)e->d_act + xoff, eg, &gp, &why, 0, &po);
+                bk.hplans[k].push_back(gp);
+                EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm};
+                ok = ok && plan_gemm(e, bk, e->w.wd, d, dff, l, L * d, (uint8_t*)e->d_h + xoff, ed, &gp, &why, 0, &po);
+                bk.hplans[k].push_back(gp);
+            }
+        }
+        if (!ok) return fail(CVY_E_INVAL, "overlap plan: " + why);
+        bk.ov = true;
     }
     // cross-kernel weight prefetch: GEMM i warms L2 with the first k-blocks of GEMM i+1 (the LM
     // head warms the next step's layer-0 QKV) while its own epilogue drains
@@ -1361,9 +1476,9 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
     return CVY_OK;
 }
 
-cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp) {
+cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp, StepParams* Pq = nullptr) {
     if (e->bf16) {
-        void* args[] = {&gp.tmW, &gp.tmX, &bk.P, &gp.g, &gp.tmN};
+        void* args[] = {&gp.tmW, &gp.tmX, Pq ? Pq : &bk.P, &gp.g, &gp.tmN};
         return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind),
                         dim3(gp.grid, gp.g.nbt), dim3(kGemmThreads), gp.smem, args, true, gp.g.split > 1 ? gp.g.split : 1);
     }
@@ -1392,27 +1507,28 @@ struct KTimer {
             bk.kev.push_back(b);
             bk.kinfo.push_back({kind, layer});
         }
-        cudaEventRecordWithFlags(bk.kev[2 * i], e->stream, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(bk.kev[2 * i], e->cur ? e->cur : e->stream, cudaEventRecordExternal);
     }
     void end() {
         if (!e->capturing_timed) return;
-        cudaEventRecordWithFlags(bk.kev[2 * i + 1], e->stream, cudaEventRecordExternal);
+        cudaEventRecordWithFlags(bk.kev[2 * i + 1], e->cur ? e->cur : e->stream, cudaEventRecordExternal);
         ++i;
     }
 };
 
 // Paged attention of one layer for every row of the bucket (+ the split-KV merge).
-cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt) {
+cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt, StepParams* Pq = nullptr) {
+    StepParams& P = Pq ? *Pq : bk.P;
     cvy_status st;
     const cvy_model_config& m = e->m;
-    const int Bp = bk.Bp;
+    const int Bp = P.Bp;
     const int G = m.n_heads / m.n_kv_heads;
     const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
     int layer = l;
-    void* aargs[] = {&bk.P, &layer};
-    if (e->attn_pk && bk.P.row_slot == nullptr && Bp <= kApMaxRows) {
+    void* aargs[] = {&P, &layer};
+    if (e->attn_pk && P.row_slot == nullptr && Bp <= kApMaxRows) {
         int nst = 3;
-        void* pargs[] = {&e->tm_kv, &bk.P, &layer, &nst};
+        void* pargs[] = {&e->tm_kv, &P, &layer, &nst};
         if ((st = launch_k(e, (const void*)attention_persistent_kernel, dim3(e->num_sms), dim3((kApConsumers + 1) * 32),
                            ap_smem_bytes(nst), pargs, true)) != CVY_OK)
             return st;
@@ -1420,7 +1536,7 @@ cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt) {
         return CVY_OK;
     }
     if (e->attn_tc) {
-        void* targs[] = {&e->tm_kv, &bk.P, &layer};
+        void* targs[] = {&e->tm_kv, &P, &layer};
         const int pps = e->attn_pps;
         const int nst = pps == 2 ? (e->attn_stages <= 2 ? 2 : e->attn_stages >= 6 ? 6 : 4) : e->attn_stages;
         const void* tf;
@@ -1441,18 +1557,18 @@ cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt) {
         const int blk = kPageTokens * m.head_dim * 2;
         const size_t tsmem = 1024 + (size_t)nst * pps * 2 * blk + kAtcWarps * 8 * 16 * 2 +
                              (size_t)kAtcWarps * (8 + 4 * m.head_dim) * 4 + 2 * nst * 8;
-        if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
+        if ((st = launch_k(e, tf, dim3(m.n_kv_heads, Bp, P.attn_splits), dim3(kAtcThreads), tsmem, targs, true)) !=
             CVY_OK)
             return st;
     } else {
         const void* af = e->bf16 ? (const void*)attention_kernel<__nv_bfloat16> : (const void*)attention_kernel<float>;
-        if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, bk.P.attn_splits), dim3(kAttnThreads), attn_smem, aargs,
+        if ((st = launch_k(e, af, dim3(m.n_kv_heads, Bp, P.attn_splits), dim3(kAttnThreads), attn_smem, aargs,
                            true)) != CVY_OK)
             return st;
     }
     if (kt) kt->end();
-    if (bk.P.attn_splits > 1) {
-        void* margs[] = {&bk.P};
+    if (P.attn_splits > 1) {
+        void* margs[] = {&P};
         const void* mf =
             e->bf16 ? (const void*)attention_merge_kernel<__nv_bfloat16> : (const void*)attention_merge_kernel<float>;
         if (kt) kt->begin(3, l);
@@ -1561,6 +1677,62 @@ cvy_status enqueue_prefill(cvy_engine* e, const std::vector<PrefillJob>& jobs) {
     return CVY_OK;
 }
 
+// Batch-split overlap: the layers of the two half-batch chains, chain k on
+// stream k.  Chain 1 starts when chain 0's first QKV is done, and (ov_serial_attn) the two
+// chains' attention launches alternate (A0, A1, A0, ...), so while one chain streams its KV
+// cache from HBM the other runs its tensor-bound projections on its CTA budget of SMs.
+// Launch priorities (ov_prio) let the projections' CTAs take SMs first as they free up.
+cvy_status enqueue_overlap_layers(cvy_engine* e, Bucket& bk, KTimer& kt, uint32_t* launches) {
+    cvy_status st;
+    const int gprio = e->ov_prio == 1 ? e->prio_hi : 0;
+    const int aprio = e->ov_prio == 2 ? e->prio_hi : 0;
+    cudaStream_t sk[2] = {e->stream, e->stream_b};
+    auto ck = [&](cudaError_t err, const char* what) { return check_cuda(e, err, what); };
+    if ((st = ck(cudaEventRecord(e->ov_ev[0], e->stream), "overlap fork")) != CVY_OK) return st;
+    if ((st = ck(cudaStreamWaitEvent(e->stream_b, e->ov_ev[0], 0), "overlap fork wait")) != CVY_OK) return st;
+    const bool pdl_saved = (e->c.flags & CVY_ENGINE_NO_PDL) != 0;
+    for (int l = 0; l < e->m.n_layers; ++l) {
+        for (int k = 0; k < 2; ++k) {
+            e->cur = sk[k];
+            GemmPlan* hp = &bk.hplans[k][(size_t)4 * l];
+            StepParams* Pk = &bk.PH[k];
+            if (l == 0 && k == 1) {
+                if ((st = ck(cudaStreamWaitEvent(e->stream_b, e->ov_ev[1], 0), "chain offset wait")) != CVY_OK) return st;
+            }
+            e->cur_prio = gprio;
+            kt.begin(1, l);
+            if ((st = launch_gemm(e, bk, hp[0], Pk)) != CVY_OK) return st;
+            kt.end();
+            if (l == 0 && k == 0) {
+                if ((st = ck(cudaEventRecord(e->ov_ev[1], e->stream), "chain offset")) != CVY_OK) return st;
+            }
+            bool waited = false;
+            if (e->ov_serial_attn && (k == 1 || l > 0)) {
+                if ((st = ck(cudaStreamWaitEvent(sk[k], e->ov_ev[2 + (1 - k)], 0), "attention order")) != CVY_OK) return st;
+                waited = true;
+            }
+            e->cur_prio = aprio;
+            // no programmatic (PDL) edge where the launch also waits on the other chain
+            if (waited) e->c.flags |= CVY_ENGINE_NO_PDL;
+            kt.begin(2, l);
+            st = launch_attention(e, bk, l, &kt, Pk);
+            if (!pdl_saved) e->c.flags &= ~(uint32_t)CVY_ENGINE_NO_PDL;
+            if (st != CVY_OK) return st;
+            if ((st = ck(cudaEventRecord(e->ov_ev[2 + k], sk[k]), "attention done")) != CVY_OK) return st;
+            e->cur_prio = gprio;
+            for (int q = 1; q < 4; ++q) {
+                kt.begin(3 + q, l);
+                if ((st = launch_gemm(e, bk, hp[q], Pk)) != CVY_OK) return st;
+                kt.end();
+            }
+            *launches += 5;
+        }
+    }
+    if ((st = ck(cudaEventRecord(e->ov_ev[0], e->stream_b), "overlap join")) != CVY_OK) return st;
+    if ((st = ck(cudaStreamWaitEvent(e->stream, e->ov_ev[0], 0), "overlap join wait")) != CVY_OK) return st;
+    return CVY_OK;
+}
+
 cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
     cvy_status st;
     uint32_t launches = 0;
@@ -1607,6 +1779,23 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
         bk.launches = launches;
         return CVY_OK;
     }
+    if (bk.ov) {
+        st = enqueue_overlap_layers(e, bk, kt, &launches);
+        e->cur = e->stream;
+        e->cur_prio = 0;
+        if (st != CVY_OK) return st;
+        // the LM head follows the join (a full edge from chain 1): no programmatic edge
+        const uint32_t saved = e->c.flags;
+        e->c.flags |= CVY_ENGINE_NO_PDL;
+        kt.begin(7, 0);
+        st = launch_gemm(e, bk, bk.plans.back());
+        e->c.flags = saved;
+        if (st != CVY_OK) return st;
+        kt.end();
+        launches++;
+        bk.launches = launches;
+        return CVY_OK;
+    }
     size_t pi = 0;
     for (int l = 0; l < m.n_layers; ++l) {
         kt.begin(1, l);
@@ -1630,6 +1819,17 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
     return CVY_OK;
 }
 
+// Wait for the oldest step in flight and return its events to the pool.
+cvy_status retire_oldest(cvy_engine* e) {
+    auto ev = e->inflight.front();
+    cvy_status st = check_cuda(e, cudaEventSynchronize(ev.second), "event sync");
+    if (st != CVY_OK) return st;
+    cudaEventElapsedTime(&e->last_step_ms, ev.first, ev.second);
+    e->inflight.pop_front();
+    e->event_pool.push_back(ev);
+    return CVY_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1638,17 +1838,53 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
     if (!e) return fail(CVY_E_INVAL, "null engine");
     if (e->dead) return fail(CVY_E_CUDA, "engine is dead");
     cudaSetDevice(e->dev);
+    // at most 2 steps in flight
+    while (e->inflight.size() >= 2) {
+        cvy_status st = retire_oldest(e);
+        if (st != CVY_OK) return st;
+    }
+    // Ring back-pressure, checked BEFORE the queued host updates are taken (a non-fatal
+    // E_FULL leaves them queued): the steps in flight plus this one may each publish up to
+    // kMaxRecPerSlot records per slot in use.  While steps are in flight, retire the oldest
+    // (its records are then in the ring and the bound shrinks); only with none in flight
+    // wait for the poller.
     std::vector<Patch> patches;
     std::vector<Upload> uploads;
     std::vector<PrefillJob> prefills;
+    std::vector<SynthJob> synths;
     int max_used = -1;
     {
-        std::lock_guard<std::mutex> lk(e->mu);
-        patches.swap(e->pending);
-        uploads.swap(e->uploads);
-        prefills.swap(e->prefill_pending);
-        for (int b = 0; b < (int)e->slots.size(); ++b)
-            if (e->slots[b].used) max_used = b;
+        auto t0 = std::chrono::steady_clock::now();
+        while (true) {
+            int mu_now = -1;
+            {
+                std::lock_guard<std::mutex> lk(e->mu);
+                for (int b = 0; b < (int)e->slots.size(); ++b)
+                    if (e->slots[b].used) mu_now = b;
+            }
+            const uint64_t worst = (uint64_t)(e->inflight.size() + 1) * (uint64_t)(mu_now + 1) * kMaxRecPerSlot;
+            const uint64_t tail = __atomic_load_n(e->h_ring_tail, __ATOMIC_ACQUIRE);
+            const uint64_t head = __atomic_load_n(&e->ring_head, __ATOMIC_ACQUIRE);
+            if (tail - head + worst <= e->c.ring_records) {
+                std::lock_guard<std::mutex> lk(e->mu);
+                for (int b = 0; b < (int)e->slots.size(); ++b)
+                    if (e->slots[b].used) max_used = b;
+                if (max_used > mu_now) continue;  // a submit raced in: re-check with its slot
+                patches.swap(e->pending);
+                uploads.swap(e->uploads);
+                prefills.swap(e->prefill_pending);
+                synths.swap(e->synth_pending);
+                break;
+            }
+            if (!e->inflight.empty()) {
+                cvy_status st = retire_oldest(e);
+                if (st != CVY_OK) return st;
+                continue;
+            }
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
+                return fail(CVY_E_FULL, "segment ring full: poll_segments is not draining it");
+            std::this_thread::yield();
+        }
     }
     // released slots still need their patch applied even if nothing is in use
     // batch bucket: multiple of 32 (epilogue chunk), 256 and 512 above 128/256
@@ -1656,41 +1892,36 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
     if (Bp > 256) Bp = 512;
     else if (Bp > 128) Bp = 256;
     if (Bp > (int)e->slots.size()) Bp = (int)e->slots.size();
-    // at most 2 steps in flight
-    while (e->inflight.size() >= 2) {
-        auto ev = e->inflight.front();
-        cvy_status st = check_cuda(e, cudaEventSynchronize(ev.second), "event sync");
-        if (st != CVY_OK) return st;
-        cudaEventElapsedTime(&e->last_step_ms, ev.first, ev.second);
-        e->inflight.pop_front();
-        e->event_pool.push_back(ev);
-    }
-    // ring back-pressure: worst case records of the steps in flight + this one
-    {
-        const uint64_t worst = (uint64_t)(e->inflight.size() + 1) * (uint64_t)(max_used + 1) * kMaxRecPerSlot;
-        auto t0 = std::chrono::steady_clock::now();
-        while (true) {
-            uint64_t tail = __atomic_load_n(e->h_ring_tail, __ATOMIC_ACQUIRE);
-            uint64_t head = __atomic_load_n(&e->ring_head, __ATOMIC_ACQUIRE);
-            if (tail - head + worst <= e->c.ring_records) break;
-            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30))
-                return fail(CVY_E_FULL, "segment ring full: poll_segments is not draining it");
-            std::this_thread::yield();
-        }
-    }
+    // from here on the queues are consumed: any failure is a CUDA error (sticky, engine dead)
     for (auto& u : uploads) {
         cvy_status st = check_cuda(e, cudaMemcpyAsync(u.dst, u.data.data(), u.data.size(), cudaMemcpyHostToDevice, e->stream),
                                    "upload");
         if (st != CVY_OK) return st;
     }
-    if (!patches.empty()) {
-        if ((int)patches.size() > e->max_patches) return fail(CVY_E_FULL, "too many pending patches");
+    for (const SynthJob& j : synths) {
+        int32_t* d_pages = e->d_page_table + (size_t)j.slot * e->c.max_pages_per_slot;
+        const int64_t n = (int64_t)e->m.n_layers * j.len * 2 * e->m.n_kv_heads * e->m.head_dim;
+        const int blocks = (int)std::min<int64_t>(4096, (n + 255) / 256);
+        if (e->bf16)
+            synth_prefix_kernel<__nv_bfloat16><<<blocks, 256, 0, e->stream>>>(
+                (__nv_bfloat16*)e->w.kv_pool, d_pages, (int)e->c.n_pages, e->m.n_layers, e->m.n_kv_heads,
+                e->m.head_dim, (int)j.len, j.seed);
+        else
+            synth_prefix_kernel<float><<<blocks, 256, 0, e->stream>>>(
+                (float*)e->w.kv_pool, d_pages, (int)e->c.n_pages, e->m.n_layers, e->m.n_kv_heads, e->m.head_dim,
+                (int)j.len, j.seed);
+        cvy_status cs = check_cuda(e, cudaGetLastError(), "synth prefix");
+        if (cs != CVY_OK) return cs;
+    }
+    // patches in chunks of the device patch buffer (stream order keeps them sequential)
+    for (size_t p0 = 0; p0 < patches.size(); p0 += (size_t)e->max_patches) {
+        const int np = (int)std::min<size_t>((size_t)e->max_patches, patches.size() - p0);
         cvy_status st = check_cuda(e,
-                                   cudaMemcpyAsync(e->d_patches, patches.data(), patches.size() * sizeof(Patch),
+                                   cudaMemcpyAsync(e->d_patches, patches.data() + p0, np * sizeof(Patch),
                                                    cudaMemcpyHostToDevice, e->stream),
                                    "patch upload");
         if (st != CVY_OK) return st;
-        apply_patches_kernel<<<1, 1, 0, e->stream>>>(e->d_slots, e->d_patches, (int)patches.size(),
+        apply_patches_kernel<<<1, 1, 0, e->stream>>>(e->d_slots, e->d_patches, np,
                                                      reinterpret_cast<SlotStatus*>(e->dm_status));
         st = check_cuda(e, cudaGetLastError(), "apply patches");
         if (st != CVY_OK) return st;

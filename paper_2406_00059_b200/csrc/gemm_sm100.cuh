@@ -532,9 +532,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // Host-side selection of the kernel instantiation for a plan (split mode is a runtime field).
 template <typename T, int EPI>
 inline const void* gemm_tc_kernel_ptr_k(int nsub, bool merge, int bk) {
-    if (bk == 32) return (const void*)gemm_tc_kernel<T, 1, false, 32, EPI>;
     if (merge) return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, true, 64, EPI> : (const void*)gemm_tc_kernel<T, 1, true, 64, EPI>;
-    return (const void*)gemm_tc_kernel<T, 1, false, 64, EPI>;
+    if (bk == 32)
+        return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, false, 32, EPI> : (const void*)gemm_tc_kernel<T, 1, false, 32, EPI>;
+    return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, false, 64, EPI> : (const void*)gemm_tc_kernel<T, 1, false, 64, EPI>;
 }
 template <typename T>
 inline const void* gemm_tc_kernel_ptr(int nsub, bool merge, int bk, int epi) {

@@ -38,7 +38,7 @@ def free_running_parity(shape, dtype, vocab, prompts, max_new, seed, tol, prefix
     dm, eng = make_engine(shape, dtype, vocab, len(prompts), seed, flags=flags,
                           max_pages_per_slot=max_pages_per_slot)
     bf16 = dtype == "bf16"
-    w = oracle.Weights(shape, seed, bf16=bf16, act_bf16=False)
+    w = oracle.Weights(shape, seed, bf16=bf16)
     max_ctx = prefix + max(len(p) for p in prompts) + max_new + 2
     oreqs = []
     rids = []

@@ -154,7 +154,7 @@ def test_7b_slice_b40_long_contexts_sampled(persistent, monkeypatch):
     prefix = [100 + (i * 37) % 500 for i in range(B)]
     rids = [eng.submit_request(p, 2, synth_prefix_len=prefix[i], synth_seed=100 + i) for i, p in enumerate(prompts)]
     sample = [0, 7, 19, 33, 39]
-    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
+    w = oracle.Weights(shape, seed, bf16=True)
     oreqs = []
     for i in sample:
         r = oracle.Request(w, prefix[i] + 8)
@@ -191,7 +191,7 @@ def test_7b_width_large_batch_sampled():
     prompts = [[1, rng.randrange(3, 32000)] for _ in range(B)]
     rids = [eng.submit_request(p, 2, synth_prefix_len=20 + (i % 50), synth_seed=i) for i, p in enumerate(prompts)]
     sample = [0, 1, 137, 255, 256, 300, 511]
-    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
+    w = oracle.Weights(shape, seed, bf16=True)
     oreqs = {}
     for i in sample:
         r = oracle.Request(w, 100)
@@ -491,7 +491,7 @@ def test_chunked_prefill_prompts_and_observations_match_oracle(which):
     B, seed, max_new = 5, 1010, 3
     flags = capi.ENGINE_DEBUG_LOGITS | capi.ENGINE_CHUNKED_PREFILL
     dm, eng = make_engine(shape, "bf16", vocab, B, seed, flags=flags, max_pages_per_slot=16)
-    w = oracle.Weights(shape, seed, bf16=True, act_bf16=False)
+    w = oracle.Weights(shape, seed, bf16=True)
     # 1 + 16 + 39 + 150 (+ the 65-token prompt's 64) rows: a 256-row pass (unmerged stream-K GEMMs)
     prompts = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 2, 17, 40, 151 if which == "tiny" else 65)]
     prefix = [0, 9, 0, 21, 3]
@@ -536,4 +536,162 @@ def test_chunked_prefill_prompts_and_observations_match_oracle(which):
                 nxt[i] = seq[-1]
                 eng.inject_observation(rids[i], obs[i], max_new)
     assert worst < 2e-2
+    eng.close()
+
+
+# ------------------------------------------------------------------ round-2 parity gaps
+def test_json_overflow_bitexact_short_segments():
+    """JSON_MEMBER / JSON_OBJECT with max_segment_bytes 16..64 (R13: an OVERFLOW cut every M bytes
+    without a natural cut; the automaton state carries on), 32k vocab, bit-exact vs the oracle."""
+    shape = slice_of(TINY, L=2, V=32000, name="tiny-v32k")
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    dm, eng = make_engine(shape, "bf16", vocab, 32, 1021, max_pages_per_slot=48)
+    cfgs = [(capi.PARSER_JSON_MEMBER, 16), (capi.PARSER_JSON_MEMBER, 24), (capi.PARSER_JSON_MEMBER, 40),
+            (capi.PARSER_JSON_MEMBER, 64), (capi.PARSER_JSON_OBJECT, 20), (capi.PARSER_JSON_OBJECT, 48)]
+    tools = [eng.register_tool(f"json{i}", kind, max_segment_bytes=ms) for i, (kind, ms) in enumerate(cfgs)]
+    rng = random.Random(21)
+    reqs, meta = [], []
+    for i in range(32):
+        k = i % len(cfgs)
+        kind, ms = cfgs[k]
+        text = validation_call(rng, rng.random() < 0.5) if kind == capi.PARSER_JSON_MEMBER else plan_stages(rng)
+        f = tok.encode(text)[:500]
+        reqs.append(([1, rng.randrange(3, 32000)], f, tools[k], 600))
+        meta.append((f, kind, ms))
+    rids, got = run_forced(eng, reqs)
+    n_over = 0
+    for rid, (f, kind, ms) in zip(rids, meta):
+        exp = expected_records(f, vocab, kind, [], ms)
+        assert as_tuples(got[rid]) == exp, rid
+        n_over += sum(1 for r in exp if r[6] & oracle.FLAG_OVERFLOW)
+    assert n_over > 50  # the OVERFLOW branch is exercised, not just reachable
+    eng.close()
+
+
+def test_ring_wrap_and_backpressure_bitexact():
+    """The smallest ring the ABI accepts (32 x slots records, power of two) carries > 10x its
+    capacity while a slow poller thread drains it: cvy_step blocks on back-pressure instead of
+    overwriting, and every request's record sequence stays bit-exact."""
+    import threading
+    import time
+    B = 16
+    ring = 512  # pow2 >= 32 * 16
+    dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, B, 1022, ring_records=ring, max_pages_per_slot=40)
+    delims = [b"a", b";", b"\n"]
+    tool = eng.register_tool("dense", capi.PARSER_LITERAL, delims)
+    rng = random.Random(22)
+    forced = [[rng.choice(b"ab;\n") for _ in range(450)] for _ in range(B)]
+    rids = [eng.submit_request(list(b"# t\n"), 1000, tool_id=tool, forced=f) for f in forced]
+    got, stop = [], threading.Event()
+
+    def poller():
+        while not stop.is_set():
+            got.extend(eng.poll_segments())
+            time.sleep(0.004)
+
+    th = threading.Thread(target=poller, daemon=True)
+    th.start()
+    blocked_steps = 0
+    for _ in range(470):
+        t0 = time.perf_counter()
+        eng.step()
+        blocked_steps += (time.perf_counter() - t0) > 0.003
+    eng.sync()
+    time.sleep(0.05)
+    stop.set()
+    th.join()
+    got.extend(eng.poll_segments())
+    by = group_records(got)
+    total = sum(len(v) for v in by.values())
+    assert total > 10 * ring
+    assert blocked_steps > 0  # back-pressure actually engaged
+    for rid, f in zip(rids, forced):
+        assert as_tuples(by[rid]) == expected_records(f, BYTE_VOCAB, oracle.PARSER_LITERAL, delims), rid
+    eng.close()
+
+
+def test_abort_and_refill_matches_oracle():
+    """NEXT-3 on the real engine: 32 validation requests through 8 slots.  A request whose
+    `location` member (seq 2) lacks ', ST' is cancelled when that record is polled (the
+    validator's abort); finished / aborted requests are released at once and the
+    next queued request is admitted into the freed slot.  Every request's records are bit-exact
+    against the oracle (aborted ones: the stream up to the GPU's cut, FINAL|CANCELLED), and every
+    step's logits of every request -- refilled slots included -- are within 2e-2 of the oracle."""
+    shape = slice_of(TINY, L=2, V=32000, name="tiny-v32k")
+    vocab = synthetic_vocab(32000)
+    tok = Tokenizer(vocab)
+    S, N = 8, 32
+    seed = 1023
+    dm, eng = make_engine(shape, "bf16", vocab, S, seed, max_pages_per_slot=40)
+    tool = eng.register_tool("validator", capi.PARSER_JSON_MEMBER)
+    rng = random.Random(23)
+    bad = [rng.random() < 0.5 for _ in range(N)]
+    forced = [tok.encode(validation_call(rng, b))[:300] for b in bad]
+    prompts = [[1, rng.randrange(3, 32000)] for _ in range(N)]
+    w = oracle.Weights(shape, seed, bf16=True)
+    queue = list(range(N))
+    live = {}      # rid -> [request index, oracle request, inputs fed, refilled slot?, cancel issued?]
+    recs, finished, rid_of = {}, {}, {}
+    maxdiff, refilled_checked, admitted = 0.0, 0, 0
+
+    def admit():
+        nonlocal admitted
+        while queue and len(live) < S:
+            i = queue.pop(0)
+            rid = eng.submit_request(prompts[i], 1000, tool_id=tool, forced=forced[i])
+            live[rid] = [i, oracle.Request(w, len(prompts[i]) + len(forced[i]) + 4), 0, admitted >= S, False]
+            rid_of[i] = rid
+            recs[rid] = []
+            admitted += 1
+
+    admit()
+    for _ in range(4000):
+        if not live:
+            break
+        eng.step()
+        eng.sync()
+        # every live request ran this step (submitted before it, round not over): compare its
+        # logits with the oracle fed the same input -- until a cancel makes the step count uncertain
+        ins, ors, gls = [], [], []
+        for rid, st in live.items():
+            i, orq, j, refill, cancelled = st
+            n_in = len(prompts[i]) + len(forced[i]) - 1
+            if cancelled or j >= n_in:
+                continue
+            ins.append(prompts[i][j] if j < len(prompts[i]) else forced[i][j - len(prompts[i])])
+            ors.append(orq)
+            gls.append((eng.debug_logits(rid), refill))
+            st[2] = j + 1
+        if ors:
+            for (gl, refill), o in zip(gls, oracle.step(ors, ins)):
+                d = float(np.max(np.abs(gl.astype(np.float64) - o)))
+                maxdiff = max(maxdiff, d)
+                assert d < 2e-2, d
+                refilled_checked += refill
+        for r in eng.poll_segments():
+            recs[r.req_id].append(r)
+            st = live.get(r.req_id)
+            if st and bad[st[0]] and r.seq == 2 and not (r.flags & capi.SEG_FINAL) and not st[4]:
+                eng.cancel_request(r.req_id)  # the validator's abort
+                st[4] = True
+            if r.flags & capi.SEG_FINAL:
+                finished[r.req_id] = r
+        for rid in [x for x in live if x in finished]:
+            eng.release_request(rid)  # frees the slot and its pages at once ...
+            del live[rid]
+        admit()                       # ... and the next queued request takes it
+    assert not live and not queue and len(finished) == N
+    n_cancelled = 0
+    for i in range(N):
+        rid = rid_of[i]
+        fin = finished[rid]
+        cancelled = bool(fin.flags & capi.SEG_CANCELLED)
+        n_cancelled += cancelled
+        n = fin.token_index + 1 if cancelled else len(forced[i])
+        exp = expected_records(forced[i][:n], vocab, oracle.PARSER_JSON_MEMBER, [], cancelled=cancelled)
+        assert as_tuples(recs[rid]) == exp, i
+        if cancelled:
+            assert bad[i] and n < len(forced[i])
+    assert n_cancelled >= 8 and refilled_checked > 100
     eng.close()

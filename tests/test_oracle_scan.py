@@ -235,6 +235,91 @@ def test_json_bruteforce_vs_stack_definition():
             assert oracle.segment(kind, [], BIG, S) == stack_cuts(S, member), S
 
 
+def stack_cuts_capped(S: bytes, member: bool, cap: int = 127):
+    """stack_cuts with the bounded nesting of reading R10: an opening bracket beyond `cap`
+    open brackets is not pushed (the automaton's depth saturates at 127)."""
+    stack, cuts, i, n = [], [], 0, len(S)
+    while i < n:
+        ch = S[i:i + 1]
+        if stack and ch == b'"':
+            j = i + 1
+            while j < n and S[j:j + 1] != b'"':
+                j += 2 if S[j:j + 1] == b"\\" else 1
+            if j >= n:
+                return cuts
+            i = j + 1
+            continue
+        if ch in (b"{", b"["):
+            if len(stack) < cap:
+                stack.append(ch)
+        elif stack and ch in (b"}", b"]"):
+            stack.pop()
+            if not stack:
+                cuts.append((i + 1, 1, 0))
+        elif member and ch == b"," and len(stack) == 1:
+            cuts.append((i + 1, 0, 0))
+        i += 1
+    return cuts
+
+
+def overflow_merge(natural, n: int, M: int):
+    """Independent reading of the OVERFLOW rule (R13) for the JSON parsers, whose automaton
+    state is not reset by an OVERFLOW cut: every natural cut stays a cut, and any run of M
+    bytes since the previous cut that reaches no natural cut is cut with OVERFLOW (delim NONE).
+    A natural cut exactly M bytes after the previous one stays natural."""
+    out, c = [], 0
+    for (p, did, fl) in natural:
+        while p - c > M:
+            c += M
+            out.append((c, oracle.DELIM_NONE, oracle.FLAG_OVERFLOW))
+        out.append((p, did, fl))
+        c = p
+    while n - c >= M:
+        c += M
+        out.append((c, oracle.DELIM_NONE, oracle.FLAG_OVERFLOW))
+    return out
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 5])
+def test_json_overflow_bruteforce_vs_merge_reading(M):
+    """JSON_MEMBER / JSON_OBJECT with a short max_segment_bytes: every string up to length 5
+    over 8 symbols equals the natural stack cuts with OVERFLOW cuts merged in."""
+    alpha = [b"{", b"}", b"[", b"]", b'"', b",", b"a", b"\\"]
+    for S in all_strings(alpha, 5):
+        for kind, member in ((MEM, True), (OBJ, False)):
+            exp = overflow_merge(stack_cuts(S, member), len(S), M)
+            assert oracle.segment(kind, [], M, S) == exp, (S, M)
+
+
+def test_json_overflow_random_long_members():
+    """Validation-shaped objects with members longer than max_segment_bytes (16..64)."""
+    rng = random.Random(31)
+    for _ in range(300):
+        obj = {f"k{i}": "".join(rng.choice('ab ,{}":\\') for _ in range(rng.randint(0, 90)))
+               for i in range(rng.randint(1, 8))}
+        S = b"x " + json.dumps(obj).encode() + b" tail"
+        M = rng.randint(16, 64)
+        for kind, member in ((MEM, True), (OBJ, False)):
+            assert oracle.segment(kind, [], M, S) == overflow_merge(stack_cuts(S, member), len(S), M)
+
+
+def test_json_depth_cap_127():
+    """Nesting deeper than 127 (R10): the depth saturates, so the object cut lands on the
+    127th closing bracket after the saturation -- equal to a stack that stops pushing at 127."""
+    S = b"[" * 130 + b"]" * 130
+    assert oracle.segment(OBJ, [], BIG, S) == [(130 + 127, 1, 0)] == stack_cuts_capped(S, False)
+    rng = random.Random(8)
+    for _ in range(200):
+        parts = []
+        for _ in range(rng.randint(1, 6)):
+            k = rng.randint(100, 140)
+            parts.append(b"{" * k + b'"a,]"' + b"," * rng.randint(0, 2) + b"]" * rng.randint(k - 5, k + 5))
+        S = b"".join(parts)
+        for kind, member in ((MEM, True), (OBJ, False)):
+            assert oracle.segment(kind, [], BIG, S) == stack_cuts_capped(S, member)
+            assert oracle.segment(kind, [], 50, S) == overflow_merge(stack_cuts_capped(S, member), len(S), 50)
+
+
 # ---------------------------------------------------------------- paper structure
 
 
