@@ -1,18 +1,23 @@
 #!/usr/bin/env python
-"""bench.py -- decode throughput of the Conveyor hot path on B200 (BASELINE.json metric).
+"""bench.py -- the Conveyor decode hot path on B200 (BASELINE.json metric).
 
 One "step" = one continuous-batching decode step of the whole hot path (SURVEY.md 8(a)
 S1-S13: embed, 32 x [QKV+RoPE+KV append, paged GQA attention, O+residual, gate/up+SwiGLU,
-down+residual], LM head + greedy sample + fused trigger scan + compaction + publish) for
-the N=1 workload of BASELINE.json configs[1] ("codegen"): Mistral-7B-shape random-init
-bf16, 64 in-flight requests per GPU, synthetic KV prefix 128 + U(0,400) tokens, teacher-
-forced ~400-token Python-script streams through the code-interpreter tool ('\\n').
+down+residual], LM head + greedy sample + fused trigger scan + compaction + publish).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Default workload = BASELINE.json configs[4], "validation" (the largest single-GPU config;
+BASELINE.json's metric names no config): Mistral-7B-shape random-init bf16, a TOTAL batch of
+512 in-flight requests split over the ranks by the router (request k -> rank k mod G), 2K-token
+contexts in the paged KV cache (synthetic prefix 1792 tokens, growing to ~2048), teacher-forced
+streams of structured JSON calls through the incremental format-validator tool (JSON_MEMBER).
+`--workload codegen` runs configs[1] (B = 64, prefixes 128 + U(0, 400), Python scripts, '\\n').
 
-Prints ONE JSON line (rank 0).  `value` = generated tokens/s of the whole job with inputs
-resident in HBM (device time, CUDA events on the engine stream, max over ranks).  Inputs
-are larger than L2 (14.2 GB of weights streamed every step), so no L2 flush is needed.
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload ...]
+
+`--gpus N` without torchrun spawns its own N ranks (127.0.0.1).  Rank 0 prints ONE JSON line:
+`value` = generated tokens/s of the whole job over the K timed steps (inputs resident in HBM;
+device time from CUDA events on the engine stream, max over ranks).  Inputs exceed L2
+(14.2 GB of weights + the KV cache streamed every step), so no L2 flush is needed.
 """
 from __future__ import annotations
 
@@ -20,6 +25,7 @@ import argparse
 import json
 import os
 import random
+import socket
 import subprocess
 import sys
 import threading
@@ -30,6 +36,11 @@ sys.path.insert(0, ROOT)
 
 METRIC = "decode tokens/s/GPU + HBM roofline %; request latency, partial vs sequential tool exec"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+WORKLOADS = {
+    "validation": {"config": "BASELINE.json configs[4] (validation)", "batch": 512},
+    "codegen": {"config": "BASELINE.json configs[1] (codegen)", "batch": 64},
+}
+SPAN_STEPS = 3
 
 
 def _flatten(d, pre=""):
@@ -77,22 +88,37 @@ def load_peaks():
 
 
 # ------------------------------------------------------------------ workload
-def codegen_workload(B: int, gen_tokens: int, seed: int = 2001, prefix_min: int = 128, prefix_spread: int = 400):
-    """Per request: synthetic prefix length, synth seed, forced token stream (teacher forcing
-    of codegen scripts)."""
+def workload_requests(name: str, indices, gen_tokens: int, prefix: int | None = None):
+    """Requests of a config's total batch (global indices `indices`: this rank's share under
+    the router).  Per request: synthetic KV prefix length, synth seed (= global index), and the
+    teacher-forced generated stream (DESIGN.md §5 "Input recipe")."""
     from inputs.vocab import Tokenizer, synthetic_vocab
-    from inputs.workloads import codegen_script
+    from inputs.workloads import codegen_script, validation_call
     vocab = synthetic_vocab(32000)
     tok = Tokenizer(vocab)
-    rng = random.Random(seed)
     reqs = []
-    for b in range(B):
-        prefix = prefix_min + (rng.randrange(0, prefix_spread) if prefix_spread > 0 else 0)
-        ids = []
-        while len(ids) < gen_tokens:
-            ids += tok.encode(codegen_script(rng, 40))
-        reqs.append({"prefix": prefix, "seed": b, "forced": ids[:gen_tokens]})
+    for k in indices:
+        rng = random.Random(2000 + 100003 * (k + 1) + (4 if name == "validation" else 1))
+        if name == "validation":
+            p = prefix if prefix is not None else 1792
+            ids = []
+            while len(ids) < gen_tokens:   # consecutive validator calls (one JSON object each)
+                ids += tok.encode(validation_call(rng, rng.random() < 0.5) + "\n")
+        else:
+            p = prefix if prefix is not None else 128 + rng.randrange(0, 400)
+            ids = []
+            while len(ids) < gen_tokens:
+                ids += tok.encode(codegen_script(rng, 40))
+        reqs.append({"k": k, "prefix": p, "seed": k, "forced": ids[:gen_tokens]})
     return vocab, reqs
+
+
+def default_prefix(name: str, gen: int):
+    """validation: contexts reach 2048 (SURVEY.md 8(d) C4: prefix 1792 + the ~256-token output);
+    a longer timed run starts from a shorter prefix so the context still ends near 2048."""
+    if name == "validation":
+        return 1792 if gen <= 256 else max(512, 2048 - gen)
+    return None
 
 
 # ------------------------------------------------------------------ clocks
@@ -127,7 +153,7 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
-        sm, mx, reasons = [], None, set()
+        sm, mx, pw, reasons = [], None, [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -136,6 +162,7 @@ class ClockSampler:
             try:
                 sm.append(float(parts[1]))
                 mx = float(parts[2])
+                pw.append(float(parts[3]))
             except ValueError:
                 continue
             for n, v in zip(names, parts[5:9]):
@@ -144,7 +171,9 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm.sort()
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        pw.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_median": pw[len(pw) // 2] if pw else None}
 
 
 # ------------------------------------------------------------------ multi-rank reduction
@@ -167,10 +196,21 @@ def reduce_over_ranks(local_ms: float, local_tokens: int, stats: list, device=No
     return float(t.item()), int(n.item()), [list(map(float, g.tolist())) for g in gathered]
 
 
-# ------------------------------------------------------------------ algorithmic bytes
+def gather_objects(obj):
+    """All ranks' `obj` (rank order); [obj] without a process group."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [obj]
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, obj)
+    return out
+
+
+# ------------------------------------------------------------------ algorithmic bytes / flops
 def gemm_launch_bytes(shape, kind: int, B: int) -> int:
-    """Algorithmic HBM bytes of one projection GEMM launch: the bf16
-    weight matrix streamed once + the bf16 activation rows read + the rows written."""
+    """Algorithmic HBM bytes of one projection GEMM launch: the bf16 weight
+    matrix streamed once + the bf16 activation rows read + the rows written (QKV: q fp32 and
+    the new token's K, V appended to the paged cache)."""
     d, H, Hkv, hd, dff, V = shape.d, shape.H, shape.Hkv, shape.hd, shape.dff, shape.V
     if kind == 1:
         N, K, out = (H + 2 * Hkv) * hd, d, B * (H * hd * 4 + 2 * Hkv * hd * 2)
@@ -185,14 +225,17 @@ def gemm_launch_bytes(shape, kind: int, B: int) -> int:
     return N * K * 2 + B * K * 2 + out
 
 
-def pk_launch_bytes(shape, ctx_lens):
-    """Algorithmic HBM bytes of one persistent all-layers launch: every layer's QKV, O,
-    gate/up and down weights streamed once (bf16) + the KV cache read (ctx incl. the new
-    token) + the new token's K, V appended.  Activations are excluded (L2-resident)."""
-    d, H, Hkv, hd, dff, L = shape.d, shape.H, shape.Hkv, shape.hd, shape.dff, shape.L
-    layer_params = (H + 2 * Hkv) * hd * d + d * H * hd + 2 * dff * d + d * dff
-    kv_tok = shape.kv_bytes_per_token
-    return 2 * L * layer_params + sum(c + 1 for c in ctx_lens) * kv_tok + len(ctx_lens) * kv_tok
+def gemm_launch_flops(shape, kind: int, B: int) -> float:
+    """Tensor-core flops of one projection launch as executed: 2 N K per batch column, twice
+    for the (hi, lo) activation pair."""
+    d, H, Hkv, hd, dff, V = shape.d, shape.H, shape.Hkv, shape.hd, shape.dff, shape.V
+    NK = {1: (H + 2 * Hkv) * hd * d, 4: d * H * hd, 5: 2 * dff * d, 6: d * dff, 7: V * d}[kind]
+    return 2.0 * NK * B * 2
+
+
+def attention_launch_bytes(shape, ctx_lens) -> int:
+    """One layer's paged attention: the K and V of keys [0, ctx] of every slot (bf16)."""
+    return sum(c + 1 for c in ctx_lens) * (shape.kv_bytes_per_token // shape.L)
 
 
 def step_alg_bytes(shape, ctx_lens):
@@ -204,9 +247,12 @@ def step_alg_bytes(shape, ctx_lens):
 # ------------------------------------------------------------------ CPU oracle timing
 def time_oracle(shape, reqs, budget_s: float, seed: int, n_req: int | None = None, max_steps: int | None = None):
     """Run the CPU oracle (as it stands, weights regenerated from the counter hash every step,
-    no caching) on a bounded sample of the same workload: decode steps for a sample of the
-    requests (their synthetic prefixes, first input token).  The sample size is calibrated
-    so the total lands near budget_s.  Returns (tokens, seconds, threads, n_req, steps)."""
+    no caching) on a bounded sample of the same workload: decode steps for n_req of the
+    requests (their synthetic prefixes, first input token).  Stops after max_steps steps, or
+    once budget_s seconds of oracle time are spent (whichever comes first; at least one of the
+    two must bound the loop).  Returns (tokens, seconds, threads, n_req, steps)."""
+    if not ((max_steps is not None and max_steps >= 1) or budget_s > 0):
+        raise ValueError("time_oracle needs max_steps >= 1 or a positive time budget")
     import oracle
     w = oracle.Weights(shape, seed, bf16=True, cache=False)
 
@@ -221,8 +267,8 @@ def time_oracle(shape, reqs, budget_s: float, seed: int, n_req: int | None = Non
         return time.perf_counter() - t0
 
     if n_req is None:
-        t1 = one_step(reqs[:1])
-        n_req = max(1, min(len(reqs), int(budget_s / 3 / max(t1, 1e-3))))
+        n_req = 4
+    n_req = max(1, min(n_req, len(reqs)))
     t_total, toks, steps, i = 0.0, 0, 0, 0
     while True:
         sample = [reqs[(i + j) % len(reqs)] for j in range(n_req)]
@@ -230,10 +276,15 @@ def time_oracle(shape, reqs, budget_s: float, seed: int, n_req: int | None = Non
         toks += n_req
         steps += 1
         i += n_req
-        # budget_s <= 0: no time budget (exactly max_steps steps, as the reference arm needs)
-        if (budget_s > 0 and t_total >= budget_s) or (max_steps and steps >= max_steps):
+        if (budget_s > 0 and t_total >= budget_s) or (max_steps is not None and steps >= max_steps):
             break
     return toks, t_total, oracle.num_threads(), n_req, steps
+
+
+def oracle_sample_text(name, n, steps, secs):
+    return (f"{steps} oracle decode step(s), each over {n} of the {WORKLOADS[name]['batch']} {name} requests "
+            f"(full 32 layers at their synthetic-prefix contexts, weights regenerated per step as the oracle "
+            f"stands), {secs:.1f} s of CPU work")
 
 
 # ------------------------------------------------------------------ reference arm
@@ -242,33 +293,37 @@ def run_reference(args):
     if rank != 0:
         return
     from inputs.configs import MISTRAL_7B
-    B = 64
-    _, reqs = codegen_workload(B, 8)
-    # calibrate: size each step (a sample of the 64 requests) to ~1 s of CPU work
-    _, t1, cores, _, _ = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=1, max_steps=1)
-    n = max(1, min(B, int(1.0 / max(t1, 1e-3))))
-    _, _, _, _, _ = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=n, max_steps=args.warmup)
-    total_tok, total_t, cores, _, _ = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=n, max_steps=args.steps)
+    B = WORKLOADS[args.workload]["batch"]
+    gen = args.warmup + args.steps + SPAN_STEPS + 8
+    prefix = args.prefix if args.prefix is not None else default_prefix(args.workload, gen)
+    _, reqs = workload_requests(args.workload, range(B), 8, prefix)
+    n = args.cpu_sample
+    if args.warmup > 0:
+        time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=n, max_steps=args.warmup)
+    total_tok, total_t, cores, _, steps = time_oracle(MISTRAL_7B, reqs, 0.0, 1001, n_req=n, max_steps=args.steps)
     value = total_tok / total_t
-    sample = f"{n} of the 64 codegen requests per step (1 decode step each, full 32 layers, their synthetic prefixes)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total_t / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(B, None),
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args.workload, B, None, None, prefix),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                             "sample": oracle_sample_text(args.workload, n, steps, total_t), "host": host_info()},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def workload_config(B, ctx_mean, prefix_min=128, prefix_spread=400):
-    return {"workload": "codegen (BASELINE.json configs[1]): Mistral-7B-shape random-init, "
-                        "teacher-forced Python-script streams, code-interpreter tool '\\n' (partial mode)"
-                        if (B, prefix_min, prefix_spread) == (64, 128, 400) else
-                        f"decode step at batch {B}, synthetic KV prefixes {prefix_min}+U(0,{prefix_spread}) "
-                        "(Mistral-7B shape, codegen streams; SURVEY.md 8(d) config points)",
-            "batch_per_gpu": B, "kv_prefix": f"{prefix_min}+U(0,{prefix_spread}) synthetic tokens",
+def workload_config(name, B_total, ctx_mean, world, prefix=None):
+    return {"workload": f"{WORKLOADS[name]['config']}: Mistral-7B-shape random-init bf16, total batch {B_total} "
+                        f"split over the ranks (request k -> rank k mod G), "
+                        + ("2K-token contexts (synthetic KV prefix, paged), teacher-forced JSON calls through the "
+                           "format-validator tool (JSON_MEMBER), partial execution"
+                           if name == "validation" else
+                           "synthetic KV prefixes 128+U(0,400), teacher-forced Python scripts through the "
+                           "code-interpreter tool ('\\n'), partial execution"),
+            "batch_total": B_total, "batch_per_gpu": None if not world else B_total // world,
+            "kv_prefix": (f"{prefix} synthetic tokens" if prefix else "128+U(0,400) synthetic tokens"),
             "ctx_mean": ctx_mean,
-            "l2": "no flush: inputs > L2 (14.2 GB weights + KV streamed per step)"}
+            "l2": "no flush: inputs > L2 (14.2 GB of weights + the KV cache streamed per step)"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -283,32 +338,42 @@ def run_ours(args):
     # test hooks for the multi-rank path on a single-GPU box: CVY_DIST_BACKEND=gloo (reductions
     # on host tensors) and CVY_SAME_GPU=1 (every rank on device 0); the driver's runs use NCCL,
     # one GPU per rank
-    backend = os.environ.get("CVY_DIST_BACKEND", "nccl")
-    if os.environ.get("CVY_SAME_GPU") == "1":
+    same_gpu = os.environ.get("CVY_SAME_GPU") == "1"
+    # NCCL refuses two ranks on one device: the single-GPU test hook reduces over gloo
+    backend = os.environ.get("CVY_DIST_BACKEND", "gloo" if same_gpu else "nccl")
+    if same_gpu:
         local = 0
-    red_dev = "cuda" if backend == "nccl" else None
+    torch.cuda.set_device(local)
+    red_dev = torch.device("cuda", local) if backend == "nccl" else None
     if world > 1:
         dist.init_process_group(backend)
-    torch.cuda.set_device(local)
 
     from inputs.configs import MISTRAL_7B
     from paper_2406_00059_b200 import build, capi
     from paper_2406_00059_b200.engine import DeviceModel, Engine
+    from paper_2406_00059_b200.router import STATS_FIELDS, Router
     build.build()
     shape = MISTRAL_7B
-    B = args.batch
+    name = args.workload
+    B_total = args.batch or WORKLOADS[name]["batch"]
+    router = Router(rank, world, every=16, device=red_dev)
+    mine = router.mine(B_total)
+    B = len(mine)
     W, K = args.warmup, args.steps
-    gen = W + K + 8
-    vocab, reqs = codegen_workload(B, gen, prefix_min=args.prefix_min, prefix_spread=args.prefix_spread)
+    gen = W + K + SPAN_STEPS + 8
+    prefix = args.prefix if args.prefix is not None else default_prefix(name, gen)
+    vocab, reqs = workload_requests(name, mine, gen, prefix)
     max_ctx = max(r["prefix"] for r in reqs) + gen + 64
     pages_per_slot = (max_ctx + 15) // 16 + 1
-    n_pages = B * pages_per_slot + 64
+    lat_pages = 0 if args.no_latency else latency_pages(router)
+    n_pages = max(B * pages_per_slot, lat_pages) + 64
     dm = DeviceModel(shape, "bf16", n_pages, seed=1001, device=local)
-    # chunked prefill only changes requests with multi-token prompts: the timed decode batch
-    # submits 1-token prompts (synthetic prefixes); the e2e leg's 16-token prompts use it
     eng = Engine(dm, vocab, max_slots=B, max_pages_per_slot=pages_per_slot, device=local,
                  flags=(capi.ENGINE_SCAN_OFF if args.scan_off else 0) | capi.ENGINE_CHUNKED_PREFILL)
-    tool = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n"])
+    if name == "validation":
+        tool = eng.register_tool("validator", capi.PARSER_JSON_MEMBER)
+    else:
+        tool = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n"])
     rids = [eng.submit_request([1], gen, tool_id=tool, forced=r["forced"], synth_prefix_len=r["prefix"],
                                synth_seed=r["seed"]) for r in reqs]
 
@@ -329,108 +394,51 @@ def run_ours(args):
     for _ in range(W):
         eng.step()
     eng.sync()
-    ctx_start = [r["prefix"] + 1 + W for r in reqs]  # positions at the first timed step
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
     wall0 = time.perf_counter()
-    ev0.record(stream)
-    for _ in range(K):
-        eng.step()
-    ev1.record(stream)
-    ev1.synchronize()
+    evs[0].record(stream)
+    for i in range(K):
+        info = eng.step()
+        router.after_step(info)
+        evs[i + 1].record(stream)
+    evs[K].synchronize()
     wall = time.perf_counter() - wall0
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     clk = clocks.stop()
-    dev_ms = ev0.elapsed_time(ev1)
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(K)]
+    dev_ms = evs[0].elapsed_time(evs[K])
+    med_local = float(np.median(step_ms))
     perf = eng.perf()
-    max_ms, total_tokens, rank_stats = reduce_over_ranks(dev_ms, B * K, [float(rank), dev_ms, float(B * K)],
+    max_ms, total_tokens, rank_stats = reduce_over_ranks(dev_ms, B * K, [float(rank), dev_ms, float(B * K), med_local],
                                                          device=red_dev)
     value = total_tokens / (max_ms / 1000.0)
-    ctx_mean = float(np.mean([c + K / 2 for c in ctx_start]))
+    ms_med = max(s[3] for s in rank_stats)
+    ctx_mean = float(np.mean([r["prefix"] + W + (K - 1) / 2.0 for r in reqs]))  # step t attends prefix + t + 1 keys
+    stats_table = router.flush()
 
-    # per-kernel probe (timed graph variant: event pair per launch, no PDL): kernel shares
-    eng.set_kernel_timing(True)
-    for _ in range(3):
+    # in-graph kernel spans of the same graph (+ %globaltimer atomics): kernel shares
+    eng.set_kernel_spans(True)
+    span_runs = []
+    for _ in range(SPAN_STEPS):
         eng.step()
-    kt = eng.kernel_times()
-    eng.set_kernel_timing(False)
+        span_runs.append(eng.kernel_spans())
+    eng.set_kernel_spans(False)
     eng.sync()
-    probe_ctx = [c + K + 2 for c in ctx_start]
-    by_kind = {}
-    gemm_ms, gemm_bytes = 0.0, 0
-    for kind, layer, ms in kt:
-        by_kind.setdefault(capi.KERNEL_KINDS[kind], [0.0, 0])
-        by_kind[capi.KERNEL_KINDS[kind]][0] += ms
-        by_kind[capi.KERNEL_KINDS[kind]][1] += 1
-        if kind in (1, 4, 5, 6, 7):
-            gemm_ms += ms
-            gemm_bytes += gemm_launch_bytes(shape, kind, B)
-    probe_ms = sum(ms for _, _, ms in kt)
-    attn_ms = by_kind.get("attention", [0, 0])[0] + by_kind.get("attention_merge", [0, 0])[0]
-    kv_bytes = sum(c + 1 for c in probe_ctx) * shape.kv_bytes_per_token
+    span_ctx = [r["prefix"] + W + K + SPAN_STEPS - 1 for r in reqs]   # the last recorded step
     peaks, peaks_src = load_peaks()
-    hbm = float(peaks["hbm_gbs"])
-    pk_ms = by_kind.get("layers_persistent", [0.0, 0])[0]
-    if pk_ms > 0:
-        # persistent all-layers kernel: one launch per step streams every layer's projection
-        # weights once and reads / appends the KV cache
-        pk_bytes = pk_launch_bytes(shape, probe_ctx)
-        achieved = pk_bytes / (pk_ms / 1000.0) / 1e9
-        traffic = load_traffic("pk_traffic.json")
-        roofline = {"bound": "hbm",
-                    "kernel": "layers_persistent_kernel (all 32 layers: tcgen05 stream-K projections + paged attention, 1 launch/step)",
-                    "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "peak_source": f"{peaks_src} HBM copy bandwidth",
-                    "alg_bytes_per_launch": pk_bytes,
-                    "traffic": (traffic or {}).get("per_launch_bytes"),
-                    "traffic_detail": None if traffic is None else {
-                        "alg_per_launch_bytes": traffic["alg_per_launch_bytes"], "ratio": traffic["ratio"],
-                        "source": "profiles/pk_traffic.json: " + traffic["source"]},
-                    "share_of_step": pk_ms / probe_ms,
-                    "kernels_ms_per_step": {k: round(v[0], 4) for k, v in by_kind.items()},
-                    "probe_step_ms": probe_ms}
-    else:
-        achieved = gemm_bytes / (gemm_ms / 1000.0) / 1e9
-        traffic = load_traffic()
-        roofline = {"bound": "hbm", "kernel": "gemm_tc_kernel (tcgen05 projections, cluster split-K for narrow N, all 129 launches/step)",
-                    "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                    "peak_source": f"{peaks_src} HBM copy bandwidth",
-                    "traffic": (traffic or {}).get("per_launch_bytes"),
-                    "traffic_detail": None if traffic is None else {
-                        "alg_per_launch_bytes": traffic["alg_per_launch_bytes"], "ratio": traffic["ratio"],
-                        "source": "profiles/gemm_traffic.json: " + traffic["source"]},
-                    "share_of_step": gemm_ms / probe_ms,
-                    "attention": {"achieved": kv_bytes / (attn_ms / 1000.0) / 1e9, "frac": kv_bytes / (attn_ms / 1000.0) / 1e9 / hbm,
-                                  "ms_per_step": attn_ms},
-                    "kernels_ms_per_step": {k: round(v[0], 4) for k, v in by_kind.items()},
-                    "probe_step_ms": probe_ms}
-    step_bytes = step_alg_bytes(shape, [c + K / 2 for c in ctx_start])
-    step_roof = {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (max_ms / K / 1000.0) / 1e9,
-                 "frac": step_bytes / (max_ms / K / 1000.0) / 1e9 / hbm}
-    # phase roofline: t_min = sum over phases of max(bytes / HBM, flops / TC);
-    # the projections' flops count the (hi, lo) activation pair twice
-    tc = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])) * 1e12
-    ctx_now = [c + K / 2 for c in ctx_start]
-    proj_bytes = 2.0 * shape.n_params_streamed
-    proj_flops = 2.0 * shape.n_params_streamed * B * 2
-    kv_tok = shape.kv_bytes_per_token
-    att_bytes = sum(c + 1 for c in ctx_now) * kv_tok + B * kv_tok
-    att_flops = 4.0 * shape.L * shape.H * shape.hd * sum(c + 1 for c in ctx_now)
-    t_proj = max(proj_bytes / (hbm * 1e9), proj_flops / tc)
-    t_att = max(att_bytes / (hbm * 1e9), att_flops / tc)
-    t_meas = max_ms / K / 1000.0
-    step_roof["phase_roofline"] = {"t_min_ms": (t_proj + t_att) * 1e3, "frac": (t_proj + t_att) / t_meas,
-                                   "projections": "tensor" if proj_flops / tc > proj_bytes / (hbm * 1e9) else "hbm",
-                                   "tc_peak_tflops": tc / 1e12}
+    roofline, kernels = span_roofline(shape, span_runs[-1], span_ctx, B, peaks, peaks_src, ms_med)
+    ctx_now = [r["prefix"] + W + (K - 1) / 2.0 for r in reqs]
+    step_roof = step_roofline(shape, ctx_now, B, max_ms / K, ms_med, peaks)
 
-    # end-to-end through the C ABI with host buffers: release, then a fresh batch whose
-    # prompts and forced streams come from host memory; timed until every FINAL is polled and
-    # every request's generated tokens are read back to the host.
+    # end-to-end through the C ABI with host buffers
     stop.set()
     th.join()
     eng.sync()
@@ -446,33 +454,129 @@ def run_ours(args):
         eng.release_request(rid)
     e2e = run_e2e(eng, reqs, tool, B)
     eng.close()
-    # whole-job e2e at N GPUs: all ranks' generated tokens / the slowest rank's wall time
     e2e_ms, e2e_tok, _ = reduce_over_ranks(e2e.pop("_dt_s") * 1e3, e2e.pop("_ntok"), [0.0], device=red_dev)
     e2e["per_rank_value"] = e2e["value"]
     e2e["value"] = e2e_tok / (e2e_ms / 1000.0)
 
+    latency = None
+    if not args.no_latency:
+        latency = run_latency_ab(dm, router, reps=args.latency_reps, device=local)
+    del dm
+
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            toks, secs, cores, n, steps = time_oracle(shape, reqs, args.cpu_budget, 1001)
+            toks, secs, cores, n, steps = time_oracle(shape, reqs, args.cpu_budget, 1001, n_req=args.cpu_sample)
             cpu = {"value": toks / secs, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                   "sample": f"{steps} decode step(s) x {n} of the 64 codegen requests (full 32 layers, their "
-                             f"synthetic prefixes), {secs:.1f} s of CPU work"}
+                   "sample": oracle_sample_text(name, n, steps, secs), "host": host_info()}
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
-                "ms_per_step": max_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": "bf16", "data": "synthetic", "config": workload_config(B, ctx_mean, args.prefix_min, args.prefix_spread),
-                "tokens_per_s_per_gpu": value / world, "roofline": roofline, "step_roofline": step_roof,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(perf.launches_per_step) * K,
-                "clocks": clk, "wall_s_timed": wall, "segments_polled": nseg[0],
-                "rank_stats": rank_stats}
+                "ms_per_step": max_ms / K, "ms_per_step_median": ms_med, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": workload_config(name, B_total, ctx_mean, world, prefix),
+                "tokens_per_s_per_gpu": value / world, "roofline": roofline, "kernels": kernels,
+                "step_roofline": step_roof, "cpu_baseline": cpu, "e2e": e2e, "latency": latency,
+                "gpu_launches": int(perf.launches_per_step) * K, "launches_per_step": int(perf.launches_per_step),
+                "clocks": clk, "wall_s_timed": wall, "segments_polled": nseg[0], "rank_stats": rank_stats,
+                "router": {"policy": "request k -> rank k mod G", "stats_every_steps": 16, "gathers": router.gathers,
+                           "fields": list(STATS_FIELDS), "last_gather": stats_table}}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
+def span_roofline(shape, spans, ctx, B, peaks, peaks_src, ms_step):
+    """Per-kernel device time from the in-graph spans of one step (cvy_kernel_spans) and the
+    roofline of the dominant kernel: achieved = algorithmic bytes per launch x launches / the
+    summed spans; frac = achieved / the measured HBM copy peak."""
+    from paper_2406_00059_b200 import capi
+    hbm = float(peaks["hbm_gbs"])
+    tc = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"]))
+    per = {}
+    for kind, layer, chain, t0, t1 in spans:
+        k = per.setdefault(kind, {"ms": 0.0, "launches": 0})
+        k["ms"] += (t1 - t0) / 1e6
+        k["launches"] += 1
+    kernels = {}
+    for kind, v in sorted(per.items()):
+        name = capi.KERNEL_KINDS[kind]
+        if kind == 2:
+            by = attention_launch_bytes(shape, ctx) * v["launches"]
+            fl = 4.0 * shape.H * shape.hd * sum(c + 1 for c in ctx) * v["launches"]
+        elif kind in (1, 4, 5, 6, 7):
+            by = gemm_launch_bytes(shape, kind, B) * v["launches"]
+            fl = gemm_launch_flops(shape, kind, B) * v["launches"]
+        else:
+            by = B * shape.d * (2 + 4 + 2 * 2) * v["launches"]
+            fl = 0.0
+        s = v["ms"] / 1e3
+        kernels[name] = {"ms_per_step": round(v["ms"], 4), "launches": v["launches"], "alg_bytes": by,
+                         "GBps": by / s / 1e9 if s > 0 else None, "hbm_frac": by / s / 1e9 / hbm if s > 0 else None,
+                         "TFLOPs": fl / s / 1e12 if s > 0 and fl else None,
+                         "tc_frac": fl / s / 1e12 / tc if s > 0 and fl and kind != 2 else None}
+    gemm_ms = sum(per[k]["ms"] for k in (1, 4, 5, 6, 7) if k in per)
+    attn_ms = per.get(2, {"ms": 0.0})["ms"]
+    if attn_ms >= gemm_ms:
+        v = per[2]
+        by = attention_launch_bytes(shape, ctx)
+        name = "attention_tc_kernel (paged GQA decode attention: TMA KV pages + mma.sync, online softmax)"
+        launches, ms = v["launches"], v["ms"]
+    else:
+        launches = sum(per[k]["launches"] for k in (1, 4, 5, 6, 7) if k in per)
+        by = sum(gemm_launch_bytes(shape, k, B) * per[k]["launches"] for k in (1, 4, 5, 6, 7) if k in per) / launches
+        name = "gemm_tc_kernel (tcgen05 projections QKV / O / gate-up / down / LM head, all launches of the step)"
+        ms = gemm_ms
+    achieved = by * launches / (ms / 1e3) / 1e9
+    traffic = load_traffic("attention_traffic.json" if attn_ms >= gemm_ms else "gemm_traffic.json")
+    roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": f"{peaks_src} HBM copy bandwidth (MEASURED_PEAKS.json)",
+                "alg_bytes_per_launch": by, "launches_per_step": launches, "ms_per_step": ms,
+                "share_of_step": ms / ms_step,
+                "timing": "sum of in-graph spans (first CTA past its grid-dependency wait -> last CTA exit, "
+                          "%globaltimer) of this kernel's launches in one step of the production graph",
+                "traffic": (traffic or {}).get("per_launch_bytes"),
+                "traffic_detail": None if traffic is None else {k: traffic[k] for k in traffic if k != "per_launch_bytes"}}
+    return roofline, kernels
+
+
+def step_roofline(shape, ctx_now, B, ms_mean, ms_med, peaks):
+    """Whole-step HBM roofline and the phase roofline of SURVEY.md 8(d)."""
+    hbm = float(peaks["hbm_gbs"])
+    tc = float(peaks.get("bf16_tflops", PEAKS_FALLBACK["bf16_tflops"])) * 1e12
+    step_bytes = step_alg_bytes(shape, ctx_now)
+    kv_tok = shape.kv_bytes_per_token
+    proj_bytes = 2.0 * shape.n_params_streamed
+    proj_flops = 2.0 * shape.n_params_streamed * B * 2
+    att_bytes = sum(c + 1 for c in ctx_now) * kv_tok + B * kv_tok
+    att_flops = 4.0 * shape.L * shape.H * shape.hd * sum(c + 1 for c in ctx_now)
+    t_proj = max(proj_bytes / (hbm * 1e9), proj_flops / tc)
+    t_att = max(att_bytes / (hbm * 1e9), att_flops / tc)
+    return {"alg_bytes_per_step": step_bytes, "achieved_GBps": step_bytes / (ms_mean / 1e3) / 1e9,
+            "frac": step_bytes / (ms_mean / 1e3) / 1e9 / hbm,
+            "frac_median_step": step_bytes / (ms_med / 1e3) / 1e9 / hbm,
+            "frac_vs_8TBps_nominal": step_bytes / (ms_mean / 1e3) / 8e12,
+            "phase_roofline": {"t_min_ms": (t_proj + t_att) * 1e3, "frac": (t_proj + t_att) / (ms_mean / 1e3),
+                               "projections": "tensor" if proj_flops / tc > proj_bytes / (hbm * 1e9) else "hbm",
+                               "tc_peak_tflops": tc / 1e12,
+                               "note": "projection flops count the (hi, lo) activation pair twice (DESIGN.md §4)"}}
+
+
+def host_info():
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def run_e2e(eng, reqs, tool, B):
-    import numpy as np
+    """The same metric end to end through the C ABI: a fresh batch whose prompts (16 tokens) and
+    forced streams come from host memory (submit copies them; the chunked prefill pass runs the
+    prompts), decoded until every FINAL is polled and every request's tokens are read back."""
     G = 64
     prompt_len = 16
     rng = random.Random(77)
@@ -500,12 +604,12 @@ def run_e2e(eng, reqs, tool, B):
     d2h = nrec * 40 + nbytes + ntok * 4
     return {"value": ntok / dt, "_dt_s": dt, "_ntok": ntok, "unit": "tokens/s", "h2d_bytes_per_step": h2d / steps,
             "d2h_bytes_per_step": d2h / steps, "steps": steps, "requests": B, "generated_per_request": G,
-            "prompt_tokens": prompt_len, "includes": "submit (host prompts + forced streams), chunked prefill "
-                                                     "(CVY_ENGINE_CHUNKED_PREFILL), decode, segment polling, "
-                                                     "token read-back"}
+            "prompt_tokens": prompt_len, "includes": "submit (host prompts + forced streams, synthetic KV prefix), "
+                                                     "chunked prefill (CVY_ENGINE_CHUNKED_PREFILL), decode, segment "
+                                                     "polling, token read-back"}
 
 
-def load_traffic(name="gemm_traffic.json"):
+def load_traffic(name):
     p = os.path.join(ROOT, "profiles", name)
     if os.path.exists(p):
         with open(p) as f:
@@ -513,18 +617,38 @@ def load_traffic(name="gemm_traffic.json"):
     return None
 
 
+# ------------------------------------------------------------------ self-launch of N ranks
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without torchrun: start N copies of this command as ranks 0..N-1 (one GPU
+    each; 127.0.0.1 rendezvous) and return the worst exit code.  Rank 0's stdout is ours."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    return max(p.wait() for p in procs)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=64)
+    ap.add_argument("--workload", default="validation", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="total batch over all ranks (default: the config's)")
+    ap.add_argument("--prefix", type=int, default=None, help="synthetic KV prefix tokens per request")
     ap.add_argument("--scan-off", action="store_true", help="trigger scan disabled (overhead A/B)")
-    ap.add_argument("--prefix-min", type=int, default=128, help="synthetic KV prefix: min tokens")
-    ap.add_argument("--prefix-spread", type=int, default=400, help="synthetic KV prefix: + U(0, spread)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-sample", type=int, default=4, help="requests per oracle step (both arms)")
+    ap.add_argument("--no-latency", action="store_true", help="skip the partial-vs-sequential latency A/B")
+    ap.add_argument("--latency-reps", type=int, default=3)
     ap.add_argument("--latency-only", default="", help="comma list of workloads: run only the latency A/B")
     ap.add_argument("--latency-batch", type=int, default=0, help="override every workload's batch")
     ap.add_argument("--latency-inflight", type=int, default=0,
@@ -534,6 +658,16 @@ def main():
     ap.add_argument("--fig6", action="store_true", help="NEXT-4: Fig. 6 tool/decode ratio sweep on the engine")
     ap.add_argument("--fig6-batch", type=int, default=16)
     args = ap.parse_args()
+    if args.steps < 1:
+        ap.error("--steps must be >= 1")
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.gpus > 1:
+        # let the driver see the communicator size; NCCL's log goes to stderr, not the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.fig6:
         print(json.dumps({"fig6": run_fig6(args.fig6_batch, verbose=True)}), flush=True)
         return
@@ -547,66 +681,130 @@ def main():
                                                  flags=fl), "chunked_prefill": bool(args.chunked_prefill)}),
               flush=True)
         return
-    if args.warmup < 3:
-        args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)
 
 
-
 # ------------------------------------------------------------------ latency: partial vs sequential
-def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flags=0):
+LAT_PREFIX = {"codegen": 128, "codegen_fence": 128, "search": 256, "search_call": 256, "planning": 512, "validation": 1792}
+LAT_TOKENS = {"codegen": 440, "codegen_fence": 460, "search": 560, "search_call": 560, "planning": 400, "validation": 320}
+LAT_BATCH = {"codegen": 64, "codegen_fence": 64, "search": 128, "search_call": 128, "planning": 256, "validation": 512}
+AB_WORKLOADS = ("codegen", "validation")
+
+
+def latency_pages(router, workloads=AB_WORKLOADS):
+    """KV pages the in-line latency A/B needs on this rank (its share of each workload)."""
+    return max(router.share(LAT_BATCH[w]) * ((LAT_PREFIX[w] + LAT_TOKENS[w] + 31) // 16 + 1) for w in workloads)
+
+
+def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flags=0, dm=None, indices=None,
+                reps=1):
     """Request completion latency with tool partial execution vs sequential tool execution on
-    the four workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool
-    costs in both modes (the baseline is the same code with partial execution
-    disabled).  Returns {workload: {...}}."""
+    the workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool costs
+    in both modes (the baseline is the same code with partial execution
+    disabled).  `indices(w)`: the global request indices this rank serves (router).  Each
+    (workload, mode) runs `reps` times, modes interleaved.  Returns {workload: {...}}."""
     from inputs.configs import MISTRAL_7B
     from inputs.tool_workloads import TOOLS, build
+    from inputs.vocab import synthetic_vocab
     from paper_2406_00059_b200 import capi
     from paper_2406_00059_b200.engine import DeviceModel, Engine
-    import numpy as np
     from paper_2406_00059_b200.runtime import Runtime, summarize
-    prefixes = {"codegen": 128, "codegen_fence": 128, "search": 256, "search_call": 256, "planning": 512, "validation": 1792}
-    max_tokens = {"codegen": 440, "codegen_fence": 460, "search": 560, "search_call": 560, "planning": 400, "validation": 320}
-    pages_per = {w: (prefixes[w] + max_tokens[w] + 31) // 16 + 1 for w in workloads}
-    slots = {w: (inflight or batches[w]) for w in workloads}
+    import numpy as np
+    idx = {w: (list(range(batches[w])) if indices is None else indices(w)) for w in workloads}
+    pages_per = {w: (LAT_PREFIX[w] + LAT_TOKENS[w] + 31) // 16 + 1 for w in workloads}
+    slots = {w: (inflight or len(idx[w])) for w in workloads}
     need = max(slots[w] * pages_per[w] for w in workloads) + 64
-    dm = DeviceModel(MISTRAL_7B, "bf16", need, seed=1002, device=device)
+    own = dm is None
+    if own:
+        dm = DeviceModel(MISTRAL_7B, "bf16", need, seed=1002, device=device)
     Bmax = max(slots[w] for w in workloads)
-    from inputs.vocab import synthetic_vocab
     eng = Engine(dm, synthetic_vocab(32000), max_slots=Bmax, max_pages_per_slot=max(pages_per.values()) + 2,
                  device=device, flags=flags)
     tool_ids = {name: eng.register_tool(name, getattr(capi, kind), delims) for name, (kind, delims) in TOOLS.items()}
     out = {}
     for w in workloads:
-        res = {}
-        for mode, label in ((capi.MODE_PARTIAL, "partial"), (capi.MODE_SEQUENTIAL, "sequential")):
-            _, specs = build(w, batches[w], tool_ids)
-            rt = Runtime(eng, mode)
-            t0 = time.perf_counter()
-            logs = rt.run(specs, max_inflight=inflight)
-            res[label] = summarize(logs, mode)
-            res[label]["steps"] = rt.steps
-            if inflight:
-                # abort-and-refill (NEXT-3): makespan of the whole queue through `inflight` slots
-                span = max(lg.t_done for lg in logs) - t0
-                res[label].update(makespan_s=span, requests_per_s=len(logs) / span, slots=inflight,
-                                  queue_latency_mean_ms=float(np.mean([lg.t_done - t0 for lg in logs])) * 1e3)
-            if verbose:
-                print(w, label, res[label], flush=True)
-        p, s_ = res["partial"]["mean_ms"], res["sequential"]["mean_ms"]
-        res["improvement"] = s_ / p - 1.0        # the paper's metric, PAPER.md:171
-        res["reduction"] = 1.0 - p / s_           # the north star's wording
-        if "detection_ms_mean" in res["partial"]:
-            d_p, d_s = res["partial"]["detection_ms_mean"], res["sequential"]["detection_ms_mean"]
-            res["detection_speedup"] = d_s / d_p - 1.0  # PAPER.md:203 reports 376.4%
-        res["batch"] = batches[w]
+        res = {"partial": [], "sequential": []}
+        for rep in range(reps):
+            for mode, label in ((capi.MODE_PARTIAL, "partial"), (capi.MODE_SEQUENTIAL, "sequential")):
+                _, specs = build(w, batches[w], tool_ids, indices=idx[w])
+                rt = Runtime(eng, mode)
+                t0 = time.perf_counter()
+                c0 = time.process_time()
+                logs = rt.run(specs, max_inflight=inflight)
+                s = summarize(logs, mode)
+                s["steps"] = rt.steps
+                s["wall_s"] = time.perf_counter() - t0
+                s["host_cpu_s"] = time.process_time() - c0
+                s["poller_cpu_s"] = rt.poller_cpu_s
+                s["dispatch_cpu_s"] = rt.dispatch_cpu_s
+                s["lat_ms"] = [(lg.t_done - lg.t_submit) * 1e3 for lg in logs]
+                if inflight:
+                    span = max(lg.t_done for lg in logs) - t0
+                    s.update(makespan_s=span, requests_per_s=len(logs) / span, slots=inflight)
+                res[label].append(s)
+                if verbose:
+                    print(w, label, rep, {k: v for k, v in s.items() if k != "lat_ms"}, flush=True)
+        p = float(np.mean([r["mean_ms"] for r in res["partial"]]))
+        q = float(np.mean([r["mean_ms"] for r in res["sequential"]]))
+        row = {"batch": batches[w], "reps": reps, "partial_mean_ms": p, "sequential_mean_ms": q,
+               "improvement": q / p - 1.0,   # the paper's metric, PAPER.md:171
+               "reduction": 1.0 - p / q,     # the north star's wording
+               "improvement_per_rep": [b["mean_ms"] / a["mean_ms"] - 1.0 for a, b in zip(res["partial"], res["sequential"])],
+               "runs": res}
+        if "detection_ms_mean" in res["partial"][0]:
+            dp = float(np.mean([r["detection_ms_mean"] for r in res["partial"]]))
+            ds = float(np.mean([r["detection_ms_mean"] for r in res["sequential"]]))
+            row.update(detection_partial_ms=dp, detection_sequential_ms=ds, detection_speedup=ds / dp - 1.0)
         if inflight:
-            res["throughput_gain"] = res["partial"]["requests_per_s"] / res["sequential"]["requests_per_s"] - 1.0
-        out[w] = res
+            row["throughput_gain"] = (np.mean([r["requests_per_s"] for r in res["partial"]]) /
+                                      np.mean([r["requests_per_s"] for r in res["sequential"]]) - 1.0)
+        out[w] = row
     eng.close()
+    if own:
+        del dm
+    return out
+
+
+def run_latency_ab(dm, router, reps=3, device=0):
+    """The latency half of the metric in the bench line: codegen (configs[1]) and validation
+    (configs[4]), partial vs sequential, `reps` repetitions each, this rank serving its router
+    share; per-request latencies are gathered over the ranks.  Host CPU: process CPU seconds
+    per mode, the poller thread's CPU and the time spent dispatching records (the paper's CPU
+    overhead figure is 0.6% extra cycles)."""
+    import numpy as np
+    res = run_latency(list(AB_WORKLOADS), LAT_BATCH, device=device, dm=dm, reps=reps,
+                      indices=lambda w: router.mine(LAT_BATCH[w]))
+    out = {}
+    for w, row in res.items():
+        per_rank = gather_objects({m: [r["lat_ms"] for r in row["runs"][m]] for m in ("partial", "sequential")})
+        lat = {m: [sum((pr[m][i] for pr in per_rank), []) for i in range(reps)] for m in ("partial", "sequential")}
+        means = {m: [float(np.mean(x)) for x in lat[m]] for m in lat}
+        allv = {m: np.array(sum(lat[m], [])) for m in lat}
+        p, q = float(np.mean(means["partial"])), float(np.mean(means["sequential"]))
+        cpu = {m: float(np.mean([r["host_cpu_s"] for r in row["runs"][m]])) for m in ("partial", "sequential")}
+        ent = {"requests": len(lat["partial"][0]), "reps": reps,
+               "partial": {"mean_ms": p, "std_ms": float(allv["partial"].std()),
+                           "p50_ms": float(np.percentile(allv["partial"], 50)),
+                           "p95_ms": float(np.percentile(allv["partial"], 95))},
+               "sequential": {"mean_ms": q, "std_ms": float(allv["sequential"].std()),
+                              "p50_ms": float(np.percentile(allv["sequential"], 50)),
+                              "p95_ms": float(np.percentile(allv["sequential"], 95))},
+               "improvement": q / p - 1.0, "reduction": 1.0 - p / q,
+               "improvement_per_rep": [b / a - 1.0 for a, b in zip(means["partial"], means["sequential"])],
+               "host_cpu_s": cpu, "host_cpu_extra_partial": cpu["partial"] / cpu["sequential"] - 1.0,
+               "dispatch_cpu_s_partial": float(np.mean([r["dispatch_cpu_s"] for r in row["runs"]["partial"]])),
+               "poller_cpu_s_partial": float(np.mean([r["poller_cpu_s"] for r in row["runs"]["partial"]])),
+               "wall_s_partial": float(np.mean([r["wall_s"] for r in row["runs"]["partial"]]))}
+        if "detection_partial_ms" in row:
+            ent.update(detection_partial_ms=row["detection_partial_ms"],
+                       detection_sequential_ms=row["detection_sequential_ms"],
+                       detection_speedup=row["detection_speedup"])
+        out[w] = ent
+    out["protocol"] = ("all requests submitted at t=0; identical seeded streams and tool costs in both modes; "
+                       "modes interleaved per repetition; latency = submit -> completion on the host clock")
     return out
 
 

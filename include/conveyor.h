@@ -230,6 +230,15 @@ typedef struct {
     const int32_t* forced;
     uint32_t forced_len;
     uint32_t reserve_tokens; /* extra KV tokens to reserve for later observation rounds */
+    /* Multi-tool routing (NEXT-2, R24): a SET of region tools (FENCE and / or CALL
+     * kinds, ids < 64) instead of one tool.  Outside a region every line is matched against
+     * each tool's open marker ("```" TAG "\n" / "@call " TAG " ") and the marker that appears
+     * selects the tool: its region's records carry its id ("the indicators for the start and
+     * end of the tool"; "identifies the function name of the tool").
+     * Lines outside a region are cut at the smallest max_segment_bytes of the set, which must
+     * be >= every marker of the set.  tool_id must then be -1 or a member.  NULL / 0: one tool. */
+    const int32_t* tool_set;
+    uint32_t n_tool_set;
 } cvy_request_desc;
 cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t* req_id);
 
@@ -257,7 +266,10 @@ typedef struct {
     uint32_t step, token_index;
     uint32_t byte_offset, byte_len;
     uint16_t delim_id, flags;  /* delim_id: LITERAL index / JSON 0=',' 1=close / NONE  */
-    uint32_t slot;             /* engine slot that produced the record (diagnostic)   */
+    uint16_t slot;             /* engine slot that produced the record (diagnostic)   */
+    int16_t tool;              /* tool the record is for: the request's tool, or for a tool
+                                  set (cvy_request_desc.tool_set) the tool whose region the
+                                  record belongs to; FINAL outside a region: -1           */
 } cvy_segment;
 
 /* Exactly one consumer thread.  Copies up to cap records (and their bytes, concatenated
@@ -312,6 +324,21 @@ typedef struct {
 } cvy_kernel_time;
 cvy_status cvy_set_kernel_timing(cvy_engine* e, int32_t on);
 cvy_status cvy_kernel_times(cvy_engine* e, cvy_kernel_time* out, uint32_t cap, uint32_t* n);
+
+/* In-graph kernel spans (measurement only).  When on, subsequent steps run a variant of the
+ * production step graph -- same kernels, same launch order, programmatic dependent launch kept --
+ * in which every launch records, with %globaltimer, the earliest moment one of its CTAs passed
+ * its grid-dependency wait (t0) and the latest CTA exit (t1).  Consecutive kernels of one chain
+ * therefore have disjoint spans, and sum(t1 - t0) of a kind is its share of the step's device
+ * time.  cvy_kernel_spans returns the spans of the most recently completed span-recording step
+ * (kind as in cvy_kernel_time; chain 1 = the second half-batch chain of the batch-split overlap,
+ * else 0).  Errors: E_STATE without a graph path or before a recorded step. */
+typedef struct {
+    int32_t kind, layer, chain;
+    uint64_t t0_ns, t1_ns;
+} cvy_kernel_span;
+cvy_status cvy_set_kernel_spans(cvy_engine* e, int32_t on);
+cvy_status cvy_kernel_spans(cvy_engine* e, cvy_kernel_span* out, uint32_t cap, uint32_t* n);
 
 /* Stream the engine launches on (cudaStream_t as void*), for external event timing. */
 void* cvy_stream(cvy_engine* e);

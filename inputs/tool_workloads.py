@@ -126,13 +126,14 @@ def _validation_plan():
     return plan
 
 
-def build(workload: str, B: int, tool_ids: dict, seed: int = 2000):
-    """Returns (vocab, [RequestSpec]) for one workload shape."""
+def build(workload: str, B: int, tool_ids: dict, seed: int = 2000, indices=None):
+    """Returns (vocab, [RequestSpec]) for one workload shape: requests 0..B-1 of the config's
+    total batch, or only the global indices given (a rank's share under the router)."""
     from paper_2406_00059_b200.runtime import RequestSpec, Round
     vocab = synthetic_vocab(32000)
     tok = Tokenizer(vocab)
     specs = []
-    for b in range(B):
+    for b in (range(B) if indices is None else indices):
         rng = random.Random(seed * 100003 + b)
         if workload == "codegen":
             text = codegen_script(rng, 40)

@@ -318,6 +318,109 @@ def call_records(tag: bytes, max_seg: int, S: bytes):
     return recs, c
 
 
+def region_records(tools, S: bytes):
+    """Multi-tool region grammars (NEXT-2; reading R24): one request holds a SET of
+    region tools -- FENCE tools ("the markdown code block syntax ```python and ``` as the
+    indicators for the start and end of the tool") and CALL tools ("when Conveyor
+    identifies the function name of the tool") -- and the open marker that
+    appears selects the tool.  tools: [(tool_id, kind, tag, max_seg)] with kind FENCE or CALL.
+    Step by step, byte by byte with a cursor c (start of the current line unit or piece):
+      outside a region (line_ok: the current line started at c and is neither a continuation of
+      a cut nor the rest of a line after a CALL close; M = min max_seg over the set):
+        '\n': if line_ok and S[c:p] == b"```" + tag + b"\n" of a FENCE tool -> OPEN record of
+              that tool, its region opens; c = p, line_ok = True;
+        else if line_ok and S[c:p] == b"@call " + tag + b" " of a CALL tool -> OPEN record of
+              that tool, its region opens with the JSON automaton at its start state; c = p;
+        else if p - c == M: c = p, line_ok = False;
+      inside a FENCE region (its max_seg; cont: the unit continues a cut line):
+        '\n': the unit not cont and equal to b"```\n" -> CLOSE record, region closes;
+              any other unit -> piece record (delim 0); c = p, cont = False;
+        else if p - c == max_seg -> piece record with OVERFLOW (delim NONE); c = p, cont = True;
+      inside a CALL region (its max_seg): the JSON automaton of JSON_MEMBER (R10-R11): ',' at
+        depth 1 -> piece record (delim 0); the bracket returning depth to 0 -> CLOSE record
+        (delim 1), the region closes and the rest of that line is not at a line start; a piece
+        reaching max_seg bytes -> OVERFLOW record (delim NONE).
+    The lowest tool id wins if two markers match at one byte (impossible for distinct tags).
+    With one tool this is fence_records / call_records.  FINAL = S[c, |S|), carrying the tool of
+    the region open at the end (-1 outside).
+    Returns (records [(start, end, delim_id, flags, tool_id)], c, tool of the FINAL)."""
+    tools = sorted(tools)
+    M = min(t[3] for t in tools)
+    fence_m = {t[0]: b"```" + t[2] + b"\n" for t in tools if t[1] == PARSER_FENCE}
+    call_m = {t[0]: b"@call " + t[2] + b" " for t in tools if t[1] == PARSER_CALL}
+    kind = {t[0]: t[1] for t in tools}
+    mseg = {t[0]: t[3] for t in tools}
+    recs = []
+    region = None
+    c = 0
+    line_ok = True
+    cont = False
+    depth = in_str = esc = 0
+    for i in range(len(S)):
+        p = i + 1
+        b = S[i]
+        if region is None:
+            if b == 0x0A:
+                hit = [t for t, m in fence_m.items() if line_ok and S[c:p] == m]
+                if hit:
+                    recs.append((c, p, 0, FLAG_OPEN, hit[0]))
+                    region, cont = hit[0], False
+                c, line_ok = p, True
+                continue
+            hit = [t for t, m in call_m.items() if line_ok and S[c:p] == m]
+            if hit:
+                recs.append((c, p, 0, FLAG_OPEN, hit[0]))
+                region, c = hit[0], p
+                depth = in_str = esc = 0
+            elif p - c == M:
+                c, line_ok = p, False
+            continue
+        if kind[region] == PARSER_FENCE:
+            if b == 0x0A:
+                if not cont and S[c:p] == b"```\n":
+                    recs.append((c, p, 0, FLAG_CLOSE, region))
+                    region, line_ok = None, True
+                else:
+                    recs.append((c, p, 0, 0, region))
+                c, cont = p, False
+            elif p - c == mseg[region]:
+                recs.append((c, p, DELIM_NONE, FLAG_OVERFLOW, region))
+                c, cont = p, True
+            continue
+        hit = -1
+        if in_str:
+            if esc:
+                esc = 0
+            elif b == 0x5C:
+                esc = 1
+            elif b == 0x22:
+                in_str = 0
+        elif depth == 0:
+            if b in (0x7B, 0x5B):
+                depth = 1
+        else:
+            if b == 0x22:
+                in_str = 1
+            elif b in (0x7B, 0x5B):
+                depth = min(depth + 1, 127)
+            elif b in (0x7D, 0x5D):
+                depth -= 1
+                if depth == 0:
+                    hit = 1
+            elif b == 0x2C and depth == 1:
+                hit = 0
+        if hit == 1:
+            recs.append((c, p, 1, FLAG_CLOSE, region))
+            region, c, line_ok = None, p, False
+        elif hit == 0:
+            recs.append((c, p, 0, 0, region))
+            c = p
+        elif p - c == mseg[region]:
+            recs.append((c, p, DELIM_NONE, FLAG_OVERFLOW, region))
+            c = p
+    return recs, c, (-1 if region is None else region)
+
+
 def plan_records(max_seg: int, S: bytes):
     r"""PLAN line grammar (NEXT-2; reading R23).  SPEC.md:81: "each newline-
     terminated line matching `#E<digits> = <Name>[<args>]` is one ToolData stage piece

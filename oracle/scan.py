@@ -18,7 +18,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from . import (DELIM_NONE, FLAG_CANCELLED, FLAG_FINAL, PARSER_CALL, PARSER_FENCE, PARSER_PLAN, call_records,
-               fence_records, plan_records, segment)
+               fence_records, plan_records, region_records, segment)
 
 NO_TOKEN = 0xFFFFFFFF
 
@@ -33,6 +33,7 @@ class Record:
     delim_id: int
     flags: int
     data: bytes
+    tool: int = -1
 
 
 def round_length(tokens, eos: int, max_new: int) -> int:
@@ -46,9 +47,12 @@ def round_length(tokens, eos: int, max_new: int) -> int:
 
 
 def round_records(tokens, vocab_bytes, kind: int, delims: list[bytes], max_seg: int,
-                  round_idx: int = 0, seq_start: int = 0, cancelled: bool = False):
+                  round_idx: int = 0, seq_start: int = 0, cancelled: bool = False, tool_id: int = -1,
+                  region_tools=None):
     """Records for one round whose generated ids are exactly `tokens` (already cut at
-    the round end).  Returns (records, stream_bytes)."""
+    the round end).  tool_id: the request's tool (each record's `tool`); region_tools: a
+    multi-tool set [(tool_id, kind, tag, max_seg)] of FENCE / CALL tools (R24; kind and
+    delims are then unused).  Returns (records, stream_bytes)."""
     pieces = [vocab_bytes[t] for t in tokens]
     S = b"".join(pieces)
     ends = []
@@ -59,27 +63,38 @@ def round_records(tokens, vocab_bytes, kind: int, delims: list[bytes], max_seg: 
     recs = []
     c_prev = 0
     seq = seq_start
-    if kind in (PARSER_FENCE, PARSER_CALL, PARSER_PLAN):
-        # region grammars: records need not tile S (text outside a region is not tool input)
+    fin_tool = tool_id
+    if region_tools is not None:
+        rr, c_prev, fin_tool = region_records(region_tools, S)
+        for (a, c, did, fl, t) in rr:
+            t1 = next(t_ for t_, e in enumerate(ends) if e >= c)
+            recs.append(Record(round_idx, seq, t1, a, c - a, did, fl, S[a:c], t))
+            seq += 1
+        cuts = []
+    elif kind in (PARSER_FENCE, PARSER_CALL, PARSER_PLAN):
+        # region grammars: records need not tile S (text outside a region is not tool input);
+        # a single FENCE / CALL tool is the set of one (R24), so FINAL carries -1 outside it
         if kind == PARSER_FENCE:
             fr, c_prev = fence_records(delims[0], max_seg, S)
         elif kind == PARSER_CALL:
             fr, c_prev = call_records(delims[0], max_seg, S)
         else:
             fr, c_prev = plan_records(max_seg, S)
+        if kind != PARSER_PLAN:
+            fin_tool = region_records([(tool_id, kind, delims[0], max_seg)], S)[2] if tool_id >= 0 else -1
         for (a, c, did, fl) in fr:
             t1 = next(t for t, e in enumerate(ends) if e >= c)
-            recs.append(Record(round_idx, seq, t1, a, c - a, did, fl, S[a:c]))
+            recs.append(Record(round_idx, seq, t1, a, c - a, did, fl, S[a:c], tool_id))
             seq += 1
         cuts = []
     else:
         cuts = segment(kind, delims, max_seg, S)
     for (c, did, fl) in cuts:
         t1 = next(t for t, e in enumerate(ends) if e >= c)  # min{t : e_t >= c} - 1 (0-based)
-        recs.append(Record(round_idx, seq, t1, c_prev, c - c_prev, did, fl, S[c_prev:c]))
+        recs.append(Record(round_idx, seq, t1, c_prev, c - c_prev, did, fl, S[c_prev:c], tool_id))
         seq += 1
         c_prev = c
     last = len(tokens) - 1 if tokens else NO_TOKEN
     recs.append(Record(round_idx, seq, last, c_prev, len(S) - c_prev, DELIM_NONE,
-                       FLAG_FINAL | (FLAG_CANCELLED if cancelled else 0), S[c_prev:]))
+                       FLAG_FINAL | (FLAG_CANCELLED if cancelled else 0), S[c_prev:], fin_tool))
     return recs, S

@@ -60,7 +60,8 @@ class ToolDesc(ctypes.Structure):
 class RequestDesc(ctypes.Structure):
     _fields_ = [("tool_id", c_i32), ("mode", c_i32), ("prompt", ctypes.POINTER(c_i32)), ("prompt_len", c_u32),
                 ("synth_prefix_len", c_u32), ("synth_seed", c_u64), ("max_new_tokens", c_u32),
-                ("forced", ctypes.POINTER(c_i32)), ("forced_len", c_u32), ("reserve_tokens", c_u32)]
+                ("forced", ctypes.POINTER(c_i32)), ("forced_len", c_u32), ("reserve_tokens", c_u32),
+                ("tool_set", ctypes.POINTER(c_i32)), ("n_tool_set", c_u32)]
 
 
 class StepInfo(ctypes.Structure):
@@ -71,11 +72,15 @@ class StepInfo(ctypes.Structure):
 class Segment(ctypes.Structure):
     _fields_ = [("req_id", c_u64), ("round", c_u32), ("seq", c_u32), ("step", c_u32), ("token_index", c_u32),
                 ("byte_offset", c_u32), ("byte_len", c_u32), ("delim_id", c_u16), ("flags", c_u16),
-                ("slot", c_u32)]
+                ("slot", c_u16), ("tool", ctypes.c_int16)]
 
 
 class KernelTime(ctypes.Structure):
     _fields_ = [("kind", c_i32), ("layer", c_i32), ("ms", c_f32)]
+
+
+class KernelSpan(ctypes.Structure):
+    _fields_ = [("kind", c_i32), ("layer", c_i32), ("chain", c_i32), ("t0_ns", c_u64), ("t1_ns", c_u64)]
 
 
 KERNEL_KINDS = {0: "embed", 1: "gemm_qkv", 2: "attention", 3: "attention_merge", 4: "gemm_o", 5: "gemm_gate_up",
@@ -115,6 +120,8 @@ PROTOTYPES = {
     "cvy_stream": (c_vp, [c_vp]),
     "cvy_set_kernel_timing": (c_i32, [c_vp, c_i32]),
     "cvy_kernel_times": (c_i32, [c_vp, ctypes.POINTER(KernelTime), c_u32, ctypes.POINTER(c_u32)]),
+    "cvy_set_kernel_spans": (c_i32, [c_vp, c_i32]),
+    "cvy_kernel_spans": (c_i32, [c_vp, ctypes.POINTER(KernelSpan), c_u32, ctypes.POINTER(c_u32)]),
     "cvy_stats_allgather": (c_i32, [ctypes.POINTER(c_vp), c_i32, ctypes.POINTER(c_u64)]),
     "cvy_debug_buffer": (c_i32, [c_vp, c_i32, c_vp, c_sz, ctypes.POINTER(c_sz)]),
     "cvy_debug_gemm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f32)]),

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
     }
     __syncthreads();
     pdl_wait();
+    if (threadIdx.x == 0) span_begin(P.spans, P.span_base + layer * 8 + 2);
 
     const int nkeys = row_nkeys(P, b);
     const int nsplit = P.attn_splits;
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
             }
         }
     }
+    if (threadIdx.x == 0) span_end(P.spans, kSpanSlots, P.span_base + layer * 8 + 2);
 }
 
 }  // namespace cvy

@@ -35,6 +35,18 @@ CVY_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_sh
 // ------------------------------------------------------------------ PDL (griddepcontrol)
 CVY_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 CVY_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+CVY_DEV unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// In-graph span of one launch (StepParams::spans): earliest post-wait start, latest exit.
+CVY_DEV void span_begin(unsigned long long* spans, int idx) {
+    if (spans && idx >= 0) atomicMin(spans + idx, globaltimer_ns());
+}
+CVY_DEV void span_end(unsigned long long* spans, int slots, int idx) {
+    if (spans && idx >= 0) atomicMax(spans + slots + idx, globaltimer_ns());
+}
 
 // ------------------------------------------------------------------ mbarrier
 CVY_DEV void mbar_init(uint64_t* bar, uint32_t count) {

@@ -245,6 +245,7 @@ struct Bucket {
     std::vector<GemmPlan> plans;  // per launch in order
     cudaGraphExec_t graph = nullptr;
     cudaGraphExec_t graph_timed = nullptr;  // event pair around every kernel, no PDL
+    cudaGraphExec_t graph_spans = nullptr;  // the production graph + in-graph kernel spans
     std::vector<cudaEvent_t> kev;
     std::vector<std::pair<int, int>> kinfo;  // (kind, layer) per launch
     uint32_t launches = 0;
@@ -378,6 +379,10 @@ struct cvy_engine {
     unsigned long long* d_trace = nullptr;  // test hook: GEMM CTA timestamps of one layer
     int trace_layer = -1;
     bool timing = false;        // launch the timed graph variant
+    bool spans_on = false;      // launch the span-recording graph variant
+    bool capturing_spans = false;
+    unsigned long long* d_spans = nullptr;  // [2][kSpanSlots] (StepParams::spans)
+    Bucket* last_spans = nullptr;
     bool capturing_timed = false;
     Bucket* last_timed = nullptr;
 };
@@ -667,6 +672,7 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     const size_t acc_cols = (ec->flags & CVY_ENGINE_CHUNKED_PREFILL) ? std::max(Bmax, kPrefillRows) : (size_t)Bmax;
     ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * acc_cols);
     ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
+    ALLOC(e->d_spans, sizeof(unsigned long long) * 2 * kSpanSlots);
     // batch-split overlap: bf16, buckets of >= 256 slots; CVY_OVERLAP=0 disables
     e->ov_ok = false;  // opt-in: measured slower at C4
     if (const char* v = getenv("CVY_OVERLAP"))
@@ -807,6 +813,7 @@ void cvy_engine_destroy(cvy_engine* e) {
     for (auto& kv : e->buckets) {
         if (kv.second.graph) cudaGraphExecDestroy(kv.second.graph);
         if (kv.second.graph_timed) cudaGraphExecDestroy(kv.second.graph_timed);
+        if (kv.second.graph_spans) cudaGraphExecDestroy(kv.second.graph_spans);
         for (cudaEvent_t ev : kv.second.kev) cudaEventDestroy(ev);
     }
     for (auto& pr : e->inflight) {
@@ -822,7 +829,7 @@ void cvy_engine_destroy(cvy_engine* e) {
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches,
                      e->d_pk_done, e->d_att_cnt, e->d_att_part2, e->d_pk_part, e->d_pk_pflag,
                      e->d_px, e->d_pact, e->d_pq, e->d_po, e->d_ph, e->d_pssq, e->d_pattn_part, e->d_prow,
-                     e->d_gemm_acc2, e->d_tile_cnt2};
+                     e->d_gemm_acc2, e->d_tile_cnt2, e->d_spans};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats, e->h_pk_err};
@@ -935,6 +942,38 @@ cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t
         if (r->forced[i] < 0 || r->forced[i] >= e->m.vocab) return fail(CVY_E_INVAL, "forced token out of range");
     std::lock_guard<std::mutex> lk(e->mu);
     if (r->tool_id < -1 || r->tool_id >= (int)e->tools.size()) return fail(CVY_E_NOTFOUND, "unknown tool id");
+    // region tool set (NEXT-2, R24); a single FENCE / CALL tool is the set of one
+    uint64_t tool_set = 0;
+    int32_t set_max_seg = 0;
+    int32_t tool_primary = r->tool_id;
+    {
+        std::vector<int32_t> ids;
+        if (r->n_tool_set > 0) {
+            if (!r->tool_set || r->n_tool_set > 64) return fail(CVY_E_INVAL, "tool_set: 1..64 tool ids");
+            ids.assign(r->tool_set, r->tool_set + r->n_tool_set);
+        } else if (r->tool_id >= 0 && (e->tools[r->tool_id].kind == CVY_PARSER_FENCE ||
+                                       e->tools[r->tool_id].kind == CVY_PARSER_CALL)) {
+            ids.push_back(r->tool_id);
+        }
+        int32_t max_marker = 0;
+        set_max_seg = 1 << 30;
+        for (int32_t id : ids) {
+            if (id < 0 || id >= (int)e->tools.size() || id >= 64) return fail(CVY_E_NOTFOUND, "tool_set: unknown tool id");
+            const ToolDev& t = e->tools[id];
+            if (t.kind != CVY_PARSER_FENCE && t.kind != CVY_PARSER_CALL)
+                return fail(CVY_E_INVAL, "tool_set: only FENCE and CALL tools select themselves by marker");
+            if (tool_set & (1ull << id)) return fail(CVY_E_INVAL, "tool_set: duplicate tool id");
+            tool_set |= 1ull << id;
+            set_max_seg = std::min(set_max_seg, t.max_seg);
+            max_marker = std::max(max_marker, t.dlen[0]);
+        }
+        if (!ids.empty()) {
+            if (set_max_seg < max_marker) return fail(CVY_E_INVAL, "tool_set: a marker is longer than the smallest max_segment_bytes");
+            if (r->n_tool_set > 0 && r->tool_id >= 0 && !(tool_set & (1ull << r->tool_id)))
+                return fail(CVY_E_INVAL, "tool_id is not a member of tool_set");
+            if (tool_primary < 0) tool_primary = ids[0];
+        }
+    }
     int slot = -1;
     for (int b = 0; b < (int)e->c.max_slots; ++b)
         if (!e->slots[b].used) {
@@ -982,7 +1021,9 @@ cvy_status cvy_submit_request(cvy_engine* e, const cvy_request_desc* r, uint64_t
     p.kind = PATCH_SUBMIT;
     p.slot = slot;
     p.req_id = e->next_req++;
-    p.tool = (e->c.flags & CVY_ENGINE_SCAN_OFF) ? -1 : r->tool_id;
+    p.tool = (e->c.flags & CVY_ENGINE_SCAN_OFF) ? -1 : tool_primary;
+    p.tool_set = (e->c.flags & CVY_ENGINE_SCAN_OFF) ? 0 : tool_set;
+    p.set_max_seg = set_max_seg;
     p.pos = (int32_t)r->synth_prefix_len + (prefill ? (int32_t)r->prompt_len - 1 : 0);
     p.cur_tok = prefill ? r->prompt[r->prompt_len - 1] : r->prompt[0];
     p.in_idx = 0;
@@ -1324,22 +1365,22 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
     std::string why;
     for (int l = 0; l < L; ++l) {
         GemmPlan gp;
-        EpiArgs eq{EPI_QKV, l, Nqkv, nullptr};
+        EpiArgs eq{EPI_QKV, l, Nqkv, nullptr, nullptr, 1};
         if (!plan_gemm(e, bk, e->w.wqkv, Nqkv, d, l, L * Nqkv, e->d_act, eq, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
-        EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d};
+        EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d, nullptr, 4};
         if (!plan_gemm(e, bk, e->w.wo, d, H * hd, l, L * d, e->d_o, eo, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
-        EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr};
+        EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr, nullptr, 5};
         if (!plan_gemm(e, bk, e->w.wgu, 2 * dff, d, l, L * 2 * dff, e->d_act, eg, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
-        EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm};
+        EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm, nullptr, 6};
         if (!plan_gemm(e, bk, e->w.wd, d, dff, l, L * d, e->d_h, ed, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
     }
     {
         GemmPlan gp;
-        EpiArgs el{EPI_LMHEAD, 0, V, nullptr};
+        EpiArgs el{EPI_LMHEAD, 0, V, nullptr, nullptr, 7};
         if (!plan_gemm(e, bk, e->w.lm_head, V, d, 0, V, e->d_act, el, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
     }
@@ -1369,6 +1410,7 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
             Q.dbg_logits = bk.P.dbg_logits ? bk.P.dbg_logits + r0 * V : nullptr;
             Q.attn_splits = 1;
             Q.attn_part = bk.P.attn_part + r0 * Hkv * (m.n_heads / Hkv) * (hd + 2);
+            Q.span_base = k * (kSpanSlots / 2);
             bk.PH[k] = Q;
             PlanOpts po;
             po.Bp = Bh;
@@ -1379,16 +1421,16 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
             const size_t xoff = r0 * e->act_ld * es;
             for (int l = 0; l < L && ok; ++l) {
                 GemmPlan gp;
-                EpiArgs eq{EPI_QKV, l, Nqkv, nullptr};
+                EpiArgs eq{EPI_QKV, l, Nqkv, nullptr, nullptr, 1};
                 ok = ok && plan_gemm(e, bk, e->w.wqkv, Nqkv, d, l, L * Nqkv, (uint8_t*)e->d_act + xoff, eq, &gp, &why, 0, &po);
                 bk.hplans[k].push_back(gp);
-                EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d};
+                EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d, nullptr, 4};
                 ok = ok && plan_gemm(e, bk, e->w.wo, d, H * hd, l, L * d, (uint8_t*)e->d_o + xoff, eo, &gp, &why, 0, &po);
                 bk.hplans[k].push_back(gp);
-                EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr};
+                EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr, nullptr, 5};
                 ok = ok && plan_gemm(e, bk, e->w.wgu, 2 * dff, d, l, L * 2 * dff, (uint8_t*)e->d_act + xoff, eg, &gp, &why, 0, &po);
                 bk.hplans[k].push_back(gp);
-                EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm};
+                EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm, nullptr, 6};
                 ok = ok && plan_gemm(e, bk, e->w.wd, d, dff, l, L * d, (uint8_t*)e->d_h + xoff, ed, &gp, &why, 0, &po);
                 bk.hplans[k].push_back(gp);
             }
@@ -1739,6 +1781,13 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
     KTimer kt(e, bk);
     const int Bp = bk.Bp;
     const cvy_model_config& m = e->m;
+    if (e->capturing_spans) {
+        if ((st = check_cuda(e, cudaMemsetAsync(e->d_spans, 0xFF, sizeof(unsigned long long) * kSpanSlots, e->stream),
+                             "span reset")) != CVY_OK ||
+            (st = check_cuda(e, cudaMemsetAsync(e->d_spans + kSpanSlots, 0, sizeof(unsigned long long) * kSpanSlots,
+                                                e->stream), "span reset")) != CVY_OK)
+            return st;
+    }
     {
         void* args[] = {&bk.P};
         const void* f = e->bf16 ? (const void*)embed_kernel<__nv_bfloat16> : (const void*)embed_kernel<float>;
@@ -1952,15 +2001,23 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
             return st;
         }
     } else {
-        cudaGraphExec_t* target = e->timing ? &bk->graph_timed : &bk->graph;
+        cudaGraphExec_t* target = e->timing ? &bk->graph_timed : e->spans_on ? &bk->graph_spans : &bk->graph;
         if (!*target) {
             cudaGraph_t g;
             e->capturing_timed = e->timing;
+            e->capturing_spans = !e->timing && e->spans_on;
+            if (e->capturing_spans) {  // kernel parameters are copied at capture: spans only in this variant
+                bk->P.spans = e->d_spans;
+                for (auto& ph : bk->PH) ph.spans = e->d_spans;
+            }
             st = check_cuda(e, cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
             if (st != CVY_OK) return st;
             cvy_status st2 = enqueue_step_kernels(e, *bk);
             cudaError_t ce = cudaStreamEndCapture(e->stream, &g);
             e->capturing_timed = false;
+            e->capturing_spans = false;
+            bk->P.spans = nullptr;
+            for (auto& ph : bk->PH) ph.spans = nullptr;
             if (st2 != CVY_OK) {
                 e->dead = true;
                 return st2;
@@ -1971,6 +2028,7 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
         }
         if ((st = check_cuda(e, cudaGraphLaunch(*target, e->stream), "graph launch")) != CVY_OK) return st;
         if (e->timing) e->last_timed = bk;
+        else if (e->spans_on) e->last_spans = bk;
     }
     cudaEventRecord(ev.second, e->stream);
     if ((st = check_cuda(e, cudaGetLastError(), "step launch")) != CVY_OK) return st;
@@ -2106,6 +2164,38 @@ cvy_status cvy_set_kernel_timing(cvy_engine* e, int32_t on) {
     if (!e) return fail(CVY_E_INVAL, "null engine");
     if (e->c.flags & CVY_ENGINE_NO_GRAPH) return fail(CVY_E_STATE, "kernel timing needs the graph path");
     e->timing = on != 0;
+    return CVY_OK;
+}
+
+cvy_status cvy_set_kernel_spans(cvy_engine* e, int32_t on) {
+    if (!e) return fail(CVY_E_INVAL, "null engine");
+    if (e->c.flags & CVY_ENGINE_NO_GRAPH) return fail(CVY_E_STATE, "kernel spans need the graph path");
+    e->spans_on = on != 0;
+    return CVY_OK;
+}
+
+cvy_status cvy_kernel_spans(cvy_engine* e, cvy_kernel_span* out, uint32_t cap, uint32_t* n) {
+    if (!e || !out || !n) return fail(CVY_E_INVAL, "null argument");
+    *n = 0;
+    if (!e->last_spans) return fail(CVY_E_STATE, "no span-recording step has run");
+    cvy_status st = cvy_sync(e);
+    if (st != CVY_OK) return st;
+    std::vector<unsigned long long> h(2 * (size_t)kSpanSlots);
+    if ((st = check_cuda(e, cudaMemcpy(h.data(), e->d_spans, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost),
+                         "span copy")) != CVY_OK)
+        return st;
+    uint32_t k = 0;
+    for (int i = 0; i < kSpanSlots && k < cap; ++i) {
+        if (h[i] == ~0ull || h[kSpanSlots + i] == 0) continue;
+        const int half = kSpanSlots / 2;
+        out[k].chain = i / half;
+        out[k].layer = (i % half) / 8;
+        out[k].kind = (i % half) % 8;
+        out[k].t0_ns = h[i];
+        out[k].t1_ns = h[kSpanSlots + i];
+        ++k;
+    }
+    *n = k;
     return CVY_OK;
 }
 

@@ -313,17 +313,115 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
 struct ScanOut {
     uint32_t off[kMaxRecPerSlot], len[kMaxRecPerSlot], tok[kMaxRecPerSlot];
     uint16_t did[kMaxRecPerSlot], flags[kMaxRecPerSlot];
+    int16_t tool[kMaxRecPerSlot];
     int n;
 };
 
-CVY_DEV void scan_emit(ScanOut& so, uint32_t off, uint32_t len, uint32_t tok, uint16_t did, uint16_t fl) {
+CVY_DEV void scan_emit(ScanOut& so, uint32_t off, uint32_t len, uint32_t tok, uint16_t did, uint16_t fl, int tool) {
     if (so.n < kMaxRecPerSlot) {
         so.off[so.n] = off;
         so.len[so.n] = len;
         so.tok[so.n] = tok;
         so.did[so.n] = did;
         so.flags[so.n] = fl;
+        so.tool[so.n] = (int16_t)tool;
         so.n++;
+    }
+}
+
+// One byte through the JSON automaton (R10-R11): returns 0 for a ',' at depth 1 (member
+// parsers only), 1 for the bracket returning depth to 0, -1 otherwise.
+CVY_DEV int json_step(SlotDev& s, uint8_t b, bool member) {
+    int hit = -1;
+    if (s.in_str) {
+        if (s.esc) s.esc = 0;
+        else if (b == '\\') s.esc = 1;
+        else if (b == '"') s.in_str = 0;
+    } else if (s.depth == 0) {
+        if (b == '{' || b == '[') s.depth = 1;
+    } else {
+        if (b == '"') s.in_str = 1;
+        else if (b == '{' || b == '[') { if (s.depth < 127) s.depth += 1; }
+        else if (b == '}' || b == ']') { s.depth -= 1; if (s.depth == 0) hit = 1; }
+        else if (b == ',' && s.depth == 1 && member) hit = 0;
+    }
+    return hit;
+}
+
+// Region tool sets (NEXT-2, R24; a single FENCE or CALL tool is the set of one).
+// Outside a region (region < 0): seg_start = start of the current line unit, win = the tools
+// whose open marker ("```" TAG "\n" / "@call " TAG " ", packed in dpack / dlen[0]) this line no
+// longer matches (all ones: a continuation of a cut line or the rest of a line after a CALL
+// close -- never a marker); the marker that completes opens its tool's region (OPEN record).
+// Inside a FENCE region: line units, esc = 2 not the close marker "```\n", 4 continuation;
+// inside a CALL region: the JSON_MEMBER automaton, its closing bracket ends the region.
+CVY_DEV void scan_byte_set(SlotDev& s, const ToolDev* tools, uint8_t b, uint32_t tok_idx, ScanOut& so) {
+    s.stream_len += 1;
+    const uint32_t p = s.stream_len;
+    const uint32_t since = p - s.seg_start;
+    if (s.region < 0) {
+        const uint32_t k = since - 1;  // index of this byte in the line
+        int opened = -1;
+        uint64_t cand = s.tool_set & ~s.win;
+        while (cand) {
+            const int i = __ffsll((long long)cand) - 1;
+            cand &= cand - 1;
+            const ToolDev& t = tools[i];
+            const uint32_t mlen = (uint32_t)t.dlen[0];
+            if (k >= mlen || b != (uint8_t)(t.dpack[k >> 3] >> (8 * (k & 7)))) {
+                s.win |= 1ull << i;
+                continue;
+            }
+            if (since == mlen && opened < 0) opened = i;  // lowest tool id first
+        }
+        if (opened >= 0) {
+            scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_OPEN, opened);
+            s.seg_start = p;
+            s.region = opened;
+            s.win = 0;
+            s.depth = s.in_str = s.esc = 0;
+        } else if (b == '\n') {
+            s.seg_start = p;
+            s.win = 0;
+        } else if ((int)since == s.set_max_seg) {
+            s.seg_start = p;
+            s.win = ~0ull;
+        }
+        return;
+    }
+    const ToolDev& t = tools[s.region];
+    if (t.kind == CVY_PARSER_FENCE) {
+        const uint32_t k = since - 1;
+        if (k >= 4 || b != (k < 3 ? (uint8_t)'`' : (uint8_t)'\n')) s.esc |= 2;
+        if (b == '\n') {
+            if (!(s.esc & 6) && since == 4) {
+                scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_CLOSE, s.region);
+                s.region = -1;
+                s.win = 0;
+            } else {
+                scan_emit(so, s.seg_start, since, tok_idx, 0, 0, s.region);
+            }
+            s.seg_start = p;
+            s.esc = 0;
+        } else if ((int)since == t.max_seg) {
+            scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW, s.region);
+            s.seg_start = p;
+            s.esc = 4;
+        }
+        return;
+    }
+    const int hit = json_step(s, b, true);
+    if (hit == 1) {
+        scan_emit(so, s.seg_start, since, tok_idx, 1, CVY_SEG_CLOSE, s.region);
+        s.seg_start = p;
+        s.region = -1;
+        s.win = ~0ull;  // the rest of this line is not at a line start
+    } else if (hit == 0) {
+        scan_emit(so, s.seg_start, since, tok_idx, 0, 0, s.region);
+        s.seg_start = p;
+    } else if ((int)since == t.max_seg) {
+        scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW, s.region);
+        s.seg_start = p;
     }
 }
 
@@ -333,42 +431,12 @@ CVY_DEV void scan_byte(SlotDev& s, const ToolDev& t, uint8_t b, uint32_t tok_idx
     const uint32_t p = s.stream_len;
     const uint32_t since = p - s.seg_start;
     int hit = -1;
-    if (t.kind == CVY_PARSER_FENCE) {
-        // region grammar (R21): seg_start = start of the current line unit, depth = inside a
-        // region, esc = mismatch bits (1: not the open marker, 2: not the close marker,
-        // 4: continuation of an overflowed line -- never a marker)
-        const uint32_t k = since - 1;  // index of this byte in the unit
-        const uint32_t olen = (uint32_t)t.dlen[0];
-        if (k >= olen || b != (uint8_t)(t.dpack[k >> 3] >> (8 * (k & 7)))) s.esc |= 1;
-        if (k >= 4 || b != (k < 3 ? (uint8_t)'`' : (uint8_t)'\n')) s.esc |= 2;
-        if (b == '\n') {
-            const bool marker_ok = !(s.esc & 4);
-            if (!s.depth) {
-                if (marker_ok && !(s.esc & 1) && since == olen) {
-                    scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_OPEN);
-                    s.depth = 1;
-                }
-            } else if (marker_ok && !(s.esc & 2) && since == 4) {
-                scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_CLOSE);
-                s.depth = 0;
-            } else {
-                scan_emit(so, s.seg_start, since, tok_idx, 0, 0);
-            }
-            s.seg_start = p;
-            s.esc = 0;
-        } else if ((int)since == t.max_seg) {
-            if (s.depth) scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW);
-            s.seg_start = p;
-            s.esc = 4;
-        }
-        return;
-    }
     if (t.kind == CVY_PARSER_PLAN) {
         // R23: per-line DFA over  #E<digits> = <Name>[<args>]\n  in depth (0 = line start,
         // 9 = last byte ']', 10 = dead: mismatch or continuation of a max_seg cut)
         int st = s.depth;
         if (b == '\n') {
-            if (st == 9) scan_emit(so, s.seg_start, since, tok_idx, 0, 0);
+            if (st == 9) scan_emit(so, s.seg_start, since, tok_idx, 0, 0, s.tool);
             s.seg_start = p;
             st = 0;
         } else {
@@ -394,26 +462,6 @@ CVY_DEV void scan_byte(SlotDev& s, const ToolDev& t, uint8_t b, uint32_t tok_idx
         s.depth = st;
         return;
     }
-    if (t.kind == CVY_PARSER_CALL && !(s.win & 1)) {
-        // R22, outside a call region: win bit 1 = this line can no longer be the marker
-        // (mismatch, continuation of a max_seg cut, or the rest of a line after a close)
-        const uint32_t k = since - 1;
-        const uint32_t mlen = (uint32_t)t.dlen[0];
-        if (k >= mlen || b != (uint8_t)(t.dpack[k >> 3] >> (8 * (k & 7)))) s.win |= 2;
-        if (b == '\n') {
-            s.seg_start = p;
-            s.win = 0;
-        } else if (!(s.win & 2) && since == mlen) {
-            scan_emit(so, s.seg_start, since, tok_idx, 0, CVY_SEG_OPEN);
-            s.seg_start = p;
-            s.win = 1;  // inside; JSON automaton from its start state
-            s.depth = s.in_str = s.esc = 0;
-        } else if ((int)since == t.max_seg) {
-            s.seg_start = p;
-            s.win |= 2;
-        }
-        return;
-    }
     if (t.kind == CVY_PARSER_LITERAL) {
         s.win = (s.win << 8) | b;
         const uint32_t avail = since < 8 ? since : 8;
@@ -424,40 +472,14 @@ CVY_DEV void scan_byte(SlotDev& s, const ToolDev& t, uint8_t b, uint32_t tok_idx
             }
         }
     } else {
-        if (s.in_str) {
-            if (s.esc) s.esc = 0;
-            else if (b == '\\') s.esc = 1;
-            else if (b == '"') s.in_str = 0;
-        } else if (s.depth == 0) {
-            if (b == '{' || b == '[') s.depth = 1;
-        } else {
-            if (b == '"') s.in_str = 1;
-            else if (b == '{' || b == '[') { if (s.depth < 127) s.depth += 1; }
-            else if (b == '}' || b == ']') { s.depth -= 1; if (s.depth == 0) hit = 1; }
-            else if (b == ',' && s.depth == 1 && t.kind != CVY_PARSER_JSON_OBJECT) hit = 0;
-        }
-    }
-    if (t.kind == CVY_PARSER_CALL) {
-        // inside a call region: member pieces, the closing bracket ends the region
-        if (hit == 1) {
-            scan_emit(so, s.seg_start, since, tok_idx, 1, CVY_SEG_CLOSE);
-            s.seg_start = p;
-            s.win = 2;  // outside, rest of this line is not a line start
-        } else if (hit == 0) {
-            scan_emit(so, s.seg_start, since, tok_idx, 0, 0);
-            s.seg_start = p;
-        } else if ((int)since == t.max_seg) {
-            scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW);
-            s.seg_start = p;
-        }
-        return;
+        hit = json_step(s, b, t.kind != CVY_PARSER_JSON_OBJECT);
     }
     if (hit >= 0) {
-        scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)hit, 0);
+        scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)hit, 0, s.tool);
         s.seg_start = p;
         s.win = 0;
     } else if ((int)since == t.max_seg) {
-        scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW);
+        scan_emit(so, s.seg_start, since, tok_idx, (uint16_t)CVY_DELIM_NONE, CVY_SEG_OVERFLOW, s.tool);
         s.seg_start = p;
         s.win = 0;
     }
@@ -511,7 +533,8 @@ CVY_DEV void sample_scan_publish(const StepParams& P, int et, int* sm_i) {
                             for (int k = 0; k < nb; ++k) {
                                 const uint8_t byte = P.vtab[(size_t)g * kMaxTokenBytes + k];
                                 if (s.stream_len < P.round_bytes) P.byte_log[(size_t)b * P.round_bytes + s.stream_len] = byte;
-                                scan_byte(s, *tool, byte, ti, so);
+                                if (s.tool_set) scan_byte_set(s, P.tools, byte, ti, so);
+                                else scan_byte(s, *tool, byte, ti, so);
                             }
                         }
                         end = (P.eos >= 0 && g == P.eos) || s.gen >= s.max_new ||
@@ -520,7 +543,8 @@ CVY_DEV void sample_scan_publish(const StepParams& P, int et, int* sm_i) {
                 }
                 if (end) {
                     const uint32_t last = s.gen > 0 ? (uint32_t)(s.gen - 1) : CVY_NO_TOKEN;
-                    scan_emit(so, s.seg_start, s.stream_len - s.seg_start, last, (uint16_t)CVY_DELIM_NONE, fin_flags);
+                    scan_emit(so, s.seg_start, s.stream_len - s.seg_start, last, (uint16_t)CVY_DELIM_NONE, fin_flags,
+                              (tool && s.tool_set) ? s.region : s.tool);
                     s.active = 0;
                     n_fin++;
                 }
@@ -559,7 +583,8 @@ CVY_DEV void sample_scan_publish(const StepParams& P, int et, int* sm_i) {
             rec.byte_len = so.len[r];
             rec.delim_id = so.did[r];
             rec.flags = so.flags[r];
-            rec.slot = (uint32_t)b;
+            rec.slot = (uint16_t)b;
+            rec.tool = so.tool[r];
             ring[(first + r) & P.ring_mask] = rec;
         }
         if (live) {

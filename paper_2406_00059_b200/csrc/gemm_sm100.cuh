@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (long long it = it0 + pre; it < pf_end && !G.wtiled; ++it)
                 tma_prefetch_l2_2d(&tmW, (int)(it % G.kblocks) * BK, G.w_row0 + (int)(it / G.kblocks) * rows_per_tile);
             pdl_wait();
+            if (G.epi.span_kind >= 0) span_begin(P.spans, P.span_base + G.epi.layer * 8 + G.epi.span_kind);
             for (int i = 0; i < pre; ++i) {
                 const int kb = (int)((it0 + i) % G.kblocks);
                 uint8_t* sx = smem + (size_t)i * stage_bytes + WB;
@@ -526,6 +527,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         tmem_dealloc(tmem_base, G.tmem_cols);
     }
+    if (threadIdx.x == 0 && G.epi.span_kind >= 0)
+        span_end(P.spans, kSpanSlots, P.span_base + G.epi.layer * 8 + G.epi.span_kind);
     if (tr && threadIdx.x == 0) tr[5] = gtimer();
 }
 

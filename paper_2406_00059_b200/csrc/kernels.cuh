@@ -80,6 +80,9 @@ __global__ void apply_patches_kernel(SlotDev* slots, const Patch* patches, int n
                 s.depth = s.in_str = s.esc = 0;
                 s.cancel = 0;
                 s.max_pos = p.max_pos;
+                s.tool_set = p.tool_set;
+                s.set_max_seg = p.set_max_seg;
+                s.region = -1;
                 status[p.slot].state = 0;
                 status[p.slot].round = 0;
                 status[p.slot].gen = 0;
@@ -101,6 +104,7 @@ __global__ void apply_patches_kernel(SlotDev* slots, const Patch* patches, int n
                 s.depth = s.in_str = s.esc = 0;
                 s.cancel = 0;
                 s.max_pos = p.max_pos;
+                s.region = -1;
                 status[p.slot].state = 0;
                 status[p.slot].round = s.round;
                 status[p.slot].gen = 0;
@@ -124,6 +128,7 @@ template <typename T>
 __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ StepParams P) {
     pdl_launch_dependents();
     pdl_wait();
+    if (threadIdx.x == 0) span_begin(P.spans, P.span_base);
     const int b = blockIdx.x;
     int tok;
     if (P.row_tok) {
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(128) embed_kernel(const __grid_constant__ Step
     __syncthreads();
     for (int blk = threadIdx.x; blk < nblk && blk < kMaxBlk; blk += blockDim.x)
         P.ssq[(size_t)blk * P.Bmax + b] = (red[blk][0] + red[blk][1]) + (red[blk][2] + red[blk][3]);
+    if (threadIdx.x == 0) span_end(P.spans, kSpanSlots, P.span_base);
 }
 
 // ------------------------------------------------------------------ paged GQA decode attention

@@ -30,6 +30,9 @@ struct SlotDev {
     int32_t depth, in_str, esc;      // JSON automaton
     int32_t cancel;
     int32_t max_pos;    // reserved KV positions (exclusive bound on pos)
+    int32_t region;     // tool set: tool whose region is open (-1: outside)
+    uint64_t tool_set;  // region-tool set (bit i = tool i; 0: the single tool `tool`)
+    int32_t set_max_seg;  // tool set: cut of a line outside a region (smallest max_seg)
     int32_t pad_;
 };
 
@@ -62,7 +65,8 @@ struct Patch {
     int32_t tool, pos, cur_tok, in_len, in_idx, max_new, force_len, max_pos;
     uint32_t round, seq;
     int32_t set_pos;   // INJECT: 1 = also set pos / cur_tok (the observation was prefilled)
-    int32_t pad_;
+    int32_t set_max_seg;  // SUBMIT: tool set's outside-line cut
+    uint64_t tool_set;    // SUBMIT: region-tool set (0: single tool)
 };
 
 enum EpiKind : int32_t { EPI_QKV = 0, EPI_RESID = 1, EPI_SWIGLU = 2, EPI_LMHEAD = 3, EPI_STORE = 4 };
@@ -127,7 +131,15 @@ struct StepParams {
     const int32_t* row_slot;
     const int32_t* row_pos;
     const int32_t* row_tok;
+    // In-graph kernel spans (measurement variant of the step graph; null otherwise):
+    // spans[i] = earliest %globaltimer at which a CTA of launch i passed its grid-dependency
+    // wait (atomicMin), spans[kSpanSlots + i] = latest CTA exit (atomicMax);
+    // i = span_base + layer * 8 + kind (kind: 0 embed, 1 QKV, 2 attention, 4 O, 5 gate/up,
+    // 6 down, 7 LM head).
+    unsigned long long* spans;
+    int32_t span_base;
 };
+constexpr int kSpanSlots = 2 * 8 * 65;  // two chains x 8 kinds x (<= 64 layers + the LM head row)
 
 // keys attended by launch row r (its position + 1), 0 for idle slots / padding rows
 __host__ __device__ inline int row_nkeys(const StepParams& P, int r) {
@@ -143,6 +155,7 @@ struct EpiArgs {
     int32_t N;                  // valid output rows
     const float* norm_w;        // RESID: the next RMSNorm's weights
     float* store_out;           // STORE (test hook): out[b][n] fp32, row stride N
+    int32_t span_kind;          // kind of this launch in StepParams::spans (-1: none)
 };
 
 }  // namespace cvy

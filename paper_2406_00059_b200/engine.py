@@ -78,6 +78,7 @@ class Record:
     flags: int
     slot: int
     data: bytes
+    tool: int = -1
 
 
 class Engine:
@@ -128,12 +129,14 @@ class Engine:
 
     def submit_request(self, prompt, max_new_tokens: int, tool_id: int = -1, mode: int = capi.MODE_PARTIAL,
                        forced=None, synth_prefix_len: int = 0, synth_seed: int = 0, reserve_tokens: int = 0,
-                       allow_full: bool = False):
+                       allow_full: bool = False, tool_set=None):
         p = np.ascontiguousarray(np.asarray(prompt, dtype=np.int32))
         f = np.ascontiguousarray(np.asarray(forced if forced is not None else [], dtype=np.int32))
+        ts = np.ascontiguousarray(np.asarray(tool_set if tool_set else [], dtype=np.int32))
         i32p = ctypes.POINTER(ctypes.c_int32)
         desc = capi.RequestDesc(tool_id, mode, p.ctypes.data_as(i32p), len(p), synth_prefix_len, synth_seed,
-                                max_new_tokens, f.ctypes.data_as(i32p) if len(f) else None, len(f), reserve_tokens)
+                                max_new_tokens, f.ctypes.data_as(i32p) if len(f) else None, len(f), reserve_tokens,
+                                ts.ctypes.data_as(i32p) if len(ts) else None, len(ts))
         rid = ctypes.c_uint64()
         st = capi.lib().cvy_submit_request(self.h, ctypes.byref(desc), ctypes.byref(rid))
         if allow_full and st == capi.CVY_E_FULL:
@@ -167,7 +170,7 @@ class Engine:
                 data = raw[off:off + s.byte_len] if with_bytes else b""
                 off += s.byte_len if with_bytes else 0
                 out.append(Record(s.req_id, s.round, s.seq, s.step, s.token_index, s.byte_offset, s.byte_len,
-                                  s.delim_id, s.flags, s.slot, data))
+                                  s.delim_id, s.flags, s.slot, data, s.tool))
             if n.value < len(self._seg_buf):
                 return out
 
@@ -218,6 +221,16 @@ class Engine:
         n = ctypes.c_uint32()
         check(capi.lib().cvy_kernel_times(self.h, buf, len(buf), ctypes.byref(n)))
         return [(buf[i].kind, buf[i].layer, buf[i].ms) for i in range(n.value)]
+
+    def set_kernel_spans(self, on: bool):
+        check(capi.lib().cvy_set_kernel_spans(self.h, 1 if on else 0))
+
+    def kernel_spans(self):
+        """[(kind, layer, chain, t0_ns, t1_ns)] of the last span-recording step (cvy_kernel_spans)."""
+        buf = (capi.KernelSpan * 2048)()
+        n = ctypes.c_uint32()
+        check(capi.lib().cvy_kernel_spans(self.h, buf, len(buf), ctypes.byref(n)))
+        return [(buf[i].kind, buf[i].layer, buf[i].chain, buf[i].t0_ns, buf[i].t1_ns) for i in range(n.value)]
 
     def stream_ptr(self) -> int:
         return capi.lib().cvy_stream(self.h) or 0

@@ -63,6 +63,9 @@ class RequestLog:
     seg_avail: list = field(default_factory=list)    # per round: [t]
     seg_work: list = field(default_factory=list)     # per round: [SegmentWork]
     seg_end: list = field(default_factory=list)      # per round: [t]
+    seg_disp: list = field(default_factory=list)     # per round: [t dispatched to the tool]
+    seg_begin: list = field(default_factory=list)    # per round: [t the tool started it]
+    seg_token: list = field(default_factory=list)    # per round: [token index of its last byte]
     held: list = field(default_factory=list)         # Sequential: segments waiting for FINAL
     pending_tools: int = 0
     final_seen: bool = False
@@ -88,6 +91,8 @@ class Runtime:
         self.logs = []
         self.stop = False
         self.steps = 0
+        self.poller_cpu_s = 0.0    # CPU time of the poller thread (polling + dispatch)
+        self.dispatch_cpu_s = 0.0  # of which: handling polled records (parse plans, dispatch tools)
 
     # ---------------------------------------------------------------- tool clock
     def _schedule(self, t, cb):
@@ -106,6 +111,8 @@ class Runtime:
         end = start + work.cost_s
         self.inst_free[key] = end
         log.seg_end[rnd][j] = end
+        log.seg_disp[rnd][j] = t_avail
+        log.seg_begin[rnd][j] = start
         log.pending_tools += 1
         self._schedule(end, lambda lg=log, r=rnd, jj=j: self._tool_done(lg, r, jj))
         return True
@@ -174,6 +181,9 @@ class Runtime:
         log.seg_avail.append([])
         log.seg_work.append([])
         log.seg_end.append([])
+        log.seg_disp.append([])
+        log.seg_begin.append([])
+        log.seg_token.append([])
         log.held = []
 
     # ---------------------------------------------------------------- poller
@@ -195,6 +205,9 @@ class Runtime:
                     log.seg_work[rnd].append(work)
                     log.seg_avail[rnd].append(now)
                     log.seg_end[rnd].append(None)
+                    log.seg_disp[rnd].append(None)
+                    log.seg_begin[rnd].append(None)
+                    log.seg_token[rnd].append(r.token_index)
                     if self.mode == capi.MODE_PARTIAL:
                         self._dispatch(log, rnd, j, now)
                     else:
@@ -216,6 +229,13 @@ class Runtime:
             self._maybe_advance(log, now)
 
     def _poller(self):
+        c0 = time.thread_time()
+        try:
+            self._poll_loop()
+        finally:
+            self.poller_cpu_s = time.thread_time() - c0
+
+    def _poll_loop(self):
         while True:
             with self.lock:
                 if self.stop:
@@ -223,8 +243,11 @@ class Runtime:
             recs = self.eng.poll_segments(with_bytes=True)
             now = time.perf_counter()
             with self.lock:
-                for r in recs:
-                    self._on_record(r, now)
+                if recs:
+                    d0 = time.thread_time()
+                    for r in recs:
+                        self._on_record(r, now)
+                    self.dispatch_cpu_s += time.thread_time() - d0
                 # fire due tool completions
                 while self.events and self.events[0][0] <= now:
                     _, _, cb = heapq.heappop(self.events)

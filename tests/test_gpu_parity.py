@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
+from oracle.scan import round_records
 from gpu_harness import (as_tuples, ensure_built, expected_records, free_running_parity, group_records,
                          make_engine)
 from inputs.configs import MISTRAL_7B, TINY, slice_of
@@ -694,4 +695,69 @@ def test_abort_and_refill_matches_oracle():
         if cancelled:
             assert bad[i] and n < len(forced[i])
     assert n_cancelled >= 8 and refilled_checked > 100
+    eng.close()
+
+
+def multi_tool_text(rng):
+    """Prose, a ```python block, an @call search, a ```bash block, an @call calc, a fence of a
+    tag outside the set (prose), in a seeded order."""
+    parts = ["Plan: run the script, then query.\n",
+             "```python\n" + codegen_script(rng, rng.randint(4, 8)) + "```\n",
+             "@call search " + json.dumps({"q": "sine wave " + str(rng.randint(0, 99)), "n": 3}) + "\n",
+             "```bash\nls -la /tmp\necho done; cat out.txt\n```\n",
+             "@call calc " + json.dumps({"expr": f"{rng.randint(1, 99)} * {rng.randint(1, 99)}"}) + " ok\n",
+             "```js\nconsole.log(1)\n```\n",
+             "Finally: " + "".join(rng.choice("abc ,\n") for _ in range(30))]
+    rng.shuffle(parts)
+    return "".join(parts)
+
+
+@pytest.mark.parametrize("vocab_kind", ["byte", "32k"])
+def test_multi_tool_sets_bitexact(vocab_kind):
+    """NEXT-2 multi-tool routing (R24): each request holds a SET of region tools -- python and
+    bash FENCE tools and search and calc CALL tools -- and the marker that appears selects the
+    tool; records carry the tool id.  Bit-exact (tool field included) against oracle
+    region_records, with OVERFLOW inside regions (a short max_segment_bytes on one tool)."""
+    if vocab_kind == "byte":
+        shape, vocab = TINY, BYTE_VOCAB
+        enc = lambda t: list(t.encode())
+    else:
+        shape, vocab = slice_of(TINY, L=2, V=32000, name="tiny-v32k"), synthetic_vocab(32000)
+        tok = Tokenizer(vocab)
+        enc = tok.encode
+    dm, eng = make_engine(shape, "bf16", vocab, 16, 1024, max_pages_per_slot=64)
+    specs = [("py", capi.PARSER_FENCE, b"python", 4096), ("sh", capi.PARSER_FENCE, b"bash", 24),
+             ("search", capi.PARSER_CALL, b"search", 4096), ("calc", capi.PARSER_CALL, b"calc", 4096)]
+    ids = {n: eng.register_tool(n, k, [tag], max_segment_bytes=ms) for (n, k, tag, ms) in specs}
+    region_tools = [(ids[n], k, tag, ms) for (n, k, tag, ms) in specs]
+    rng = random.Random(24)
+    reqs, forced = [], []
+    for i in range(16):
+        f = enc(multi_tool_text(rng))[:900]
+        forced.append(f)
+        reqs.append(f)
+    rids = [eng.submit_request([1, 10], 1000, forced=f, tool_set=list(ids.values())) for f in reqs]
+    got = []
+    finals = set()
+    for _ in range(2000):
+        eng.step()
+        for r in eng.poll_segments():
+            got.append(r)
+            if r.flags & capi.SEG_FINAL:
+                finals.add(r.req_id)
+        if len(finals) == len(rids):
+            break
+    eng.sync()
+    got += eng.poll_segments()
+    by = group_records(got)
+    n_tools_seen = set()
+    for rid, f in zip(rids, forced):
+        exp, _ = round_records(f, vocab, 0, [], 4096, region_tools=region_tools)
+        want = [(r.round, r.seq, r.token_index, r.byte_offset, r.byte_len, r.delim_id, r.flags, r.data, r.tool)
+                for r in exp]
+        have = [(r.round, r.seq, r.token_index, r.byte_offset, r.byte_len, r.delim_id, r.flags, r.data, r.tool)
+                for r in by[rid]]
+        assert have == want, rid
+        n_tools_seen |= {r[8] for r in want if r[8] >= 0}
+    assert n_tools_seen == set(ids.values())
     eng.close()

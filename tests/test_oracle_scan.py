@@ -612,3 +612,122 @@ def test_region_grammars_token_index_random_splits(kind, tag):
             last = r.byte_offset + r.byte_len - 1
             assert r.token_index == max(i for i in range(len(pieces)) if bounds[i] <= last)
         assert recs[-1].byte_offset == tail
+
+
+# ------------------------------------------------------------------ multi-tool region sets (NEXT-2, R24)
+def mixed_region_reading(S: bytes, fences: dict, calls: dict):
+    """Independent reading of R24 without overflow, search-based: from the current position,
+    find the first line start whose line is a fence open marker (b"```" + tag + b"\\n") or
+    begins with a call marker (b"@call " + tag + b" "); a fence region is then walked line by
+    line (regex) to the b"```\\n" line, a call region through its JSON value with an explicit
+    stack (as search_call_reading); scanning resumes at the next line start.
+    fences / calls: {tool_id: tag}.  Returns (records with tool ids, FINAL start, FINAL tool)."""
+    marks = sorted([(t, b"```" + g + b"\n", "F") for t, g in fences.items()] +
+                   [(t, b"@call " + g + b" ", "C") for t, g in calls.items()])
+    recs, pos = [], 0
+    starts = [0] + [m.end() for m in re.finditer(rb"\n", S)]
+    while True:
+        found = None
+        for s in starts:
+            if s < pos:
+                continue
+            hit = [(t, m, k) for (t, m, k) in marks if S.startswith(m, s)]
+            if hit:
+                found = (s,) + hit[0]
+                break
+        if found is None:
+            return recs, _tail_after(S, pos), -1
+        a, tool, m, kind = found
+        recs.append((a, a + len(m), 0, oracle.FLAG_OPEN, tool))
+        c = a + len(m)
+        if kind == "F":
+            closed = False
+            for mm in re.finditer(rb"[^\n]*\n", S[c:]):
+                x, y = c + mm.start(), c + mm.end()
+                if mm.group(0) == b"```\n":
+                    recs.append((x, y, 0, oracle.FLAG_CLOSE, tool))
+                    pos, closed = y, True
+                    break
+                recs.append((x, y, 0, 0, tool))
+            if not closed:
+                last = S.rfind(b"\n", c)
+                return recs, (c if last < 0 else last + 1), tool
+            continue
+        stack, in_s, esc, i, closed = [], False, False, c, False
+        while i < len(S):
+            ch = S[i:i + 1]
+            if in_s:
+                if esc:
+                    esc = False
+                elif ch == b"\\":
+                    esc = True
+                elif ch == b'"':
+                    in_s = False
+            elif not stack:
+                if ch in (b"{", b"["):
+                    stack.append(ch)
+            elif ch == b'"':
+                in_s = True
+            elif ch in (b"{", b"["):
+                stack.append(ch)
+            elif ch in (b"}", b"]"):
+                stack.pop()
+                if not stack:
+                    recs.append((c, i + 1, 1, oracle.FLAG_CLOSE, tool))
+                    pos, closed = i + 1, True
+                    break
+            elif ch == b"," and len(stack) == 1:
+                recs.append((c, i + 1, 0, 0, tool))
+                c = i + 1
+            i += 1
+        if not closed:
+            return recs, c, tool
+        nl = S.find(b"\n", pos)
+        if nl < 0:
+            return recs, _tail_after(S, pos), -1
+        pos = nl + 1
+
+
+def test_region_single_tool_is_fence_or_call():
+    """A set of one FENCE (CALL) tool is exactly the pinned FENCE (CALL) grammar, overflow included."""
+    rng = random.Random(41)
+    toks = [b"```p\n", b"```\n", b"@call p ", b"{", b"}", b",", b'"', b"a", b"\n", b" ", b"`"]
+    for _ in range(3000):
+        S = b"".join(rng.choice(toks) for _ in range(rng.randint(0, 30)))
+        M = rng.choice([6, 9, 13, BIG])
+        rf, cf, _ = oracle.region_records([(3, FEN, b"p", M)], S)
+        assert ([r[:4] for r in rf], cf) == oracle.fence_records(b"p", M, S) and all(r[4] == 3 for r in rf)
+        M = rng.choice([8, 11, 17, BIG])
+        rc, cc, _ = oracle.region_records([(5, CAL, b"p", M)], S)
+        assert ([r[:4] for r in rc], cc) == oracle.call_records(b"p", M, S) and all(r[4] == 5 for r in rc)
+
+
+def test_region_two_fences_bruteforce():
+    """Every string up to length 7 over {`, p, q, \\n, a} with FENCE tools p (id 0) and q (id 1)."""
+    n = 0
+    for S in all_strings([b"`", b"p", b"q", b"\n", b"a"], 7):
+        assert oracle.region_records([(0, FEN, b"p", BIG), (1, FEN, b"q", BIG)], S) == \
+            mixed_region_reading(S, {0: b"p", 1: b"q"}, {}), S
+        n += 1
+    assert n == sum(5 ** k for k in range(8))
+
+
+def test_region_mixed_fences_and_calls_random():
+    """Random streams mixing two fence tags, two call tools, JSON and prose."""
+    rng = random.Random(43)
+    toks = [b"```py\n", b"```sh\n", b"```\n", b"@call s ", b"@call t ", b"@call u ", b"{", b"}", b"[", b"]",
+            b",", b'"', b"\\", b"a", b"\n", b" ", b"`"]
+    tools = [(0, FEN, b"py", BIG), (1, FEN, b"sh", BIG), (2, CAL, b"s", BIG), (3, CAL, b"t", BIG)]
+    for _ in range(20000):
+        S = b"".join(rng.choice(toks) for _ in range(rng.randint(0, 40)))
+        assert oracle.region_records(tools, S) == mixed_region_reading(S, {0: b"py", 1: b"sh"}, {2: b"s", 3: b"t"}), S
+
+
+def test_region_set_outside_cut_is_the_smallest_max_segment():
+    """Outside a region the line is cut at the smallest max_segment_bytes of the set; the rest
+    of that line is a continuation and cannot open a region (hand-checked)."""
+    tools = [(0, FEN, b"p", 6), (1, CAL, b"s", 20)]
+    S = b"aaaaaa```p\n```p\nx\n"
+    recs, c, t = oracle.region_records(tools, S)
+    # "aaaaaa" is cut at 6 bytes, "```p\n" is then a continuation: no OPEN; the next line opens
+    assert recs == [(11, 16, 0, oracle.FLAG_OPEN, 0), (16, 18, 0, 0, 0)] and (c, t) == (18, 0)

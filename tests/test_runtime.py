@@ -240,3 +240,58 @@ def test_time_oracle_runs_exactly_the_requested_steps():
     assert (steps, n, toks) == (3, 2, 6) and t > 0
     toks, t, _, n, steps = bench.time_oracle(TINY, reqs, 1e-9, 7, n_req=1, max_steps=50)
     assert steps == 1 and toks == 1
+
+
+def _check_timeline(lg):
+    from paper_2406_00059_b200 import timeline
+    ev = timeline.events(lg)
+    assert [e[0] for e in ev] == sorted(e[0] for e in ev)
+    assert {e[1] for e in ev} <= set(timeline.KINDS)
+    at = {}
+    for (t, k, r, j, p, d) in ev:
+        at.setdefault((r, p), {})[k] = t
+    for (r, p), ks in at.items():
+        if "PieceExecuted" in ks:
+            assert ks["TokenDecoded"] <= ks["PieceDispatched"] <= ks["ToolStart"] <= ks["PieceExecuted"]
+    # pieces of one tool instance are dispatched in order
+    disp = [(r, p, t) for (t, k, r, j, p, d) in ev if k == "PieceDispatched"]
+    for r in {x[0] for x in disp}:
+        ts = [t for (rr, p, t) in sorted(x for x in disp if x[0] == r)]
+        assert ts == sorted(ts)
+    tsv = timeline.to_tsv(ev)
+    rows = [ln.split("\t") for ln in tsv.splitlines()]
+    assert all(len(x) == 6 for x in rows) and len(rows) == len(ev)
+    assert "decode" in timeline.gantt(ev)
+    return ev
+
+
+def test_timeline_codegen_pieces_overlap_decode():
+    """Fig. 3: in Partial mode the interpreter executes lines while the
+    decode continues; the exported timeline (SPEC.md:387 columns) shows every piece but the
+    last few dispatched before RoundEnd, and ResponseReady after the last PieceExecuted."""
+    logs, _ = run("codegen", 2, capi.MODE_PARTIAL)
+    for lg in logs:
+        ev = _check_timeline(lg)
+        t_end = next(t for (t, k, *_ ) in ev if k == "RoundEnd")
+        disp = [t for (t, k, *_ ) in ev if k == "PieceDispatched"]
+        assert sum(t < t_end for t in disp) >= len(disp) - 2
+        assert ev[-1][1] == "ResponseReady"
+    logs, _ = run("codegen", 2, capi.MODE_SEQUENTIAL)
+    for lg in logs:
+        ev = _check_timeline(lg)
+        t_end = next(t for (t, k, *_ ) in ev if k == "RoundEnd")
+        assert all(t >= t_end for (t, k, *_ ) in ev if k == "PieceDispatched")
+
+
+def test_timeline_validation_abort_precedes_round_end():
+    """SPEC.md:352 / Fig. 7: in Partial mode the AbortSignal of an offending
+    request comes before its (cancelled) RoundEnd, far before a full decode would end."""
+    logs, _ = run("validation", 4, capi.MODE_PARTIAL)
+    aborted = [lg for lg in logs if lg.t_abort is not None]
+    assert aborted
+    for lg in aborted:
+        ev = _check_timeline(lg)
+        t_ab = next(t for (t, k, *_ ) in ev if k == "AbortSignal")
+        t_end = next(t for (t, k, *_ ) in ev if k == "RoundEnd")
+        assert t_ab <= t_end
+        assert t_ab < 0.5 * len(lg.spec.rounds[0].forced) * STEP_S * 1e6
