@@ -113,14 +113,12 @@ enum {
     CVY_ENGINE_DEBUG_LOGITS = 2, /* keep the last step's fp32 logits for cvy_debug_logits   */
     CVY_ENGINE_SCAN_OFF = 4,     /* trigger scan disabled for every slot (overhead A/B)      */
     CVY_ENGINE_NO_PDL = 8,       /* no programmatic dependent launch between kernels        */
-    CVY_ENGINE_NO_PERSISTENT = 16, /* one kernel per GEMM / attention instead of the
-                                     persistent all-layers kernel (A/B and parity)          */
+    /* 16: reserved (was the persistent all-layers kernel's opt-out; that kernel is gone) */
     CVY_ENGINE_CHUNKED_PREFILL = 32, /* prompt and observation tokens (all but the last) run
                                      as one batched prefill pass at the next step boundary
                                      instead of one token per decode step (NEXT-1)           */
     CVY_ENGINE_TILED_WEIGHTS = 64 /* wqkv / wo / wgu / wd are tile-major (packed by
-                                     cvy_pack_weights_tiled); bf16 only, excludes the
-                                     persistent all-layers kernel                            */
+                                     cvy_pack_weights_tiled); bf16 only                      */
 };
 
 typedef struct {

@@ -19,7 +19,7 @@ MODE_PARTIAL, MODE_SEQUENTIAL = 0, 1
 SEG_FINAL, SEG_OVERFLOW, SEG_CANCELLED, SEG_OPEN, SEG_CLOSE = 1, 2, 4, 8, 16
 DELIM_NONE = 0xFFFF
 NO_TOKEN = 0xFFFFFFFF
-ENGINE_NO_GRAPH, ENGINE_DEBUG_LOGITS, ENGINE_SCAN_OFF, ENGINE_NO_PDL, ENGINE_NO_PERSISTENT = 1, 2, 4, 8, 16
+ENGINE_NO_GRAPH, ENGINE_DEBUG_LOGITS, ENGINE_SCAN_OFF, ENGINE_NO_PDL = 1, 2, 4, 8
 ENGINE_CHUNKED_PREFILL = 32
 ENGINE_TILED_WEIGHTS = 64
 
@@ -84,7 +84,7 @@ class KernelSpan(ctypes.Structure):
 
 
 KERNEL_KINDS = {0: "embed", 1: "gemm_qkv", 2: "attention", 3: "attention_merge", 4: "gemm_o", 5: "gemm_gate_up",
-                6: "gemm_down", 7: "gemm_lm_head+sample_scan", 8: "layers_persistent", 9: "persistent_reset"}
+                6: "gemm_down", 7: "gemm_lm_head+sample_scan"}
 
 
 class PerfInfo(ctypes.Structure):

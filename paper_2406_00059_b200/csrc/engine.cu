@@ -24,8 +24,6 @@
 #include "gemm_sm100.cuh"
 #include "kernels.cuh"
 #include "attention_tc.cuh"
-#include "layers_persistent.cuh"
-#include "attention_pk.cuh"
 #include "step_params.h"
 
 using namespace cvy;
@@ -254,11 +252,6 @@ struct Bucket {
     bool ov = false;
     StepParams PH[2];
     std::vector<GemmPlan> hplans[2];  // per chain: 4 GEMMs per layer (QKV, O, gate/up, down)
-    // persistent layer kernel (layers_persistent.cuh): all L layers in one launch
-    bool pk = false;
-    CUtensorMap pk_w[4], pk_x[3];
-    PkParams pkp;
-    size_t pk_smem = 0;
 };
 
 }  // namespace
@@ -350,7 +343,6 @@ struct cvy_engine {
     std::vector<uint8_t> vlen_host;
     bool attn_tc = false;       // bf16 KV, head_dim 64/128, G <= 4: TMA + mma.sync attention
     int attn_stages = 2;
-    bool attn_pk = false;       // persistent attention kernel (CVY_ATTN_PERSISTENT=1, attention_pk.cuh)
     int attn_pps = 2;           // KV pages per attention stage: 2 x 2 stages = 32 KB of ring per CTA,
                                 // 6 CTAs per SM, so the decode grid (Hkv x B) runs in one wave
                                 // (measured at B=64: attention -3..6% vs 4 pages x 3 stages)
@@ -367,14 +359,6 @@ struct cvy_engine {
     std::vector<PrefillJob> prefill_pending;
     std::map<int, Bucket> prefill_buckets;
     uint64_t prefill_rows_total = 0;
-    int32_t* d_pk_done = nullptr;   // persistent kernel: [L][5] phase-done counters
-    int32_t* d_att_cnt = nullptr;   // persistent kernel: split attention segment tickets
-    float* d_att_part2 = nullptr;   // persistent kernel: [num_sms][2][G*(hd+2)] partials
-    float* d_pk_part = nullptr;     // persistent kernel: [2][num_sms][128 rows][<=128 cols] GEMM partials
-    uint32_t* d_pk_pflag = nullptr; // persistent kernel: [2][num_sms] partial tags
-    int32_t* d_pk_err = nullptr;    // device alias of h_pk_err
-    int32_t* h_pk_err = nullptr;    // first timed-out wait of the persistent kernel (0: none)
-    bool pk_ok = false;             // model shape supported by the persistent kernel
     bool w_tiled = false;           // projection weights packed tile-major (CVY_ENGINE_TILED_WEIGHTS)
     unsigned long long* d_trace = nullptr;  // test hook: GEMM CTA timestamps of one layer
     int trace_layer = -1;
@@ -395,36 +379,6 @@ cvy_status check_cuda(cvy_engine* e, cudaError_t err, const char* what) {
     if (err != cudaSuccess) {
         e->dead = true;
         std::string msg = std::string(what) + ": " + cudaGetErrorString(err);
-        if (e->h_pk_err && e->h_pk_err[0]) {
-            // site codes: 0x1gg epilogue tfull, 0x200 W ring, 0x3pp data producer, 0x4xx MMA,
-            // 0x5pp epilogue/attention; bits 12+: progress counter (layers_persistent.cuh)
-            msg += " (persistent kernel waits timed out:";
-            for (int r = 1; r < 8; ++r)
-                if (e->h_pk_err[2 * r]) {
-                    char buf[96];
-                    std::snprintf(buf, sizeof(buf), " site 0x%x progress %u cta %d;", (unsigned)e->h_pk_err[2 * r] & 0xFFFu,
-                                  (unsigned)e->h_pk_err[2 * r] >> 12, e->h_pk_err[2 * r + 1]);
-                    msg += buf;
-                }
-            msg += ")";
-            if (const char* dump = getenv("CVY_PK_DUMP")) {
-                if (FILE* f = std::fopen(dump, "w")) {
-                    for (int c = 0; c < e->num_sms; ++c) {
-                        std::fprintf(f, "%d", c);
-                        for (int r = 1; r < 8; ++r) {
-                            const unsigned v = (unsigned)e->h_pk_err[16 + c * 8 + r];
-                            std::fprintf(f, " %x:%u", v & 0xFFFu, v >> 12);
-                        }
-                        for (int r = 1; r < 8; ++r) {
-                            const int32_t* raw = e->h_pk_err + 16 + 8 * e->num_sms + c * 16 + 2 * r;
-                            std::fprintf(f, " [%08x %08x]", (unsigned)raw[1], (unsigned)raw[0]);
-                        }
-                        std::fprintf(f, "\n");
-                    }
-                    std::fclose(f);
-                }
-            }
-        }
         return fail(CVY_E_CUDA, msg);
     }
     return CVY_OK;
@@ -685,22 +639,6 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
         ALLOC(e->d_gemm_acc2, sizeof(float) * max_rows * (size_t)Bmax);
         ALLOC(e->d_tile_cnt2, sizeof(int32_t) * 8192);
     }
-    e->pk_ok = e->bf16 && hd == 128 && (H / Hkv) <= 4 && H % Hkv == 0 && d % 128 == 0 && ((H + 2 * Hkv) * hd) % 128 == 0 &&
-               (2 * dff) % 128 == 0 && (H * hd) % 64 == 0 && dff % 64 == 0 && !(ec->flags & CVY_ENGINE_NO_PERSISTENT) &&
-               !(ec->flags & CVY_ENGINE_TILED_WEIGHTS);  // the persistent kernel reads row-major weights
-    // opt-in until it beats the one-kernel-per-op path (DESIGN.md §7 "Persistent layer kernel")
-    {
-        const char* pe = getenv("CVY_PERSISTENT");
-        e->pk_ok = e->pk_ok && pe != nullptr && atoi(pe) != 0;
-    }
-    if (e->pk_ok) {
-        ALLOC(e->d_pk_done, sizeof(int32_t) * (size_t)m->n_layers * kPkPhases);
-        ALLOC(e->d_att_cnt, sizeof(int32_t) * (size_t)Bmax * Hkv);
-        ALLOC(e->d_att_part2, sizeof(float) * (size_t)prop.multiProcessorCount * 2 * (H / Hkv) * (hd + 2));
-        ALLOC(e->d_pk_part, sizeof(float) * 2 * (size_t)prop.multiProcessorCount * 128 * std::min(Bmax, kPkMaxBp));
-        ALLOC(e->d_pk_pflag, sizeof(uint32_t) * 2 * (size_t)prop.multiProcessorCount);
-        HALLOC(e->h_pk_err, e->d_pk_err, sizeof(int32_t) * (16 + 24 * (size_t)prop.multiProcessorCount));  // host-mapped: readable after a trap
-    }
     if ((ec->flags & CVY_ENGINE_CHUNKED_PREFILL) && e->bf16) {
         const size_t R = kPrefillRows;
         ALLOC(e->d_px, sizeof(float) * R * d);
@@ -780,10 +718,6 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
         e->attn_stages = 2;
         if (const char* as = getenv("CVY_ATTN_STAGES")) e->attn_stages = std::max(2, std::min(6, atoi(as)));
         if (const char* ap = getenv("CVY_ATTN_PPS")) e->attn_pps = atoi(ap) == 2 ? 2 : 4;
-        if (const char* apk = getenv("CVY_ATTN_PERSISTENT"))
-            e->attn_pk = atoi(apk) != 0 && hd == 128 && (H / Hkv) <= 4;
-        if (e->attn_pk)
-            cudaFuncSetAttribute(attention_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ap_smem_bytes(3));
         for (const void* f : {(const void*)attention_tc_kernel<128, 2>, (const void*)attention_tc_kernel<128, 3>,
                               (const void*)attention_tc_kernel<128, 4>, (const void*)attention_tc_kernel<64, 2>,
                               (const void*)attention_tc_kernel<64, 3>, (const void*)attention_tc_kernel<64, 4>,
@@ -795,7 +729,6 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     // kernel attributes
     set_gemm_smem_attrs();
     cudaFuncSetAttribute(gemm_simt_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e->pk_ok) cudaFuncSetAttribute(layers_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     cudaFuncSetAttribute(gemm_simt_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (cudaDeviceSynchronize() != cudaSuccess) {
         cvy_engine_destroy(e);
@@ -827,12 +760,11 @@ void cvy_engine_destroy(cvy_engine* e) {
     void* dptrs[] = {e->d_trace, e->d_slots, e->d_page_table, e->d_in_buf, e->d_force_buf, e->d_rope, e->d_x, e->d_act, e->d_q,
                      e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches,
-                     e->d_pk_done, e->d_att_cnt, e->d_att_part2, e->d_pk_part, e->d_pk_pflag,
                      e->d_px, e->d_pact, e->d_pq, e->d_po, e->d_ph, e->d_pssq, e->d_pattn_part, e->d_prow,
                      e->d_gemm_acc2, e->d_tile_cnt2, e->d_spans};
     for (void* p : dptrs)
         if (p) cudaFree(p);
-    void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats, e->h_pk_err};
+    void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats};
     for (void* p : hptrs)
         if (p) cudaFreeHost(p);
     for (auto& ev : e->ov_ev)
@@ -1459,60 +1391,6 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
             a.tmN = b.tmW;
         }
     }
-    // persistent all-layers kernel (layers_persistent.cuh) when the shape and batch allow it
-    if (e->pk_ok && (Bp == 32 || Bp == 64 || Bp == 128)) {
-        PkParams& K = bk.pkp;
-        std::memset(&K, 0, sizeof(K));
-        const int Nq[4] = {Nqkv, d, 2 * dff, d}, Kq[4] = {d, H * hd, d, dff};
-        const void* Wq[4] = {e->w.wqkv, e->w.wo, e->w.wgu, e->w.wd};
-        bool ok = true;
-        for (int q = 0; q < 4 && ok; ++q) {
-            K.g[q].N = Nq[q];
-            K.g[q].K = Kq[q];
-            K.g[q].tiles = Nq[q] / 128;
-            K.g[q].kblocks = Kq[q] / 64;
-            ok = make_tmap(&bk.pk_w[q], Wq[q], (uint64_t)L * Nq[q], (uint64_t)Kq[q], (uint64_t)Kq[q], 128, 64);
-        }
-        const void* Xq[3] = {e->d_act, e->d_o, e->d_h};
-        const int XK[3] = {d, H * hd, dff};
-        for (int q = 0; q < 3 && ok; ++q)
-            ok = make_tmap(&bk.pk_x[q], Xq[q], (uint64_t)(2 * e->slots.size()), (uint64_t)XK[q], (uint64_t)e->act_ld,
-                           (uint32_t)Bp, 64);
-        // D ring: one activation k-block per slot; an attention unit (4 KV pages) spans att_su
-        // slots.  ~96 KB of data ring, the rest of shared memory for the weight ring.
-        K.x_slot = 2u * Bp * 128u;
-        K.att_ppslot = (int)(K.x_slot / 8192u);  // 1, 2 or 4 (Bp 32, 64, 128)
-        K.att_su = 8 / K.att_ppslot;
-        K.x_arrivals = K.att_ppslot;
-        K.x_stages = std::max<int>(K.att_su, (int)((96u * 1024u) / K.x_slot));
-        if (const char* v = getenv("CVY_PK_XSTAGES")) K.x_stages = std::max(K.att_su, std::min(16, atoi(v)));
-        // the idle data ring doubles as the stream-K reduction scratch (kPkMaxCon x 16 KB)
-        K.x_stages = std::max<int>(K.x_stages, (int)((kPkMaxCon * 16384u + K.x_slot - 1) / K.x_slot));
-        const uint32_t fixed = PkSmem::total(0, K.x_stages, K.x_slot) + 16 * 12;
-        K.w_stages = std::min<int>(12, (int)((232448 - fixed) / kPkWStage));
-        if (const char* v = getenv("CVY_PK_WSTAGES")) K.w_stages = std::max(2, std::min(K.w_stages, atoi(v)));
-        K.tmem_cols = pow2_at_least((uint32_t)(4 * Bp));
-        K.l2_pf = 0;
-        if (const char* v = getenv("CVY_PK_L2PF")) K.l2_pf = std::max(0, atoi(v));
-        K.done = e->d_pk_done;
-        K.att_cnt = e->d_att_cnt;
-        K.att_part = e->d_att_part2;
-        K.part = e->d_pk_part;
-        K.pflag = e->d_pk_pflag;
-        K.err = e->d_pk_err;
-        K.trace = e->d_trace;
-        K.trace_layer = e->trace_layer;
-        K.trace_phase = 1;
-        if (const char* v = getenv("CVY_PK_TRACE_PHASE")) K.trace_phase = atoi(v);
-        bk.pk_smem = PkSmem::total(K.w_stages, K.x_stages, K.x_slot);
-        int nb = 0;
-        if (ok && K.w_stages >= 2 && bk.pk_smem <= 232448 &&
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, layers_persistent_kernel, kPkThreads, bk.pk_smem) ==
-                cudaSuccess &&
-            nb >= 1)
-            bk.pk = true;
-        cudaGetLastError();
-    }
     auto res = e->buckets.emplace(Bp, std::move(bk));
     *out = &res.first->second;
     return CVY_OK;
@@ -1568,15 +1446,6 @@ cvy_status launch_attention(cvy_engine* e, Bucket& bk, int l, KTimer* kt, StepPa
     const size_t attn_smem = sizeof(float) * (G * m.head_dim + G * kAttnThreads + 3 * kAttnMaxG + 4 * kAttnMaxG);
     int layer = l;
     void* aargs[] = {&P, &layer};
-    if (e->attn_pk && P.row_slot == nullptr && Bp <= kApMaxRows) {
-        int nst = 3;
-        void* pargs[] = {&e->tm_kv, &P, &layer, &nst};
-        if ((st = launch_k(e, (const void*)attention_persistent_kernel, dim3(e->num_sms), dim3((kApConsumers + 1) * 32),
-                           ap_smem_bytes(nst), pargs, true)) != CVY_OK)
-            return st;
-        if (kt) kt->end();
-        return CVY_OK;
-    }
     if (e->attn_tc) {
         void* targs[] = {&e->tm_kv, &P, &layer};
         const int pps = e->attn_pps;
@@ -1795,38 +1664,6 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
         if ((st = launch_k(e, f, dim3(Bp), dim3(128), 0, args, true)) != CVY_OK) return st;
         kt.end();
         launches++;
-    }
-    if (bk.pk) {
-        // all layers in one persistent launch (one CTA per SM, co-resident: cooperative)
-        kt.begin(9, 0);
-        if ((st = check_cuda(e, cudaMemsetAsync(e->d_pk_done, 0, sizeof(int32_t) * m.n_layers * kPkPhases, e->stream),
-                             "persistent counters reset")) != CVY_OK)
-            return st;
-        kt.end();
-        void* args[] = {&bk.pk_w[0], &bk.pk_w[1], &bk.pk_w[2], &bk.pk_w[3], &bk.pk_x[0], &bk.pk_x[1],
-                        &bk.pk_x[2], &e->tm_kv, &bk.P, &bk.pkp};
-        cudaLaunchConfig_t cfg;
-        std::memset(&cfg, 0, sizeof(cfg));
-        cfg.gridDim = dim3(e->num_sms);
-        cfg.blockDim = dim3(kPkThreads);
-        cfg.dynamicSmemBytes = bk.pk_smem;
-        cfg.stream = e->stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        kt.begin(8, 0);
-        cudaError_t err = cudaLaunchKernelExC(&cfg, (const void*)layers_persistent_kernel, args);
-        if (err != cudaSuccess) return fail(CVY_E_CUDA, std::string("persistent launch: ") + cudaGetErrorString(err));
-        kt.end();
-        launches += 1;
-        kt.begin(7, 0);
-        if ((st = launch_gemm(e, bk, bk.plans.back())) != CVY_OK) return st;
-        kt.end();
-        launches++;
-        bk.launches = launches;
-        return CVY_OK;
     }
     if (bk.ov) {
         st = enqueue_overlap_layers(e, bk, kt, &launches);

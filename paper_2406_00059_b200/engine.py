@@ -24,12 +24,9 @@ def model_config(shape, dtype: str = "bf16") -> capi.ModelConfig:
 
 def tiled_default(shape, dtype: str) -> bool:
     """Tile-major projection weights (CVY_ENGINE_TILED_WEIGHTS) unless the shape cannot be
-    tiled, the persistent all-layers kernel (row-major weights) is requested, or
-    CVY_TILED_WEIGHTS=0."""
+    tiled or CVY_TILED_WEIGHTS=0."""
     import os
     if dtype != "bf16" or os.environ.get("CVY_TILED_WEIGHTS", "1") == "0":
-        return False
-    if os.environ.get("CVY_PERSISTENT", "0") not in ("", "0"):
         return False
     rows = [(shape.H + 2 * shape.Hkv) * shape.hd, shape.d, 2 * shape.dff]
     cols = [shape.d, shape.H * shape.hd, shape.dff]
@@ -55,7 +52,7 @@ class DeviceModel:
             nbytes = getattr(sizes, name)
             self.tensors[name] = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=dev)
         self.tensors["kv_pool"].zero_()
-        self.w = capi.Weights(*[self.tensors[n].data_ptr() for n, _ in capi.Weights._fields_])
+        self.w = capi.Weights(*[self.tensors[n].data_ptr() for n, _ in capi.WeightSizes._fields_])
         check(capi.lib().cvy_init_synthetic_weights(ctypes.byref(self.cfg), ctypes.byref(self.w), seed, device))
         self.tiled = tiled_default(shape, dtype) if tiled is None else bool(tiled)
         if self.tiled:

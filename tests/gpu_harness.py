@@ -2,6 +2,9 @@
 oracle side by side on the same seeded inputs (inputs/)."""
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 
 import oracle
@@ -77,6 +80,11 @@ def free_running_parity(shape, dtype, vocab, prompts, max_new, seed, tol, prefix
         eng.poll_segments()
         t += 1
     eng.close()
+    log = os.environ.get("CVY_PARITY_LOG")
+    if log:  # measured margins (e.g. gpurun_out/parity.jsonl), for DESIGN.md §4
+        with open(log, "a") as f:
+            f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", ""), "shape": shape.name,
+                                "dtype": dtype, "B": len(prompts), "max_abs_diff": maxdiff, "tol": tol}) + "\n")
     return maxdiff, gens
 
 

@@ -68,17 +68,13 @@ def test_tiny_fp32_with_synthetic_prefix():
 
 
 # ------------------------------------------------------------------ 7B shape
-@pytest.mark.parametrize("persistent", [True, False])
-def test_7b_two_layer_slice_bf16(persistent, monkeypatch):
-    """2-layer 7B slice through the persistent all-layers kernel (CVY_PERSISTENT=1) and through
-    the one-kernel-per-op path (CVY_ENGINE_NO_PERSISTENT)."""
-    monkeypatch.setenv("CVY_PERSISTENT", "1")
+def test_7b_two_layer_slice_bf16():
+    """2-layer 7B slice, three requests of different prompt lengths over a 40-token prefix."""
     shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
     vocab = synthetic_vocab(32000)
     prompts = [[1, 300, 5000], [1, 77], [1, 31999, 2000, 12]]
     d, _ = free_running_parity(shape, "bf16", vocab, prompts, max_new=3, seed=1003, tol=2e-2, prefix=40,
-                               synth_seeds=[11, 12, 13],
-                               extra_flags=0 if persistent else capi.ENGINE_NO_PERSISTENT)
+                               synth_seeds=[11, 12, 13])
     assert d < 2e-2
 
 
@@ -106,7 +102,6 @@ def test_pack_weights_tiled_is_the_tile_permutation():
 @pytest.mark.parametrize("tiled", ["1", "0"])
 def test_7b_two_layer_slice_weight_layouts(tiled, monkeypatch):
     """The projection GEMMs over tile-major (CVY_ENGINE_TILED_WEIGHTS) and row-major weights."""
-    monkeypatch.setenv("CVY_PERSISTENT", "0")
     monkeypatch.setenv("CVY_TILED_WEIGHTS", tiled)
     shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
     vocab = synthetic_vocab(32000)
@@ -116,21 +111,12 @@ def test_7b_two_layer_slice_weight_layouts(tiled, monkeypatch):
     assert d < 2e-2
 
 
-def set_mode(monkeypatch, mode):
-    """mode "1": persistent all-layers kernel; "0": one kernel per op; "attn": one kernel per op
-    with the persistent attention kernel (attention_pk.cuh; hd 128, G <= 4, else attention_tc)."""
-    monkeypatch.setenv("CVY_PERSISTENT", "1" if mode == "1" else "0")
-    monkeypatch.setenv("CVY_ATTN_PERSISTENT", "1" if mode == "attn" else "0")
-
-
 @pytest.mark.parametrize("H,Hkv,hd,prefix", [(8, 2, 64, 90), (4, 2, 128, 230), (4, 4, 128, 17), (8, 8, 64, 300),
                                              (8, 2, 128, 500)])
-@pytest.mark.parametrize("persistent", ["1", "0", "attn"])
-def test_tensor_core_attention_shapes(H, Hkv, hd, prefix, persistent, monkeypatch):
+def test_tensor_core_attention_shapes(H, Hkv, hd, prefix):
     """The TMA + mma.sync attention kernels across head_dim 64/128 and GQA groups 1, 2, 4,
     contexts spanning several 4-page pipeline stages and split-KV partitions."""
     from inputs.configs import ModelShape
-    set_mode(monkeypatch, persistent)
     shape = ModelShape(f"att-{H}-{Hkv}-{hd}", L=2, d=512, H=H, Hkv=Hkv, hd=hd, dff=1024, V=512, eps=1e-5,
                        rope_base=1e4, eos=-1)
     vocab = [bytes([i % 256]) * (1 + i // 256) for i in range(512)]
@@ -140,12 +126,9 @@ def test_tensor_core_attention_shapes(H, Hkv, hd, prefix, persistent, monkeypatc
     assert d < 2e-3
 
 
-@pytest.mark.parametrize("persistent", ["1", "0", "attn"])
-def test_7b_slice_b40_long_contexts_sampled(persistent, monkeypatch):
-    """40 requests with 100..600-token synthetic contexts on a 2-layer 7B slice: many attention
-    segments per CTA (the persistent kernel snaps CTA shares to segment boundaries), multi-chunk
-    runs, stream-K tiles shared by several CTAs.  Sampled requests vs the oracle, two steps."""
-    set_mode(monkeypatch, persistent)
+def test_7b_slice_b40_long_contexts_sampled():
+    """40 requests with 100..600-token synthetic contexts on a 2-layer 7B slice: multi-chunk
+    attention runs, batch-padded GEMMs.  Sampled requests vs the oracle, two steps."""
     shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
     vocab = synthetic_vocab(32000)
     B, seed = 40, 1006
