@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
         fence_mbar_init();
     }
     __syncthreads();
-    pdl_wait();
-    if (threadIdx.x == 0) span_begin(P.spans, P.span_base + layer * 8 + 2);
 
+    // The split's key range and pages depend only on the slot state and page table (complete
+    // before this step's graph starts), so they are read before the grid-dependency wait.
     const int nkeys = row_nkeys(P, b);
     const int nsplit = P.attn_splits;
     const int per = (((nkeys + nsplit - 1) / nsplit) + 16 * PPS - 1) / (16 * PPS) * (16 * PPS);
@@ -97,27 +97,47 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
 
     if (warp == kAtcWarps) {
         // ============ producer: TMA page blocks into the stage ring ============
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            for (int t = 0; t < n_tiles; ++t) {
-                const int st = t % STAGES;
-                const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
-                mbar_wait(&empty_bar[st], ph ^ 1u);
-                const int np = min(PPS, n_pages - t * PPS);
-                mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(np * 2 * BLK));
-                for (int p = 0; p < np; ++p) {
-                    const int page = pt[pg_begin + t * PPS + p];
+        // Pages strictly below the one holding this step's new key (written by the QKV
+        // epilogue) were written by earlier steps: the first stages made only of such pages are
+        // issued BEFORE griddepcontrol.wait, so their HBM reads overlap the previous kernel's
+        // tail (decode rows only; a prefill pass writes several keys per slot).  The page ids
+        // are read 32 at a time by the whole warp (no dependent load per TMA issue).
+        const int safe_pages = (P.row_slot || !P.attn_early) ? 0 : max(0, (nkeys - 1) / 16 - pg_begin);
+        const uint64_t pol = policy_evict_first();
+        int chunk_base = -32, my_page = 0;
+        auto page_of = [&](int i) {  // page id of split page i (warp-uniform i, increasing)
+            if (i >= chunk_base + 32) {
+                chunk_base = i & ~31;
+                const int j = chunk_base + lane;
+                my_page = j < n_pages ? pt[pg_begin + j] : 0;
+            }
+            return __shfl_sync(0xffffffffu, my_page, i & 31);
+        };
+        auto issue = [&](int t) {
+            const int st = t % STAGES;
+            const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
+            mbar_wait(&empty_bar[st], ph ^ 1u);
+            const int np = min(PPS, n_pages - t * PPS);
+            if (lane == 0) mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(np * 2 * BLK));
+            for (int p = 0; p < np; ++p) {
+                const int page = page_of(t * PPS + p);
+                if (lane == 0)
                     for (int c = 0; c < 2; ++c) {
                         const int row0 = ((((layer * P.n_pages + page) * 2 + c) * P.Hkv) + g) * 16;
                         for (int h = 0; h < HALVES; ++h)
                             tma_load_2d(stages + (size_t)st * STAGE + (size_t)(p * 2 + c) * BLK + h * 2048, &tmKV,
                                         &full_bar[st], h * 64, row0, pol);
                     }
-                }
             }
-        }
+        };
+        int t = 0;
+        for (; t < n_tiles && t < STAGES && (t + 1) * PPS <= safe_pages; ++t) issue(t);
+        pdl_wait();
+        for (; t < n_tiles; ++t) issue(t);
         return;
     }
+    pdl_wait();
+    if (threadIdx.x == 0) span_begin(P.spans, P.span_base + layer * 8 + 2);
 
     // ============ consumers ============
     const int grp = lane >> 2, tig = lane & 3;

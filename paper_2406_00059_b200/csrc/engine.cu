@@ -112,6 +112,13 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     // width (6144 rows: 24 tiles x 4-CTA clusters; measured QKV 0.896 -> 0.836 ms/step at B=64),
     // not for the 4096-row O / down GEMMs (16 tiles: too few CTAs)
     g.nsub = (g.merge && N >= 6144) ? 2 : 1;
+    // batch tiles (Bp > 128): the narrow GEMMs (O, down) also take 256-row tiles, K split over a
+    // 2-CTA cluster per (tile, batch tile) -- half the shared-memory traffic per MMA of 128-row
+    // tiles, which cap the tensor pipe at ~2/3 there (measured at B = 512: down 97 -> 81 us)
+    bool bt_split = g.merge && g.nbt > 1 && allow_kernel_split && !streamk &&
+                    ((N + 255) / 256) * g.nbt * 2 <= num_sms && K / 64 >= 2;
+    if (const char* v = getenv("CVY_GEMM_BT_SPLIT")) bt_split = bt_split && atoi(v) != 0;  // A/B knob
+    if (bt_split) g.nsub = 2;
     if (const char* ns = getenv("CVY_GEMM_NSUB")) g.nsub = std::max(1, std::min(2, atoi(ns)));
     if (nsub_override > 0) g.nsub = nsub_override;
     if (g.merge) {
@@ -136,7 +143,11 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     g.kblocks = K / g.bk;
     const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bq, 2, g.bk);
     const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
-    int stages = std::min(12, (int)((232448 - fixed) / stage));
+    // shared-memory budget per CTA (A/B knob CVY_GEMM_SMEM: a smaller ring lets the next
+    // kernel's CTA co-reside and start its weight stream under this kernel's epilogue tail)
+    uint32_t budget = 232448;
+    if (const char* v = getenv("CVY_GEMM_SMEM")) budget = std::max(fixed + 2 * stage, std::min<uint32_t>(232448, atoi(v)));
+    int stages = std::min(12, (int)((budget - fixed) / stage));
     if (stages < 2) {
         *why = "not enough shared memory for 2 stages";
         return false;
@@ -145,12 +156,12 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     *smem = (size_t)stages * stage + fixed;
     // split mode: tiles <= SMs (one tile, or one cluster of S CTAs per tile)
     g.split = 0;
-    if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk && (g.nbt == 1 || !allow_kernel_split)) {
+    if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk && (g.nbt == 1 || !allow_kernel_split || bt_split)) {
         int S = 1;
         // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
-        while (allow_kernel_split && S < kMaxSplit && g.tiles * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
+        while (allow_kernel_split && S < kMaxSplit && g.tiles * g.nbt * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
         if (S == 3 && !getenv("CVY_GEMM_ALLOW_S3")) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
-        if (g.tiles <= num_sms) g.split = S;
+        if ((bt_split ? g.tiles * g.nbt : g.tiles) <= num_sms) g.split = S;
         // the DSMEM staging of the partial must fit in the pipeline smem
         if (g.split > 1 && (size_t)g.nsub * Bq * 512 > (size_t)stages * stage) g.split = 0;
         // the kernel's reduce-scatter sums at most kMaxSplit ranks (gemm_sm100.cuh, t4[kMaxSplit])
@@ -1190,6 +1201,8 @@ StepParams base_params(cvy_engine* e, int Bp) {
     const int want = cells >= e->num_sms ? 1 : (2 * e->num_sms + cells - 1) / cells;
     P.attn_splits = std::max(1, std::min(e->attn_splits_max, want));
     if (const char* as = getenv("CVY_ATTN_SPLITS")) P.attn_splits = std::max(1, std::min(e->attn_splits_max, atoi(as)));
+    P.attn_early = 1;
+    if (const char* v = getenv("CVY_ATTN_EARLY")) P.attn_early = atoi(v);  // A/B knob
     P.vtab = e->d_vtab;
     P.vlen = e->d_vlen;
     P.tools = e->d_tools;

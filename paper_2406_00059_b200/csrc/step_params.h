@@ -109,6 +109,7 @@ struct StepParams {
     // attention split-KV workspace
     float* attn_part;           // [Bmax][Hkv][nsplit][G*(hd+2)]
     int32_t attn_splits;
+    int32_t attn_early;         // attention_tc: issue old-page TMA loads before the PDL wait (1)
     // scan / publish
     const uint8_t* vtab;        // [V][16]
     const uint8_t* vlen;        // [V]
