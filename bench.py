@@ -700,12 +700,14 @@ def latency_pages(router, workloads=AB_WORKLOADS):
 
 
 def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flags=0, dm=None, indices=None,
-                reps=1):
+                reps=1, des=None):
     """Request completion latency with tool partial execution vs sequential tool execution on
     the workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool costs
     in both modes (the baseline is the same code with partial execution
     disabled).  `indices(w)`: the global request indices this rank serves (router).  Each
-    (workload, mode) runs `reps` times, modes interleaved.  Returns {workload: {...}}."""
+    (workload, mode) runs `reps` times, modes interleaved.  `des`: a schedule model passed to
+    runtime.summarize (the GPU tests pass the oracle's O-3 DES; bench.py never does).
+    Returns {workload: {...}}."""
     from inputs.configs import MISTRAL_7B
     from inputs.tool_workloads import TOOLS, build
     from inputs.vocab import synthetic_vocab
@@ -734,7 +736,7 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flag
                 t0 = time.perf_counter()
                 c0 = time.process_time()
                 logs = rt.run(specs, max_inflight=inflight)
-                s = summarize(logs, mode)
+                s = summarize(logs, mode, des=des)
                 s["steps"] = rt.steps
                 s["wall_s"] = time.perf_counter() - t0
                 s["host_cpu_s"] = time.process_time() - c0

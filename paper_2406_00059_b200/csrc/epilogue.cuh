@@ -295,13 +295,27 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                 esm[et * kEsmLd + i] = valid ? lg : -INFINITY;
             }
             epi_sync();
-            if (et < ncols) {
-                uint64_t best = 0;
-                for (int r = 0; r < 128; ++r) {
-                    uint64_t k = argmax_key(esm[r * kEsmLd + et], (uint32_t)(n0 + r));
-                    best = k > best ? k : best;
+            // warp-level tile argmax: warp w takes columns w, w+4, ...; each lane folds 4 of
+            // the tile's 128 rows (conflict-free: row stride 33 words), then a 5-step shuffle
+            // max over the 64-bit (value, ~index) keys; lane 0 folds the tile's best into the
+            // column's global key (atomicMax keeps the largest value, lowest index on ties)
+            {
+                const int w = et >> 5, ln = et & 31;
+                for (int c = w; c < ncols; c += kEpiThreads / 32) {
+                    unsigned long long best = 0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int r = ln + 32 * i;
+                        const unsigned long long k = argmax_key(esm[r * kEsmLd + c], (uint32_t)(n0 + r));
+                        best = k > best ? k : best;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+                        best = t > best ? t : best;
+                    }
+                    if (ln == 0) atomicMax(&P.am_keys[cb + c], best);
                 }
-                atomicMax(&P.am_keys[cb + et], (unsigned long long)best);
             }
             epi_sync();
             break;

@@ -152,6 +152,32 @@ def test_codegen_only_last_line_after_decode(monkeypatch):
         assert len(late) <= 2
 
 
+@pytest.mark.gpu
+def test_engine_latency_matches_des_and_partial_wins():
+    """S13 on the real engine (2-layer 7B slice, 32k vocab, CUDA graphs): the runtime's measured
+    request latencies agree with the oracle's O-3 DES recomputed from each request's logged
+    round / segment timeline, in both modes, and partial execution beats
+    sequential execution on every workload shape; validation aborts are detected earlier in
+    partial mode."""
+    import bench
+    from inputs.configs import MISTRAL_7B, slice_of
+    from paper_2406_00059_b200.engine import DeviceModel
+    shape = slice_of(MISTRAL_7B, L=2, name="7b-L2")
+    w = ["codegen", "search", "planning", "validation"]
+    batches = {"codegen": 8, "search": 8, "planning": 8, "validation": 16}
+    dm = DeviceModel(shape, "bf16", 16 * 200, seed=1002)
+    res = bench.run_latency(w, batches, dm=dm, des=oracle_des)
+    for name, row in res.items():
+        assert row["partial_mean_ms"] < row["sequential_mean_ms"], (name, row["improvement"])
+        for mode in ("partial", "sequential"):
+            r = row["runs"][mode][0]
+            if "des_max_abs_err_ms" in r:
+                assert r["des_max_abs_err_ms"] < 40, (name, mode, r["des_max_abs_err_ms"])
+            elif name != "validation":
+                raise AssertionError(f"{name} {mode}: no DES cross-check")
+    assert res["validation"]["detection_partial_ms"] < res["validation"]["detection_sequential_ms"]
+
+
 # ------------------------------------------------------------------ NEXT-4: Fig. 6 sweep
 def test_sweep_builder_tool_time_is_r_times_decode_time():
     """build_sweep assigns line costs so a round's tool time is r x its decode time at the
