@@ -1201,7 +1201,7 @@ StepParams base_params(cvy_engine* e, int Bp) {
     const int want = cells >= e->num_sms ? 1 : (2 * e->num_sms + cells - 1) / cells;
     P.attn_splits = std::max(1, std::min(e->attn_splits_max, want));
     if (const char* as = getenv("CVY_ATTN_SPLITS")) P.attn_splits = std::max(1, std::min(e->attn_splits_max, atoi(as)));
-    P.attn_early = 1;
+    P.attn_early = 0;  // measured neutral; off keeps the in-graph spans clean
     if (const char* v = getenv("CVY_ATTN_EARLY")) P.attn_early = atoi(v);  // A/B knob
     P.vtab = e->d_vtab;
     P.vlen = e->d_vlen;
