@@ -700,20 +700,21 @@ def latency_pages(router, workloads=AB_WORKLOADS):
 
 
 def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flags=0, dm=None, indices=None,
-                reps=1, des=None):
+                reps=1, des=None, runtime="native"):
     """Request completion latency with tool partial execution vs sequential tool execution on
     the workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool costs
     in both modes (the baseline is the same code with partial execution
     disabled).  `indices(w)`: the global request indices this rank serves (router).  Each
     (workload, mode) runs `reps` times, modes interleaved.  `des`: a schedule model passed to
     runtime.summarize (the GPU tests pass the oracle's O-3 DES; bench.py never does).
+    `runtime`: "native" (cvy_runtime_*, C++ poller / executors / driver) or "python".
     Returns {workload: {...}}."""
     from inputs.configs import MISTRAL_7B
     from inputs.tool_workloads import TOOLS, build
     from inputs.vocab import synthetic_vocab
     from paper_2406_00059_b200 import capi
     from paper_2406_00059_b200.engine import DeviceModel, Engine
-    from paper_2406_00059_b200.runtime import Runtime, summarize
+    from paper_2406_00059_b200.runtime import NativeRuntime, Runtime, summarize
     import numpy as np
     idx = {w: (list(range(batches[w])) if indices is None else indices(w)) for w in workloads}
     pages_per = {w: (LAT_PREFIX[w] + LAT_TOKENS[w] + 31) // 16 + 1 for w in workloads}
@@ -732,7 +733,7 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flag
         for rep in range(reps):
             for mode, label in ((capi.MODE_PARTIAL, "partial"), (capi.MODE_SEQUENTIAL, "sequential")):
                 _, specs = build(w, batches[w], tool_ids, indices=idx[w])
-                rt = Runtime(eng, mode)
+                rt = NativeRuntime(eng, mode) if runtime == "native" else Runtime(eng, mode)
                 t0 = time.perf_counter()
                 c0 = time.process_time()
                 logs = rt.run(specs, max_inflight=inflight)
@@ -744,7 +745,7 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flag
                 s["dispatch_cpu_s"] = rt.dispatch_cpu_s
                 s["lat_ms"] = [(lg.t_done - lg.t_submit) * 1e3 for lg in logs]
                 if inflight:
-                    span = max(lg.t_done for lg in logs) - t0
+                    span = max(lg.t_done for lg in logs) - min(lg.t_submit for lg in logs)
                     s.update(makespan_s=span, requests_per_s=len(logs) / span, slots=inflight)
                 res[label].append(s)
                 if verbose:

@@ -358,6 +358,114 @@ cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap,
 cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int32_t N, int32_t K, int32_t B,
                           int32_t iters, int32_t device, float* ms);
 
+/* ======================================================================================
+ * Native host runtime: the scheduler of PAPER.md:146 (Fig. 4)
+ * above the engine, in C++ threads (no interpreter lock on the path):
+ *   (1) requests are submitted (cvy_submit_request), (2) the calling thread runs decoding
+ *   iterations back to back (cvy_step: continuous batching), (8) a poller thread drains the
+ *   pinned segment ring (cvy_poll_segments) while decoding continues, and (6)/(7) tool
+ *   executors run the pieces on worker threads beside decoding;
+ *   Partial mode dispatches every piece the moment it is polled ("tool partial execution",
+ *   PAPER.md:39, :144); Sequential mode holds a round's pieces until its FINAL record ("tool
+ *   invocation always happens after decoding to the EOS"; reading R15);
+ *   when a round's FINAL is in and all its pieces have executed, the round's observation is
+ *   fed back (cvy_inject_observation, step (g)) and the next round decodes;
+ *   a piece whose plan says `abort` cancels its request when it completes (the validator,
+ *   PAPER.md:187, :223); with max_inflight > 0 a finished / aborted request's slot is
+ *   released at once and the next queued request admitted (abort-and-refill, NEXT-3).
+ * Pieces of one (request, round, instance) run serially in arrival order; instances run in
+ * parallel (up to n_workers at a time); a piece also waits for its dependencies (earlier
+ * pieces of the round: planning DAGs).  What a tool does with a piece is the
+ * plan callback's business: it maps a piece (bytes, flags) to {skip, cost, instance, deps,
+ * abort}; the built-in executor then occupies a worker for `cost_ms` (a tool stub with the
+ * caller's seeded cost model; a real tool would run there).  All times are seconds on the
+ * host steady clock, relative to cvy_runtime_run's start.
+ * ====================================================================================== */
+typedef struct cvy_runtime cvy_runtime;
+
+/* Plan of one piece (filled by the plan callback; zero-initialised before the call). */
+typedef struct {
+    int32_t skip;        /* 1: not tool input (e.g. a FENCE marker, a drafted code line) */
+    int32_t abort;       /* 1: cancel the request when this piece completes (validator) */
+    double cost_ms;      /* executor time of the piece                                   */
+    int32_t instance;    /* tool instance: pieces of one instance run serially           */
+    uint32_t n_deps;     /* <= 8 indices of earlier accepted pieces of the same round    */
+    int32_t deps[8];
+} cvy_piece_plan;
+
+/* Called on the poller thread for every polled piece (a non-FINAL record, or a FINAL with
+ * bytes) of a round bound to a tool.  piece = index among the round's accepted pieces so far
+ * (a skipped piece does not consume an index).  request = index into cvy_runtime_run's array. */
+typedef void (*cvy_plan_fn)(void* user, uint32_t request, uint32_t round, uint32_t piece, const uint8_t* data,
+                            uint32_t len, uint16_t flags, cvy_piece_plan* out);
+
+typedef struct {
+    cvy_exec_mode mode;
+    uint32_t n_workers;     /* executor threads (>= 1)                                  */
+    uint32_t max_inflight;  /* 0: submit every request at t = 0                         */
+    cvy_plan_fn plan;       /* required                                                 */
+    void* plan_user;
+    uint32_t poll_sleep_us; /* poller back-off when the ring is empty (0: 20 us)        */
+} cvy_runtime_config;
+
+typedef struct {
+    const int32_t* forced;      /* teacher-forced generated tokens of the round (>= 1)  */
+    uint32_t forced_len;
+    int32_t tool_id;            /* -1: no tool                                          */
+    const int32_t* observation; /* tokens injected after the round (before the next)    */
+    uint32_t observation_len;
+} cvy_round_desc;
+
+typedef struct {
+    const int32_t* prompt;
+    uint32_t prompt_len;
+    uint32_t synth_prefix_len;
+    uint64_t synth_seed;
+    const cvy_round_desc* rounds;
+    uint32_t n_rounds;          /* >= 1 */
+} cvy_rt_request;
+
+/* Per request / round / piece logs (the inputs of the paper's latency model). */
+typedef struct {
+    uint64_t req_id;
+    double t_submit, t_done, t_abort; /* t_abort < 0: not aborted */
+    uint32_t n_rounds_run;
+    uint32_t aborted;
+} cvy_rt_request_log;
+typedef struct {
+    double t_start, t_final;          /* round start (submit / injection) and FINAL polled */
+    uint32_t n_pieces;
+} cvy_rt_round_log;
+typedef struct {
+    double t_avail, t_dispatch, t_begin, t_end; /* polled, released to the tool, started, done */
+    double cost_ms;
+    int32_t instance;
+    uint32_t token_index;
+    uint32_t n_deps;
+    int32_t deps[8];
+} cvy_rt_piece_log;
+typedef struct {
+    uint64_t steps, records, pieces, injections, cancels;
+    double wall_s;
+    double poller_cpu_s;    /* poller thread CPU time (polling + planning + dispatch)     */
+    double dispatch_cpu_s;  /* of which: handling polled records                          */
+    double driver_cpu_s;    /* the calling thread (cvy_step loop)                         */
+    double worker_cpu_s;    /* executor threads (stub executors sleep: ~0)                */
+} cvy_rt_stats;
+
+cvy_status cvy_runtime_create(cvy_engine* e, const cvy_runtime_config* cfg, cvy_runtime** out);
+/* Runs every request to completion (copies the descriptors; blocks the calling thread, which
+ * drives cvy_step).  E_INVAL bad descriptors, E_FULL a request could not be admitted even
+ * with the engine idle, E_STATE timeout or an engine error (see cvy_last_error).  May be
+ * called again: each call replaces the previous logs. */
+cvy_status cvy_runtime_run(cvy_runtime* rt, const cvy_rt_request* reqs, uint32_t n, double timeout_s);
+cvy_status cvy_runtime_request_log(cvy_runtime* rt, uint32_t request, cvy_rt_request_log* out);
+cvy_status cvy_runtime_round_log(cvy_runtime* rt, uint32_t request, uint32_t round, cvy_rt_round_log* out);
+cvy_status cvy_runtime_piece_log(cvy_runtime* rt, uint32_t request, uint32_t round, uint32_t piece,
+                                 cvy_rt_piece_log* out);
+cvy_status cvy_runtime_stats(cvy_runtime* rt, cvy_rt_stats* out);
+void cvy_runtime_destroy(cvy_runtime* rt);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,8 +7,8 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libconveyor.so")
-SOURCES = ["engine.cu"]
-DEPS = ["engine.cu", "common.cuh", "epilogue.cuh", "gemm_sm100.cuh", "kernels.cuh", "attention_tc.cuh", "step_params.h"]
+SOURCES = ["engine.cu", "runtime.cpp"]
+DEPS = ["engine.cu", "common.cuh", "epilogue.cuh", "gemm_sm100.cuh", "kernels.cuh", "attention_tc.cuh", "step_params.h", "runtime.cpp"]
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

@@ -93,6 +93,52 @@ class PerfInfo(ctypes.Structure):
 
 assert ctypes.sizeof(Segment) == 40
 
+# ------------------------------------------------------------------ native host runtime
+class PiecePlan(ctypes.Structure):
+    _fields_ = [("skip", c_i32), ("abort", c_i32), ("cost_ms", ctypes.c_double), ("instance", c_i32),
+                ("n_deps", c_u32), ("deps", c_i32 * 8)]
+
+
+PLAN_FN = ctypes.CFUNCTYPE(None, c_vp, c_u32, c_u32, c_u32, ctypes.POINTER(ctypes.c_uint8), c_u32, ctypes.c_uint16,
+                           ctypes.POINTER(PiecePlan))
+
+
+class RuntimeConfig(ctypes.Structure):
+    _fields_ = [("mode", c_i32), ("n_workers", c_u32), ("max_inflight", c_u32), ("plan", PLAN_FN),
+                ("plan_user", c_vp), ("poll_sleep_us", c_u32)]
+
+
+class RoundDesc(ctypes.Structure):
+    _fields_ = [("forced", ctypes.POINTER(c_i32)), ("forced_len", c_u32), ("tool_id", c_i32),
+                ("observation", ctypes.POINTER(c_i32)), ("observation_len", c_u32)]
+
+
+class RtRequest(ctypes.Structure):
+    _fields_ = [("prompt", ctypes.POINTER(c_i32)), ("prompt_len", c_u32), ("synth_prefix_len", c_u32),
+                ("synth_seed", c_u64), ("rounds", ctypes.POINTER(RoundDesc)), ("n_rounds", c_u32)]
+
+
+class RtRequestLog(ctypes.Structure):
+    _fields_ = [("req_id", c_u64), ("t_submit", ctypes.c_double), ("t_done", ctypes.c_double),
+                ("t_abort", ctypes.c_double), ("n_rounds_run", c_u32), ("aborted", c_u32)]
+
+
+class RtRoundLog(ctypes.Structure):
+    _fields_ = [("t_start", ctypes.c_double), ("t_final", ctypes.c_double), ("n_pieces", c_u32)]
+
+
+class RtPieceLog(ctypes.Structure):
+    _fields_ = [("t_avail", ctypes.c_double), ("t_dispatch", ctypes.c_double), ("t_begin", ctypes.c_double),
+                ("t_end", ctypes.c_double), ("cost_ms", ctypes.c_double), ("instance", c_i32),
+                ("token_index", c_u32), ("n_deps", c_u32), ("deps", c_i32 * 8)]
+
+
+class RtStats(ctypes.Structure):
+    _fields_ = [("steps", c_u64), ("records", c_u64), ("pieces", c_u64), ("injections", c_u64), ("cancels", c_u64),
+                ("wall_s", ctypes.c_double), ("poller_cpu_s", ctypes.c_double), ("dispatch_cpu_s", ctypes.c_double),
+                ("driver_cpu_s", ctypes.c_double), ("worker_cpu_s", ctypes.c_double)]
+
+
 # name -> (restype, argtypes): every symbol declared in include/conveyor.h
 PROTOTYPES = {
     "cvy_abi_version": (c_i32, []),
@@ -125,6 +171,13 @@ PROTOTYPES = {
     "cvy_stats_allgather": (c_i32, [ctypes.POINTER(c_vp), c_i32, ctypes.POINTER(c_u64)]),
     "cvy_debug_buffer": (c_i32, [c_vp, c_i32, c_vp, c_sz, ctypes.POINTER(c_sz)]),
     "cvy_debug_gemm": (c_i32, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, ctypes.POINTER(c_f32)]),
+    "cvy_runtime_create": (c_i32, [c_vp, ctypes.POINTER(RuntimeConfig), ctypes.POINTER(c_vp)]),
+    "cvy_runtime_run": (c_i32, [c_vp, ctypes.POINTER(RtRequest), c_u32, ctypes.c_double]),
+    "cvy_runtime_request_log": (c_i32, [c_vp, c_u32, ctypes.POINTER(RtRequestLog)]),
+    "cvy_runtime_round_log": (c_i32, [c_vp, c_u32, c_u32, ctypes.POINTER(RtRoundLog)]),
+    "cvy_runtime_piece_log": (c_i32, [c_vp, c_u32, c_u32, c_u32, ctypes.POINTER(RtPieceLog)]),
+    "cvy_runtime_stats": (c_i32, [c_vp, ctypes.POINTER(RtStats)]),
+    "cvy_runtime_destroy": (None, [c_vp]),
 }
 
 _lib = None

@@ -415,6 +415,9 @@ bool model_ok(const cvy_model_config* m, std::string* why) {
 
 }  // namespace
 
+// the native runtime (runtime.cpp) reports its errors through the same thread-local message
+cvy_status cvy_internal_fail(cvy_status st, const std::string& msg) { return fail(st, msg); }
+
 // ============================================================================ C ABI
 extern "C" {
 

@@ -298,6 +298,110 @@ class Runtime:
         return logs
 
 
+class NativeRuntime:
+    """The same scheduler in C++ behind the ABI (cvy_runtime_*, runtime.cpp): a native poller
+    thread, n_workers executor threads (the plan's cost occupies a worker: a tool stub), the
+    calling thread driving cvy_step.  Python is entered only through the plan callback, once
+    per polled piece.  run() returns RequestLog objects like Runtime.run, so summarize /
+    round_timelines / timeline.py work unchanged."""
+
+    def __init__(self, eng, mode: int, n_workers: int = 64, poll_sleep_us: int = 20):
+        self.eng = eng
+        self.mode = mode
+        self.n_workers = n_workers
+        self.poll_sleep_us = poll_sleep_us
+        self.steps = 0
+        self.poller_cpu_s = 0.0
+        self.dispatch_cpu_s = 0.0
+        self.stats = None
+
+    def run(self, specs: list[RequestSpec], timeout_s: float = 600.0, max_inflight: int | None = None):
+        import ctypes
+        from .capi import check
+        L = capi.lib()
+        errors = []
+
+        def plan_cb(user, request, rnd, piece, data, n, flags, out):
+            try:
+                rd = specs[request].rounds[rnd]
+                work = rd.plan(piece, ctypes.string_at(data, n) if n else b"", flags) if rd.plan else None
+                o = out.contents
+                if work is None:
+                    o.skip = 1
+                    return
+                o.cost_ms = float(work.cost_s) * 1e3
+                o.instance = int(work.instance)
+                deps = list(work.deps)[:8]
+                o.n_deps = len(deps)
+                for k, d in enumerate(deps):
+                    o.deps[k] = int(d)
+                o.abort = 1 if work.abort else 0
+            except Exception as exc:  # never unwind into C
+                errors.append(exc)
+                out.contents.skip = 1
+
+        cb = capi.PLAN_FN(plan_cb)
+        cfg = capi.RuntimeConfig(self.mode, self.n_workers, max_inflight or 0, cb, None, self.poll_sleep_us)
+        h = ctypes.c_void_p()
+        check(L.cvy_runtime_create(self.eng.h, ctypes.byref(cfg), ctypes.byref(h)))
+        keep = []
+        reqs = (capi.RtRequest * len(specs))()
+        for i, sp in enumerate(specs):
+            arr = lambda xs: (ctypes.c_int32 * max(1, len(xs)))(*xs)
+            rds = (capi.RoundDesc * len(sp.rounds))()
+            for k, rd in enumerate(sp.rounds):
+                f, o = arr(rd.forced), arr(rd.observation)
+                keep += [f, o]
+                rds[k] = capi.RoundDesc(f, len(rd.forced), rd.tool_id, o, len(rd.observation))
+            pr = arr(sp.prompt)
+            keep += [rds, pr]
+            reqs[i] = capi.RtRequest(pr, len(sp.prompt), sp.synth_prefix, sp.synth_seed, rds, len(sp.rounds))
+        try:
+            check(L.cvy_runtime_run(h, reqs, len(specs), float(timeout_s)))
+            if errors:
+                raise errors[0]
+            logs = []
+            for i, sp in enumerate(specs):
+                rl = capi.RtRequestLog()
+                check(L.cvy_runtime_request_log(h, i, ctypes.byref(rl)))
+                lg = RequestLog(sp, rid=rl.req_id, t_submit=rl.t_submit, t_done=rl.t_done,
+                                t_abort=rl.t_abort if rl.aborted else None, done=True, released=True)
+                for r in range(rl.n_rounds_run):
+                    ro = capi.RtRoundLog()
+                    check(L.cvy_runtime_round_log(h, i, r, ctypes.byref(ro)))
+                    lg.round_start.append(ro.t_start)
+                    lg.round_final.append(ro.t_final if ro.t_final >= 0 else None)
+                    cols = ([], [], [], [], [], [])
+                    for j in range(ro.n_pieces):
+                        pl = capi.RtPieceLog()
+                        check(L.cvy_runtime_piece_log(h, i, r, j, ctypes.byref(pl)))
+                        cols[0].append(pl.t_avail)
+                        cols[1].append(SegmentWork(pl.cost_ms / 1e3, pl.instance, [pl.deps[k] for k in range(pl.n_deps)]))
+                        cols[2].append(pl.t_end if pl.t_end >= 0 else None)
+                        cols[3].append(pl.t_dispatch if pl.t_dispatch >= 0 else None)
+                        cols[4].append(pl.t_begin if pl.t_begin >= 0 else None)
+                        cols[5].append(pl.token_index)
+                    lg.seg_avail.append(cols[0])
+                    lg.seg_work.append(cols[1])
+                    lg.seg_end.append(cols[2])
+                    lg.seg_disp.append(cols[3])
+                    lg.seg_begin.append(cols[4])
+                    lg.seg_token.append(cols[5])
+                lg.round = max(0, rl.n_rounds_run - 1)
+                lg.final_seen = True
+                logs.append(lg)
+            st = capi.RtStats()
+            check(L.cvy_runtime_stats(h, ctypes.byref(st)))
+            self.stats = {f: getattr(st, f) for f, _ in capi.RtStats._fields_}
+            self.steps = st.steps
+            self.poller_cpu_s = st.poller_cpu_s
+            self.dispatch_cpu_s = st.dispatch_cpu_s
+            return logs
+        finally:
+            L.cvy_runtime_destroy(h)
+            del keep
+
+
 def round_timelines(log: RequestLog):
     """Per round of one request: decode time g (round start -> FINAL polled) and the logged
     segments as (availability offset, cost, instance, deps) -- the inputs of the paper's

@@ -10,7 +10,7 @@ from paper_2406_00059_b200 import capi
 from paper_2406_00059_b200.engine import DeviceModel, Engine
 flags = int(os.environ.get("FLAGS", "0"))
 B = int(os.environ.get("B", "64"))
-vocab, reqs = bench.codegen_workload(B, 40)
+vocab, reqs = bench.workload_requests("codegen", range(B), 40)
 dm = DeviceModel(MISTRAL_7B, "bf16", B * 40 + 64, seed=1001)
 eng = Engine(dm, vocab, max_slots=B, max_pages_per_slot=40, flags=flags)
 tool = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n"])

@@ -3,7 +3,8 @@
 // ring (cvy_poll_segments: "exactly one consumer thread"), and a third thread submits and
 // cancels requests concurrently (applied at the next step boundary).  Built with
 // -fsanitize=thread together with a ThreadSanitizer build of libconveyor
-// (scripts/tsan.sh); run on a B200.  Exit code 0 = contract exercised without errors;
+// (scripts/tsan.sh); run on a B200.  A second phase runs the native runtime (cvy_runtime_*:
+// driver, poller and executor threads) over 16 requests in both modes with aborts and refill.  Exit code 0 = contract exercised without errors;
 // TSan reports go to stderr (halt_on_error=1 makes any race fatal).
 #include <cuda_runtime.h>
 
@@ -166,10 +167,68 @@ int main() {
     stop.store(true);
     client.join();
     poller.join();
+    {
+        // drain, then release everything still held so the native runtime below starts clean
+        std::vector<cvy_segment> recs(256);
+        uint32_t n = 0;
+        size_t used = 0;
+        while (cvy_poll_segments(e, recs.data(), (uint32_t)recs.size(), &n, nullptr, 0, &used) == CVY_OK) {
+        }
+        std::lock_guard<std::mutex> g(mu);
+        for (uint64_t id : live) {
+            cvy_cancel_request(e, id);
+        }
+        for (int s = 0; s < 4; ++s) CHECK(cvy_step(e, nullptr));
+        CHECK(cvy_sync(e));
+        while (cvy_poll_segments(e, recs.data(), (uint32_t)recs.size(), &n, nullptr, 0, &used) == CVY_OK) {
+        }
+        for (uint64_t id : live) cvy_release_request(e, id);
+    }
+    // the native runtime (cvy_runtime_*): its driver / poller / worker threads under TSan,
+    // with a plan callback that aborts some requests and spreads pieces over 2 instances
+    uint64_t rt_pieces = 0;
+    for (int mode = 0; mode < 2; ++mode) {
+        cvy_runtime_config rc{};
+        rc.mode = mode == 0 ? CVY_MODE_PARTIAL : CVY_MODE_SEQUENTIAL;
+        rc.n_workers = 4;
+        rc.max_inflight = 4;
+        rc.plan = [](void*, uint32_t request, uint32_t, uint32_t piece, const uint8_t*, uint32_t, uint16_t,
+                     cvy_piece_plan* out) {
+            out->cost_ms = 0.2;
+            out->instance = (int32_t)(piece % 2);
+            if (piece >= 2) {
+                out->n_deps = 1;
+                out->deps[0] = (int32_t)piece - 2;
+            }
+            out->abort = (request % 3 == 1 && piece == 3) ? 1 : 0;
+        };
+        cvy_runtime* rt = nullptr;
+        CHECK(cvy_runtime_create(e, &rc, &rt));
+        std::vector<cvy_round_desc> rounds(16);
+        std::vector<cvy_rt_request> reqs(16);
+        int32_t prompt[2] = {'#', '\n'};
+        const int32_t obs[3] = {'o', 'k', '\n'};
+        for (int i = 0; i < 16; ++i) {
+            rounds[i] = cvy_round_desc{forced.data(), (uint32_t)forced.size(), tool, obs, 3};
+            reqs[i] = cvy_rt_request{prompt, 2, (uint32_t)(i % 7), (uint64_t)i, &rounds[i], 1};
+        }
+        CHECK(cvy_runtime_run(rt, reqs.data(), 16, 120.0));
+        cvy_rt_stats st{};
+        CHECK(cvy_runtime_stats(rt, &st));
+        rt_pieces += st.pieces;
+        for (uint32_t i = 0; i < 16; ++i) {
+            cvy_rt_request_log lg{};
+            CHECK(cvy_runtime_request_log(rt, i, &lg));
+            if (lg.t_done < lg.t_submit) return 8;
+        }
+        cvy_runtime_destroy(rt);
+    }
     cvy_engine_destroy(e);
     for (void* b : bufs) cudaFree(b);
-    std::printf("tsan driver ok: %llu submitted, %llu cancel calls, %llu records, %llu FINAL\n",
+    std::printf("tsan driver ok: %llu submitted, %llu cancel calls, %llu records, %llu FINAL; native runtime: "
+                "%llu pieces executed over 2 x 16 requests\n",
                 (unsigned long long)n_submitted.load(), (unsigned long long)n_cancel.load(),
-                (unsigned long long)n_records.load(), (unsigned long long)n_final.load());
+                (unsigned long long)n_records.load(), (unsigned long long)n_final.load(),
+                (unsigned long long)rt_pieces);
     return n_final.load() > 0 ? 0 : 7;
 }

@@ -153,8 +153,10 @@ def test_codegen_only_last_line_after_decode(monkeypatch):
 
 
 @pytest.mark.gpu
-def test_engine_latency_matches_des_and_partial_wins():
-    """S13 on the real engine (2-layer 7B slice, 32k vocab, CUDA graphs): the runtime's measured
+@pytest.mark.parametrize("runtime", ["native", "python"])
+def test_engine_latency_matches_des_and_partial_wins(runtime):
+    """S13 on the real engine (2-layer 7B slice, 32k vocab, CUDA graphs), through the native C++
+    runtime (cvy_runtime_*) and the Python one: the runtime's measured
     request latencies agree with the oracle's O-3 DES recomputed from each request's logged
     round / segment timeline, in both modes, and partial execution beats
     sequential execution on every workload shape; validation aborts are detected earlier in
@@ -166,7 +168,7 @@ def test_engine_latency_matches_des_and_partial_wins():
     w = ["codegen", "search", "planning", "validation"]
     batches = {"codegen": 8, "search": 8, "planning": 8, "validation": 16}
     dm = DeviceModel(shape, "bf16", 16 * 200, seed=1002)
-    res = bench.run_latency(w, batches, dm=dm, des=oracle_des)
+    res = bench.run_latency(w, batches, dm=dm, des=oracle_des, runtime=runtime)
     for name, row in res.items():
         assert row["partial_mean_ms"] < row["sequential_mean_ms"], (name, row["improvement"])
         for mode in ("partial", "sequential"):
@@ -176,6 +178,25 @@ def test_engine_latency_matches_des_and_partial_wins():
             elif name != "validation":
                 raise AssertionError(f"{name} {mode}: no DES cross-check")
     assert res["validation"]["detection_partial_ms"] < res["validation"]["detection_sequential_ms"]
+
+
+@pytest.mark.gpu
+def test_native_runtime_refill_and_abort():
+    """NEXT-3 through the native runtime: 24 validation requests through 6 slots
+    (max_inflight); every request completes, aborted ones are cancelled when the validator's
+    offending member executes, and Partial finishes the
+    queue sooner than Sequential."""
+    import bench
+    from inputs.configs import MISTRAL_7B, slice_of
+    from paper_2406_00059_b200.engine import DeviceModel
+    dm = DeviceModel(slice_of(MISTRAL_7B, L=2, name="7b-L2"), "bf16", 6 * 140, seed=1002)
+    res = bench.run_latency(["validation"], {"validation": 24}, dm=dm, inflight=6, runtime="native")
+    row = res["validation"]
+    for mode in ("partial", "sequential"):
+        r = row["runs"][mode][0]
+        assert r["n"] == 24 and r["aborted"] > 0, r
+    assert row["throughput_gain"] > 0, row["throughput_gain"]
+    assert row["detection_partial_ms"] < row["detection_sequential_ms"]
 
 
 # ------------------------------------------------------------------ NEXT-4: Fig. 6 sweep
