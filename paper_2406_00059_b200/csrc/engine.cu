@@ -1272,7 +1272,6 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
             *why = "tile-major weights need 64-element k-blocks (batch tiles of <= 128 columns)";
             return false;
         }
-        if (g.wtiled) g.l2_prefetch = 0;
         // tile-major: a [rows * K / 64][64] view, box = one 128-row x 64-column tile (16 KB)
         if (!(g.wtiled ? make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total * K / 64, 64, 64, 128, 64)
                        : make_tmap(&gp.tmW, Wbase, (uint64_t)L_rows_total, (uint64_t)K, (uint64_t)K,

@@ -233,10 +233,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
                 load_w_tile<NSUB, BK>(smem + (size_t)i * stage_bytes, &tmW, &full_bar[i], G, tile, kb, pol_w);
             }
-            // deeper look-ahead into L2 while the previous kernel drains (HBM would idle otherwise)
+            // look-ahead into L2 beyond the smem ring (l2_prefetch k-blocks, rolling with the main
+            // loop): more weight bytes in flight per SM than the ring holds
+            auto l2_pf = [&](long long it) {
+                const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
+                if (!G.wtiled) {
+                    tma_prefetch_l2_2d(&tmW, kb * BK, G.w_row0 + tile * rows_per_tile);
+                } else {
+#pragma unroll
+                    for (int s = 0; s < NSUB; ++s)
+                        tma_prefetch_l2_2d(&tmW, 0, ((G.w_row0 / 128 + tile * NSUB + s) * G.kblocks + kb) * 128);
+                }
+            };
+            long long pf_next = it0 + pre;
             const long long pf_end = min(it1, it0 + pre + (long long)G.l2_prefetch);
-            for (long long it = it0 + pre; it < pf_end && !G.wtiled; ++it)
-                tma_prefetch_l2_2d(&tmW, (int)(it % G.kblocks) * BK, G.w_row0 + (int)(it / G.kblocks) * rows_per_tile);
+            for (; pf_next < pf_end; ++pf_next) l2_pf(pf_next);
             pdl_wait();
             if (G.epi.span_kind >= 0) span_begin(P.spans, P.span_base + G.epi.layer * 8 + G.epi.span_kind);
             for (int i = 0; i < pre; ++i) {
@@ -252,6 +263,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (long long it = it0 + pre; it < it1; ++it) {
                 const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
+                if (G.l2_prefetch > 0 && pf_next < it1) l2_pf(pf_next++);
                 uint8_t* sw = smem + (size_t)stage * stage_bytes;
                 mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
                 load_w_tile<NSUB, BK>(sw, &tmW, &full_bar[stage], G, tile, kb, pol_w);
