@@ -124,9 +124,15 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
                 if (lane == 0)
                     for (int c = 0; c < 2; ++c) {
                         const int row0 = ((((layer * P.n_pages + page) * 2 + c) * P.Hkv) + g) * 16;
-                        for (int h = 0; h < HALVES; ++h)
-                            tma_load_2d(stages + (size_t)st * STAGE + (size_t)(p * 2 + c) * BLK + h * 2048, &tmKV,
-                                        &full_bar[st], h * 64, row0, pol);
+                        uint8_t* dst = stages + (size_t)st * STAGE + (size_t)(p * 2 + c) * BLK;
+                        if (HALVES == 2 && P.kv_tma3d) {
+                            // the whole 4 KB block in one box: [2 halves][16 rows][64], the same
+                            // shared-memory image as the two 2D boxes
+                            tma_load_3d(dst, &tmKV, &full_bar[st], 0, row0, 0, pol);
+                        } else {
+                            for (int h = 0; h < HALVES; ++h)
+                                tma_load_2d(dst + h * 2048, &tmKV, &full_bar[st], h * 64, row0, pol);
+                        }
                     }
             }
         };

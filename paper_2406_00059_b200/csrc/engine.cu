@@ -83,6 +83,22 @@ bool make_tmap(CUtensorMap* out, const void* base, uint64_t rows, uint64_t cols,
     return r == CUDA_SUCCESS;
 }
 
+// 3D view of a [rows][128] bf16 KV pool: dims (64 elements, rows, 2 halves), strides 256 B
+// (row) and 128 B (half); box (64, 16, 2) = one 4 KB block, 128B swizzle per 128-byte row,
+// landing in shared memory as [half][16 rows][64] (the layout of two 16 x 64 2D boxes).
+bool make_tmap_kv3(CUtensorMap* out, const void* base, uint64_t rows) {
+    auto fn = get_encode_fn();
+    if (!fn) return false;
+    cuuint64_t gdim[3] = {64, rows, 2};
+    cuuint64_t gstride[2] = {256, 128};
+    cuuint32_t box[3] = {64, 16, 2};
+    cuuint32_t estride[3] = {1, 1, 1};
+    CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gdim, gstride, box, estride,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Tile/pipeline configuration of the tcgen05 GEMM for a padded batch Bp.
 //   Bp <= 128: 2 sub-tiles (256 weight rows) per tile, hi/lo planes merged (MMA N = 2*Bp)
 //   Bp 160..256: 1 sub-tile, planes as two MMAs into one accumulator (N = Bp)
@@ -357,7 +373,8 @@ struct cvy_engine {
     int attn_pps = 2;           // KV pages per attention stage: 2 x 2 stages = 32 KB of ring per CTA,
                                 // 6 CTAs per SM, so the decode grid (Hkv x B) runs in one wave
                                 // (measured at B=64: attention -3..6% vs 4 pages x 3 stages)
-    CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd]
+    CUtensorMap tm_kv;          // 2D view of the KV pool: [L*pages*2*Hkv*16 rows][hd] (3D when kv_tma3d)
+    bool kv_tma3d = false;
     // chunked prefill (NEXT-1): row tables and activation buffers of a prefill pass
     float* d_px = nullptr;
     void* d_pact = nullptr;
@@ -725,7 +742,12 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     e->attn_tc = e->bf16 && (hd == 64 || hd == 128) && (H / Hkv) <= 4;
     if (e->attn_tc) {
         const uint64_t rows = (uint64_t)m->n_layers * ec->n_pages * 2 * Hkv * kPageTokens;
-        if (!make_tmap(&e->tm_kv, w->kv_pool, rows, (uint64_t)hd, (uint64_t)hd, 16, 64)) {
+        // hd 128: a 3D view (64 dims, rows, 2 halves; strides 256 B and 128 B) so one TMA box
+        // moves a whole 4 KB (page, K/V, kv-head) block (CVY_KV_TMA3D=0: two 2D boxes)
+        e->kv_tma3d = hd == 128;
+        if (const char* v = getenv("CVY_KV_TMA3D")) e->kv_tma3d = e->kv_tma3d && atoi(v) != 0;
+        if (e->kv_tma3d && !make_tmap_kv3(&e->tm_kv, w->kv_pool, rows)) e->kv_tma3d = false;
+        if (!e->kv_tma3d && !make_tmap(&e->tm_kv, w->kv_pool, rows, (uint64_t)hd, (uint64_t)hd, 16, 64)) {
             cvy_engine_destroy(e);
             return fail(CVY_E_CUDA, "KV tensor map encode failed");
         }
@@ -1204,6 +1226,7 @@ StepParams base_params(cvy_engine* e, int Bp) {
     const int want = cells >= e->num_sms ? 1 : (2 * e->num_sms + cells - 1) / cells;
     P.attn_splits = std::max(1, std::min(e->attn_splits_max, want));
     if (const char* as = getenv("CVY_ATTN_SPLITS")) P.attn_splits = std::max(1, std::min(e->attn_splits_max, atoi(as)));
+    P.kv_tma3d = e->kv_tma3d ? 1 : 0;
     P.attn_early = 0;  // measured neutral; off keeps the in-graph spans clean
     if (const char* v = getenv("CVY_ATTN_EARLY")) P.attn_early = atoi(v);  // A/B knob
     P.vtab = e->d_vtab;

@@ -110,6 +110,7 @@ struct StepParams {
     float* attn_part;           // [Bmax][Hkv][nsplit][G*(hd+2)]
     int32_t attn_splits;
     int32_t attn_early;         // attention_tc: issue old-page TMA loads before the PDL wait (1)
+    int32_t kv_tma3d;           // attention_tc, hd 128: the KV tensor map is 3D, one box per 4 KB block
     // scan / publish
     const uint8_t* vtab;        // [V][16]
     const uint8_t* vlen;        // [V]
