@@ -437,6 +437,41 @@ def test_submit_errors_and_full():
     eng.close()
 
 
+def test_degenerate_cases_bitexact():
+    """Degenerate inputs: a step with no request in flight is a no-op (no records, no error);
+    one-token rounds (LITERAL and JSON tools) give exactly one FINAL holding that token's bytes;
+    a stream made only of zero-byte special tokens gives one empty FINAL; a stream without any
+    delimiter gives one FINAL with all bytes; max_new_tokens = 1 free-running generates exactly
+    one token.  Records bit-exact against the oracle's round_records."""
+    vocab = synthetic_vocab(32000)
+    shape = slice_of(TINY, L=2, V=32000, name="tiny-v32k")
+    dm, eng = make_engine(shape, "bf16", vocab, 8, 1014, max_pages_per_slot=8)
+    lit = eng.register_tool("interp", capi.PARSER_LITERAL, [b"\n"])
+    js = eng.register_tool("validator", capi.PARSER_JSON_MEMBER)
+    for _ in range(3):  # nothing in flight
+        eng.step()
+    eng.sync()
+    assert eng.poll_segments() == []
+    tok = Tokenizer(vocab)
+    nl = tok.encode("print(1)\n")[-1]
+    cases = [(lit, capi.PARSER_LITERAL, [b"\n"], [nl]),                     # one token holding the delimiter
+             (js, capi.PARSER_JSON_MEMBER, [], tok.encode("{")[:1]),          # one token, no cut
+             (lit, capi.PARSER_LITERAL, [b"\n"], [0, 1, 0]),                  # zero-byte specials only
+             (lit, capi.PARSER_LITERAL, [b"\n"], tok.encode("x = 1 + 2 no newline"))]
+    rids = [eng.submit_request([1], len(f), tool_id=t, forced=f) for t, _, _, f in cases]
+    free = eng.submit_request([1, 5], 1)
+    for _ in range(24):
+        eng.step()
+    eng.sync()
+    got = group_records(eng.poll_segments())
+    okind = {capi.PARSER_LITERAL: oracle.PARSER_LITERAL, capi.PARSER_JSON_MEMBER: oracle.PARSER_JSON_MEMBER}
+    for rid, (_, kind, delims, forced) in zip(rids, cases):
+        assert as_tuples(got[rid]) == expected_records(forced, vocab, okind[kind], delims), forced
+    assert len(eng.round_tokens(free)) == 1 and eng.request_state(free) == 1
+    assert [r.flags & capi.SEG_FINAL for r in got.get(free, [])] in ([], [capi.SEG_FINAL])
+    eng.close()
+
+
 def test_tool_registration_errors():
     dm, eng = make_engine(TINY, "bf16", BYTE_VOCAB, 1, 1012)
     eng.register_tool("a", capi.PARSER_LITERAL, [b"\n"])
