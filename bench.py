@@ -468,7 +468,8 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             toks, secs, cores, n, steps = time_oracle(shape, reqs, args.cpu_budget, 1001, n_req=args.cpu_sample)
             cpu = {"value": toks / secs, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                   "sample": oracle_sample_text(name, n, steps, secs), "host": host_info()}
+                   "sample": oracle_sample_text(name, n, steps, secs), "host": host_info(),
+                   "extras": oracle_extras()}
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
                 "ms_per_step": max_ms / K, "ms_per_step_median": ms_med, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
@@ -561,6 +562,57 @@ def step_roofline(shape, ctx_now, B, ms_mean, ms_med, peaks):
                                "note": "projection flops count the (hi, lo) activation pair twice (DESIGN.md §4)"}}
 
 
+def _oracle_tiny_c0():
+    """SURVEY.md 8(d) "O-1 tiny: the full C0": 4 requests, the 7-byte prompt then 64 forced
+    bytes each, through the tiny model (fp32) one step at a time; prints one JSON line."""
+    import oracle
+    from inputs.configs import TINY
+    from inputs.workloads import codegen_script
+    prompt = list(b"# task\n")
+    rng = random.Random(7)
+    seqs = [prompt + list(codegen_script(rng, 6).encode())[:64] for _ in range(4)]
+    t0 = time.perf_counter()
+    w = oracle.Weights(TINY, 1000, bf16=False)
+    reqs = [oracle.Request(w, 128) for _ in seqs]
+    for t in range(len(seqs[0])):
+        oracle.step(reqs, [sq[t] for sq in seqs])
+    dt = time.perf_counter() - t0
+    print(json.dumps({"tokens": 4 * len(seqs[0]), "seconds": dt, "tokens_per_s": 4 * len(seqs[0]) / dt,
+                      "threads": oracle.num_threads()}))
+
+
+def oracle_extras():
+    """The rest of SURVEY.md 8(d)'s CPU-oracle protocol, bounded to a few seconds: O-1 tiny
+    (C0) at 1 OpenMP thread and at all cores (subprocesses: OMP_NUM_THREADS is read at load),
+    and O-2 segmentation throughput over the C1 (LITERAL) and C4 (JSON_MEMBER) forced streams."""
+    import oracle
+    from oracle.scan import round_records
+    out = {"omp_num_threads_env": os.environ.get("OMP_NUM_THREADS")}
+    for label, env in (("tiny_c0_1thread", {"OMP_NUM_THREADS": "1"}), ("tiny_c0_all_cores", {})):
+        e = dict(os.environ)
+        e.pop("OMP_NUM_THREADS", None)
+        e.update(env)
+        try:
+            r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-tiny"], env=e,
+                               capture_output=True, text=True, timeout=300)
+            out[label] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as exc:  # reported, never fatal to the bench line
+            out[label] = {"error": str(exc)[:200]}
+    from inputs.vocab import synthetic_vocab
+    vocab = synthetic_vocab(32000)
+    for wl, kind, delims in (("codegen", oracle.PARSER_LITERAL, [b"\n"]),
+                             ("validation", oracle.PARSER_JSON_MEMBER, [])):
+        _, reqs = workload_requests(wl, range(64), 256, 0)
+        nbytes = sum(sum(len(vocab[t]) for t in r["forced"]) for r in reqs)
+        ntok = sum(len(r["forced"]) for r in reqs)
+        t0 = time.perf_counter()
+        nrec = sum(len(round_records(r["forced"], vocab, kind, delims, 4096)[0]) for r in reqs)
+        dt = time.perf_counter() - t0
+        out[f"scan_{wl}"] = {"requests": 64, "tokens": ntok, "bytes": nbytes, "records": nrec, "seconds": dt,
+                             "MB_per_s": nbytes / dt / 1e6, "tokens_per_s": ntok / dt}
+    return out
+
+
 def host_info():
     model = None
     try:
@@ -637,8 +689,8 @@ def spawn_ranks(n: int) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)   # median of >= 200 steps
+    ap.add_argument("--warmup", type=int, default=20)   # after 20 warm-up steps
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="validation", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0, help="total batch over all ranks (default: the config's)")
@@ -656,8 +708,12 @@ def main():
     ap.add_argument("--chunked-prefill", action="store_true",
                     help="NEXT-1: prompts / observations as batched prefill passes (CVY_ENGINE_CHUNKED_PREFILL)")
     ap.add_argument("--fig6", action="store_true", help="NEXT-4: Fig. 6 tool/decode ratio sweep on the engine")
+    ap.add_argument("--oracle-tiny", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--fig6-batch", type=int, default=16)
     args = ap.parse_args()
+    if args.oracle_tiny:
+        _oracle_tiny_c0()
+        return
     if args.steps < 1:
         ap.error("--steps must be >= 1")
     if args.warmup < 3:
@@ -700,7 +756,7 @@ def latency_pages(router, workloads=AB_WORKLOADS):
 
 
 def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flags=0, dm=None, indices=None,
-                reps=1, des=None, runtime="native"):
+                reps=1, des=None, runtime="native", arrival_rate=None):
     """Request completion latency with tool partial execution vs sequential tool execution on
     the workload shapes (BASELINE.json configs[1..4]); identical seeded streams and tool costs
     in both modes (the baseline is the same code with partial execution
@@ -708,6 +764,9 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flag
     (workload, mode) runs `reps` times, modes interleaved.  `des`: a schedule model passed to
     runtime.summarize (the GPU tests pass the oracle's O-3 DES; bench.py never does).
     `runtime`: "native" (cvy_runtime_*, C++ poller / executors / driver) or "python".
+    `arrival_rate` {workload: requests/s of the whole job}: Poisson arrivals (seeded, identical
+    in both modes; native runtime) instead of all requests at t = 0; latency then runs from
+    each request's arrival.
     Returns {workload: {...}}."""
     from inputs.configs import MISTRAL_7B
     from inputs.tool_workloads import TOOLS, build
@@ -734,9 +793,19 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flag
             for mode, label in ((capi.MODE_PARTIAL, "partial"), (capi.MODE_SEQUENTIAL, "sequential")):
                 _, specs = build(w, batches[w], tool_ids, indices=idx[w])
                 rt = NativeRuntime(eng, mode) if runtime == "native" else Runtime(eng, mode)
+                arr = None
+                if arrival_rate and w in arrival_rate:
+                    # this rank's requests arrive as its share of a Poisson process of the job's rate
+                    share = len(idx[w]) / max(1, batches[w])
+                    g = random.Random(4242 + rep)
+                    t, arr = 0.0, []
+                    for _ in specs:
+                        t += g.expovariate(arrival_rate[w] * share)
+                        arr.append(t)
                 t0 = time.perf_counter()
                 c0 = time.process_time()
-                logs = rt.run(specs, max_inflight=inflight)
+                logs = rt.run(specs, max_inflight=inflight, arrivals=arr) if arr is not None else \
+                    rt.run(specs, max_inflight=inflight)
                 s = summarize(logs, mode, des=des)
                 s["steps"] = rt.steps
                 s["wall_s"] = time.perf_counter() - t0
@@ -771,6 +840,9 @@ def run_latency(workloads, batches, device=0, verbose=False, inflight=None, flag
     return out
 
 
+LAT_POISSON_RATE = {"codegen": 50.0, "validation": 250.0}  # requests/s of the whole job
+
+
 def run_latency_ab(dm, router, reps=3, device=0):
     """The latency half of the metric in the bench line: codegen (configs[1]) and validation
     (configs[4]), partial vs sequential, `reps` repetitions each, this rank serving its router
@@ -780,8 +852,10 @@ def run_latency_ab(dm, router, reps=3, device=0):
     import numpy as np
     res = run_latency(list(AB_WORKLOADS), LAT_BATCH, device=device, dm=dm, reps=reps,
                       indices=lambda w: router.mine(LAT_BATCH[w]))
+    res_p = run_latency(list(AB_WORKLOADS), LAT_BATCH, device=device, dm=dm, reps=reps,
+                        indices=lambda w: router.mine(LAT_BATCH[w]), arrival_rate=LAT_POISSON_RATE)
     out = {}
-    for w, row in res.items():
+    for w, row in list(res.items()) + [(w + "_poisson", r) for w, r in res_p.items()]:
         per_rank = gather_objects({m: [r["lat_ms"] for r in row["runs"][m]] for m in ("partial", "sequential")})
         lat = {m: [sum((pr[m][i] for pr in per_rank), []) for i in range(reps)] for m in ("partial", "sequential")}
         means = {m: [float(np.mean(x)) for x in lat[m]] for m in lat}
@@ -806,8 +880,10 @@ def run_latency_ab(dm, router, reps=3, device=0):
                        detection_sequential_ms=row["detection_sequential_ms"],
                        detection_speedup=row["detection_speedup"])
         out[w] = ent
-    out["protocol"] = ("all requests submitted at t=0; identical seeded streams and tool costs in both modes; "
-                       "modes interleaved per repetition; latency = submit -> completion on the host clock")
+    out["protocol"] = ("native C++ runtime (cvy_runtime_*); identical seeded streams and tool costs in both modes; "
+                       "modes interleaved per repetition; all requests submitted at t=0, and *_poisson: Poisson "
+                       f"arrivals at {LAT_POISSON_RATE} requests/s of the whole job (seeded per repetition, identical "
+                       "in both modes), latency from arrival; latency = submit/arrival -> completion on the host clock")
     return out
 
 

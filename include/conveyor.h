@@ -423,12 +423,16 @@ typedef struct {
     uint64_t synth_seed;
     const cvy_round_desc* rounds;
     uint32_t n_rounds;          /* >= 1 */
+    double t_arrival;           /* seconds after cvy_runtime_run starts (0: at start); requests
+                                   are admitted in arrival order once arrived (Poisson-arrival
+                                   latency protocol)                        */
 } cvy_rt_request;
 
 /* Per request / round / piece logs (the inputs of the paper's latency model). */
 typedef struct {
     uint64_t req_id;
-    double t_submit, t_done, t_abort; /* t_abort < 0: not aborted */
+    double t_arrival;                 /* as given; latency = t_done - t_arrival            */
+    double t_submit, t_done, t_abort; /* t_submit: admitted; t_abort < 0: not aborted      */
     uint32_t n_rounds_run;
     uint32_t aborted;
 } cvy_rt_request_log;

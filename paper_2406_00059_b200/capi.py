@@ -115,11 +115,13 @@ class RoundDesc(ctypes.Structure):
 
 class RtRequest(ctypes.Structure):
     _fields_ = [("prompt", ctypes.POINTER(c_i32)), ("prompt_len", c_u32), ("synth_prefix_len", c_u32),
-                ("synth_seed", c_u64), ("rounds", ctypes.POINTER(RoundDesc)), ("n_rounds", c_u32)]
+                ("synth_seed", c_u64), ("rounds", ctypes.POINTER(RoundDesc)), ("n_rounds", c_u32),
+                ("t_arrival", ctypes.c_double)]
 
 
 class RtRequestLog(ctypes.Structure):
-    _fields_ = [("req_id", c_u64), ("t_submit", ctypes.c_double), ("t_done", ctypes.c_double),
+    _fields_ = [("req_id", c_u64), ("t_arrival", ctypes.c_double), ("t_submit", ctypes.c_double),
+                ("t_done", ctypes.c_double),
                 ("t_abort", ctypes.c_double), ("n_rounds_run", c_u32), ("aborted", c_u32)]
 
 

@@ -69,6 +69,7 @@ struct Req {
     std::vector<std::vector<int32_t>> forced, obs;
     std::vector<int32_t> tool;
     uint32_t reserve = 0;
+    double t_arrival = 0;
     // state
     uint64_t rid = 0;
     bool submitted = false, final_seen = false, done = false, released = false;
@@ -96,8 +97,9 @@ struct cvy_runtime {
     std::condition_variable cv_driver, cv_work;
     std::vector<Req> reqs;
     std::unordered_map<uint64_t, uint32_t> by_rid;
-    std::deque<uint32_t> waiting;
-    uint32_t active = 0;
+    std::deque<uint32_t> waiting;  // not yet admitted, in arrival order
+    uint32_t active = 0;           // not finished
+    uint32_t inflight = 0;         // admitted, not finished
     std::map<std::tuple<uint32_t, uint32_t, int32_t>, Inst> inst;
     std::deque<Task> ready;
     bool stop = false;
@@ -126,10 +128,26 @@ struct cvy_runtime {
         cvy_status s = cvy_submit_request(e, &d, &r.rid);
         if (s != CVY_OK) return s;
         r.submitted = true;
+        inflight++;
         r.rounds.emplace_back();
         r.rounds.back().t_start = r.t_submit;
         by_rid[r.rid] = i;
         return CVY_OK;
+    }
+
+    // admit waiting requests that have arrived, in arrival order, within max_inflight
+    void admit(double t) {  // caller holds mu
+        while (!waiting.empty() && reqs[waiting.front()].t_arrival <= t &&
+               (cfg.max_inflight == 0 || inflight < cfg.max_inflight)) {
+            const uint32_t k = waiting.front();
+            waiting.pop_front();
+            cvy_status s = submit(k);
+            if (s != CVY_OK) {
+                err = std::string("submit: ") + cvy_last_error();
+                reqs[k].done = true;
+                active--;
+            }
+        }
     }
 
     void finish(uint32_t i, double t) {  // caller holds mu
@@ -137,19 +155,12 @@ struct cvy_runtime {
         r.done = true;
         r.t_done = t;
         active--;
+        inflight--;
         if (cfg.max_inflight > 0) {
             // abort-and-refill (NEXT-3): the slot and its pages go back now (applied at the next
             // step boundary) and a waiting request takes them
             if (cvy_release_request(e, r.rid) == CVY_OK) r.released = true;
-            while (!waiting.empty()) {
-                const uint32_t k = waiting.front();
-                waiting.pop_front();
-                cvy_status s = submit(k);
-                if (s == CVY_OK) break;
-                err = std::string("refill submit: ") + cvy_last_error();
-                reqs[k].done = true;
-                active--;
-            }
+            admit(t);
         }
         cv_driver.notify_all();
     }
@@ -407,6 +418,7 @@ cvy_status cvy_runtime_run(cvy_runtime* rt, const cvy_rt_request* reqs, uint32_t
         const cvy_rt_request& q = reqs[i];
         if (!q.prompt || q.prompt_len < 1 || !q.rounds || q.n_rounds < 1)
             return cvy_internal_fail(CVY_E_INVAL, "runtime: request needs a prompt and >= 1 round");
+        if (!(q.t_arrival >= 0)) return cvy_internal_fail(CVY_E_INVAL, "runtime: t_arrival must be >= 0");
         for (uint32_t k = 0; k < q.n_rounds; ++k)
             if (!q.rounds[k].forced || q.rounds[k].forced_len < 1 || (q.rounds[k].observation_len && !q.rounds[k].observation))
                 return cvy_internal_fail(CVY_E_INVAL, "runtime: a round needs >= 1 forced token");
@@ -419,6 +431,7 @@ cvy_status cvy_runtime_run(cvy_runtime* rt, const cvy_rt_request* reqs, uint32_t
         r.prompt.assign(q.prompt, q.prompt + q.prompt_len);
         r.synth_prefix = q.synth_prefix_len;
         r.synth_seed = q.synth_seed;
+        r.t_arrival = q.t_arrival;
         for (uint32_t k = 0; k < q.n_rounds; ++k) {
             const cvy_round_desc& d = q.rounds[k];
             r.forced.emplace_back(d.forced, d.forced + d.forced_len);
@@ -440,20 +453,15 @@ cvy_status cvy_runtime_run(cvy_runtime* rt, const cvy_rt_request* reqs, uint32_t
     cvy_status result = CVY_OK;
     {
         std::lock_guard<std::mutex> lk(rt->mu);
-        const uint32_t first = rt->cfg.max_inflight ? std::min(n, rt->cfg.max_inflight) : n;
         rt->active = n;
-        for (uint32_t i = 0; i < n; ++i) {
-            if (i >= first) {
-                rt->waiting.push_back(i);
-                continue;
-            }
-            cvy_status s = rt->submit(i);
-            if (s != CVY_OK) {
-                rt->err = std::string("submit: ") + cvy_last_error();
-                result = s;
-                break;
-            }
-        }
+        rt->inflight = 0;
+        std::vector<uint32_t> order(n);
+        for (uint32_t i = 0; i < n; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t a, uint32_t b) { return rt->reqs[a].t_arrival < rt->reqs[b].t_arrival; });
+        for (uint32_t i : order) rt->waiting.push_back(i);
+        rt->admit(0.0);
+        if (!rt->err.empty()) result = CVY_E_FULL;
     }
     if (result != CVY_OK) {
         for (auto& r : rt->reqs)
@@ -470,6 +478,7 @@ cvy_status cvy_runtime_run(cvy_runtime* rt, const cvy_rt_request* reqs, uint32_t
         {
             std::unique_lock<std::mutex> lk(rt->mu);
             if (rt->active == 0 || rt->stop) break;
+            rt->admit(rt->now());
             for (const Req& r : rt->reqs)
                 if (r.submitted && !r.done && !r.final_seen) {
                     busy = true;
@@ -521,6 +530,7 @@ cvy_status cvy_runtime_request_log(cvy_runtime* rt, uint32_t request, cvy_rt_req
     std::lock_guard<std::mutex> lk(rt->mu);
     const Req& r = rt->reqs[request];
     out->req_id = r.rid;
+    out->t_arrival = r.t_arrival;
     out->t_submit = r.t_submit;
     out->t_done = r.t_done;
     out->t_abort = r.t_abort;

@@ -315,7 +315,11 @@ class NativeRuntime:
         self.dispatch_cpu_s = 0.0
         self.stats = None
 
-    def run(self, specs: list[RequestSpec], timeout_s: float = 600.0, max_inflight: int | None = None):
+    def run(self, specs: list[RequestSpec], timeout_s: float = 600.0, max_inflight: int | None = None,
+            arrivals: list[float] | None = None):
+        """arrivals: per-request arrival times (seconds after the start; None: all at t = 0).
+        With arrivals, a request's latency runs from its arrival (RequestLog.t_submit = the
+        arrival), so admission waits count."""
         import ctypes
         from .capi import check
         L = capi.lib()
@@ -355,7 +359,8 @@ class NativeRuntime:
                 rds[k] = capi.RoundDesc(f, len(rd.forced), rd.tool_id, o, len(rd.observation))
             pr = arr(sp.prompt)
             keep += [rds, pr]
-            reqs[i] = capi.RtRequest(pr, len(sp.prompt), sp.synth_prefix, sp.synth_seed, rds, len(sp.rounds))
+            reqs[i] = capi.RtRequest(pr, len(sp.prompt), sp.synth_prefix, sp.synth_seed, rds, len(sp.rounds),
+                                     float(arrivals[i]) if arrivals is not None else 0.0)
         try:
             check(L.cvy_runtime_run(h, reqs, len(specs), float(timeout_s)))
             if errors:
@@ -364,7 +369,8 @@ class NativeRuntime:
             for i, sp in enumerate(specs):
                 rl = capi.RtRequestLog()
                 check(L.cvy_runtime_request_log(h, i, ctypes.byref(rl)))
-                lg = RequestLog(sp, rid=rl.req_id, t_submit=rl.t_submit, t_done=rl.t_done,
+                lg = RequestLog(sp, rid=rl.req_id, t_submit=rl.t_arrival if arrivals is not None else rl.t_submit,
+                                t_done=rl.t_done,
                                 t_abort=rl.t_abort if rl.aborted else None, done=True, released=True)
                 for r in range(rl.n_rounds_run):
                     ro = capi.RtRoundLog()
