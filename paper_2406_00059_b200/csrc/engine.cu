@@ -274,11 +274,6 @@ struct Bucket {
     std::vector<cudaEvent_t> kev;
     std::vector<std::pair<int, int>> kinfo;  // (kind, layer) per launch
     uint32_t launches = 0;
-    // batch-split overlap: two half-batch chains on two streams, so one half's
-    // HBM-bound attention runs beside the other half's tensor-bound projections
-    bool ov = false;
-    StepParams PH[2];
-    std::vector<GemmPlan> hplans[2];  // per chain: 4 GEMMs per layer (QKV, O, gate/up, down)
 };
 
 }  // namespace
@@ -292,17 +287,7 @@ struct cvy_engine {
     int dev = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
-    cudaStream_t stream_b = nullptr;   // second chain of the batch-split overlap
-    cudaStream_t cur = nullptr;        // stream launch_k enqueues on (stream or stream_b)
-    int cur_prio = 0;                  // launch priority attribute (0: none)
-    cudaEvent_t ov_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // fork / join / attention order
-    int prio_hi = 0, prio_lo = 0;      // device stream-priority range (greatest, least)
-    bool ov_ok = false;                // batch-split overlap enabled for buckets >= 256
-    int ov_gemm_sms = 0;               // CTA budget of one overlapped GEMM (its share of the SMs)
-    int ov_prio = 1;                   // 1: GEMMs at high launch priority, 2: attention, 0: none
-    bool ov_serial_attn = true;        // the two chains' attention launches run one after the other
-    float* d_gemm_acc2 = nullptr;      // stream-K scratch of chain 1 (chain 0 uses d_gemm_acc)
-    int32_t* d_tile_cnt2 = nullptr;
+    cudaStream_t cur = nullptr;        // stream launch_k enqueues on
     bool dead = false;
     bool bf16 = true;
     int act_ld = 0;
@@ -658,18 +643,6 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
     ALLOC(e->d_gemm_acc, sizeof(float) * max_rows * acc_cols);
     ALLOC(e->d_tile_cnt, sizeof(int32_t) * 8192);
     ALLOC(e->d_spans, sizeof(unsigned long long) * 2 * kSpanSlots);
-    // batch-split overlap: bf16, buckets of >= 256 slots; CVY_OVERLAP=0 disables
-    e->ov_ok = false;  // opt-in: measured slower at C4
-    if (const char* v = getenv("CVY_OVERLAP"))
-        e->ov_ok = e->bf16 && Bmax >= 256 && (hd == 64 || hd == 128) && (H / Hkv) <= 4 && atoi(v) != 0;
-    e->ov_gemm_sms = prop.multiProcessorCount / 2;
-    if (const char* v = getenv("CVY_OV_GEMM_SMS")) e->ov_gemm_sms = std::max(8, std::min(prop.multiProcessorCount, atoi(v)));
-    if (const char* v = getenv("CVY_OV_PRIO")) e->ov_prio = atoi(v);
-    if (const char* v = getenv("CVY_OV_SERIAL_ATTN")) e->ov_serial_attn = atoi(v) != 0;
-    if (e->ov_ok) {
-        ALLOC(e->d_gemm_acc2, sizeof(float) * max_rows * (size_t)Bmax);
-        ALLOC(e->d_tile_cnt2, sizeof(int32_t) * 8192);
-    }
     if ((ec->flags & CVY_ENGINE_CHUNKED_PREFILL) && e->bf16) {
         const size_t R = kPrefillRows;
         ALLOC(e->d_px, sizeof(float) * R * d);
@@ -717,18 +690,11 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
             cvy_engine_destroy(e);
             return fail(CVY_E_INVAL, "vocab entry longer than 16 bytes");
         }
-    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&e->stream_b, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
         cvy_engine_destroy(e);
         return fail(CVY_E_CUDA, "stream create");
     }
     e->cur = e->stream;
-    cudaDeviceGetStreamPriorityRange(&e->prio_lo, &e->prio_hi);
-    for (auto& ev : e->ov_ev)
-        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
-            cvy_engine_destroy(e);
-            return fail(CVY_E_CUDA, "event create");
-        }
     e->slots.resize(Bmax);
     for (int p = (int)ec->n_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
     if (const char* tl = getenv("CVY_GEMM_TRACE_LAYER")) {
@@ -778,7 +744,6 @@ void cvy_engine_destroy(cvy_engine* e) {
     if (!e) return;
     cudaSetDevice(e->dev);
     if (e->stream) cudaStreamSynchronize(e->stream);
-    if (e->stream_b) cudaStreamSynchronize(e->stream_b);
     for (auto& kv : e->buckets) {
         if (kv.second.graph) cudaGraphExecDestroy(kv.second.graph);
         if (kv.second.graph_timed) cudaGraphExecDestroy(kv.second.graph_timed);
@@ -797,15 +762,12 @@ void cvy_engine_destroy(cvy_engine* e) {
                      e->d_o, e->d_h, e->d_ssq, e->d_am, e->d_dbg, e->d_lm_done, e->d_attn_part, e->d_vtab, e->d_vlen,
                      e->d_tools, e->d_ring_tail, e->d_step, e->d_gemm_acc, e->d_tile_cnt, e->d_patches,
                      e->d_px, e->d_pact, e->d_pq, e->d_po, e->d_ph, e->d_pssq, e->d_pattn_part, e->d_prow,
-                     e->d_gemm_acc2, e->d_tile_cnt2, e->d_spans};
+                     e->d_spans};
     for (void* p : dptrs)
         if (p) cudaFree(p);
     void* hptrs[] = {e->h_ring, e->h_ring_tail, e->h_byte_log, e->h_tok_log, e->h_status, e->h_stats};
     for (void* p : hptrs)
         if (p) cudaFreeHost(p);
-    for (auto& ev : e->ov_ev)
-        if (ev) cudaEventDestroy(ev);
-    if (e->stream_b) cudaStreamDestroy(e->stream_b);
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -1152,13 +1114,8 @@ cvy_status launch_k(cvy_engine* e, const void* func, dim3 grid, dim3 block, size
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = e->cur ? e->cur : e->stream;
-    cudaLaunchAttribute attr[3];
+    cudaLaunchAttribute attr[2];
     int na = 0;
-    if (e->cur_prio != 0) {
-        attr[na].id = cudaLaunchAttributePriority;
-        attr[na].val.priority = e->cur_prio;
-        ++na;
-    }
     if (pdl && !(e->c.flags & CVY_ENGINE_NO_PDL) && !e->capturing_timed) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;
@@ -1247,24 +1204,15 @@ StepParams base_params(cvy_engine* e, int Bp) {
     return P;
 }
 
-// Options of a half-batch plan (batch-split overlap): its padded batch, its CTA budget, its own
-// stream-K scratch, and the rows of the activation tensor map left after the row offset of X.
-struct PlanOpts {
-    int Bp = 0;
-    int sms = 0;
-    float* part = nullptr;
-    int32_t* tile_cnt = nullptr;
-    int64_t x_rows = 0;
-};
 
 // plan one GEMM: W rows N per layer, K, epilogue
 bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int layer, int L_rows_total, const void* X,
-               EpiArgs epi, GemmPlan* out, std::string* why, int xcap = 0, const PlanOpts* po = nullptr) {
+               EpiArgs epi, GemmPlan* out, std::string* why, int xcap = 0) {
     if (xcap <= 0) xcap = (int)e->slots.size();  // activation buffer rows (planes are xcap rows apart)
     GemmPlan gp;
     std::memset(&gp, 0, sizeof(gp));
-    const int Bp = (po && po->Bp) ? po->Bp : bk.Bp;
-    const int sms = (po && po->sms) ? po->sms : e->num_sms;
+    const int Bp = bk.Bp;
+    const int sms = e->num_sms;
     gp.W = Wbase;
     gp.X = X;
     gp.w_row0 = (int64_t)layer * N;
@@ -1283,8 +1231,8 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
             const int k = epi.kind == EPI_QKV ? 0 : epi.kind == EPI_SWIGLU ? 2 : (K == ::m_d(e) ? 1 : 3);
             g.trace = e->d_trace + (size_t)k * kTraceStride * e->num_sms;
         }
-        g.part = (po && po->part) ? po->part : e->d_gemm_acc;
-        g.tile_cnt = (po && po->tile_cnt) ? po->tile_cnt : e->d_tile_cnt;
+        g.part = e->d_gemm_acc;
+        g.tile_cnt = e->d_tile_cnt;
         // measurement knob (wrong results): the gate/up epilogue's debug bits (GemmTC::dbg)
         if (const char* dg = getenv("CVY_GEMM_DBG_GU"))
             if (epi.kind == EPI_SWIGLU) g.dbg = atoi(dg);
@@ -1303,7 +1251,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
             return false;
         }
         const uint32_t xrows = g.merge ? (uint32_t)g.bq : (uint32_t)g.mma_n;
-        if (!make_tmap(&gp.tmX, X, (uint64_t)((po && po->x_rows) ? po->x_rows : 2 * xcap), (uint64_t)K, (uint64_t)e->act_ld, xrows,
+        if (!make_tmap(&gp.tmX, X, (uint64_t)(2 * xcap), (uint64_t)K, (uint64_t)e->act_ld, xrows,
                        (uint32_t)g.bk)) {
             *why = "cuTensorMapEncodeTiled (activations) failed";
             return false;
@@ -1353,60 +1301,6 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
         EpiArgs el{EPI_LMHEAD, 0, V, nullptr, nullptr, 7};
         if (!plan_gemm(e, bk, e->w.lm_head, V, d, 0, V, e->d_act, el, &gp, &why)) return fail(CVY_E_INVAL, why);
         bk.plans.push_back(gp);
-    }
-    // batch-split overlap: chain k owns slots [k*Bp/2, (k+1)*Bp/2); its
-    // StepParams are the full ones with every per-slot pointer advanced by k*Bp/2 rows, so the
-    // unchanged kernels see a batch of Bp/2 slots.  Each chain's GEMMs get their own stream-K
-    // scratch and a budget of ov_gemm_sms CTAs; the rest of the SMs run the other chain's attention.
-    if (e->ov_ok && Bp >= 256 && !bk.P.row_slot) {
-        const int Bh = Bp / 2;
-        const size_t es = dtype_size(m.dtype);
-        bool ok = true;
-        for (int k = 0; k < 2 && ok; ++k) {
-            const size_t r0 = (size_t)k * Bh;
-            StepParams Q = bk.P;
-            Q.Bp = Bh;
-            Q.slots = bk.P.slots + r0;
-            Q.page_table = bk.P.page_table + r0 * bk.P.max_pages;
-            Q.in_buf = bk.P.in_buf + r0 * bk.P.input_cap;
-            Q.force_buf = bk.P.force_buf + r0 * bk.P.forced_cap;
-            Q.x = bk.P.x + r0 * d;
-            Q.act = (uint8_t*)bk.P.act + r0 * e->act_ld * es;
-            Q.o = (uint8_t*)bk.P.o + r0 * e->act_ld * es;
-            Q.h = (uint8_t*)bk.P.h + r0 * e->act_ld * es;
-            Q.q = bk.P.q + r0 * H * hd;
-            Q.ssq = bk.P.ssq + r0;
-            Q.am_keys = bk.P.am_keys + r0;
-            Q.dbg_logits = bk.P.dbg_logits ? bk.P.dbg_logits + r0 * V : nullptr;
-            Q.attn_splits = 1;
-            Q.attn_part = bk.P.attn_part + r0 * Hkv * (m.n_heads / Hkv) * (hd + 2);
-            Q.span_base = k * (kSpanSlots / 2);
-            bk.PH[k] = Q;
-            PlanOpts po;
-            po.Bp = Bh;
-            po.sms = e->ov_gemm_sms;
-            po.part = k == 0 ? e->d_gemm_acc : e->d_gemm_acc2;
-            po.tile_cnt = k == 0 ? e->d_tile_cnt : e->d_tile_cnt2;
-            po.x_rows = (int64_t)2 * e->slots.size() - (int64_t)r0;
-            const size_t xoff = r0 * e->act_ld * es;
-            for (int l = 0; l < L && ok; ++l) {
-                GemmPlan gp;
-                EpiArgs eq{EPI_QKV, l, Nqkv, nullptr, nullptr, 1};
-                ok = ok && plan_gemm(e, bk, e->w.wqkv, Nqkv, d, l, L * Nqkv, (uint8_t*)e->d_act + xoff, eq, &gp, &why, 0, &po);
-                bk.hplans[k].push_back(gp);
-                EpiArgs eo{EPI_RESID, l, d, e->w.mlp_norm + (size_t)l * d, nullptr, 4};
-                ok = ok && plan_gemm(e, bk, e->w.wo, d, H * hd, l, L * d, (uint8_t*)e->d_o + xoff, eo, &gp, &why, 0, &po);
-                bk.hplans[k].push_back(gp);
-                EpiArgs eg{EPI_SWIGLU, l, 2 * dff, nullptr, nullptr, 5};
-                ok = ok && plan_gemm(e, bk, e->w.wgu, 2 * dff, d, l, L * 2 * dff, (uint8_t*)e->d_act + xoff, eg, &gp, &why, 0, &po);
-                bk.hplans[k].push_back(gp);
-                EpiArgs ed{EPI_RESID, l, d, (l + 1 < L) ? e->w.attn_norm + (size_t)(l + 1) * d : e->w.final_norm, nullptr, 6};
-                ok = ok && plan_gemm(e, bk, e->w.wd, d, dff, l, L * d, (uint8_t*)e->d_h + xoff, ed, &gp, &why, 0, &po);
-                bk.hplans[k].push_back(gp);
-            }
-        }
-        if (!ok) return fail(CVY_E_INVAL, "overlap plan: " + why);
-        bk.ov = true;
     }
     // cross-kernel weight prefetch: GEMM i warms L2 with the first k-blocks of GEMM i+1 (the LM
     // head warms the next step's layer-0 QKV) while its own epilogue drains
@@ -1626,62 +1520,6 @@ cvy_status enqueue_prefill(cvy_engine* e, const std::vector<PrefillJob>& jobs) {
     return CVY_OK;
 }
 
-// Batch-split overlap: the layers of the two half-batch chains, chain k on
-// stream k.  Chain 1 starts when chain 0's first QKV is done, and (ov_serial_attn) the two
-// chains' attention launches alternate (A0, A1, A0, ...), so while one chain streams its KV
-// cache from HBM the other runs its tensor-bound projections on its CTA budget of SMs.
-// Launch priorities (ov_prio) let the projections' CTAs take SMs first as they free up.
-cvy_status enqueue_overlap_layers(cvy_engine* e, Bucket& bk, KTimer& kt, uint32_t* launches) {
-    cvy_status st;
-    const int gprio = e->ov_prio == 1 ? e->prio_hi : 0;
-    const int aprio = e->ov_prio == 2 ? e->prio_hi : 0;
-    cudaStream_t sk[2] = {e->stream, e->stream_b};
-    auto ck = [&](cudaError_t err, const char* what) { return check_cuda(e, err, what); };
-    if ((st = ck(cudaEventRecord(e->ov_ev[0], e->stream), "overlap fork")) != CVY_OK) return st;
-    if ((st = ck(cudaStreamWaitEvent(e->stream_b, e->ov_ev[0], 0), "overlap fork wait")) != CVY_OK) return st;
-    const bool pdl_saved = (e->c.flags & CVY_ENGINE_NO_PDL) != 0;
-    for (int l = 0; l < e->m.n_layers; ++l) {
-        for (int k = 0; k < 2; ++k) {
-            e->cur = sk[k];
-            GemmPlan* hp = &bk.hplans[k][(size_t)4 * l];
-            StepParams* Pk = &bk.PH[k];
-            if (l == 0 && k == 1) {
-                if ((st = ck(cudaStreamWaitEvent(e->stream_b, e->ov_ev[1], 0), "chain offset wait")) != CVY_OK) return st;
-            }
-            e->cur_prio = gprio;
-            kt.begin(1, l);
-            if ((st = launch_gemm(e, bk, hp[0], Pk)) != CVY_OK) return st;
-            kt.end();
-            if (l == 0 && k == 0) {
-                if ((st = ck(cudaEventRecord(e->ov_ev[1], e->stream), "chain offset")) != CVY_OK) return st;
-            }
-            bool waited = false;
-            if (e->ov_serial_attn && (k == 1 || l > 0)) {
-                if ((st = ck(cudaStreamWaitEvent(sk[k], e->ov_ev[2 + (1 - k)], 0), "attention order")) != CVY_OK) return st;
-                waited = true;
-            }
-            e->cur_prio = aprio;
-            // no programmatic (PDL) edge where the launch also waits on the other chain
-            if (waited) e->c.flags |= CVY_ENGINE_NO_PDL;
-            kt.begin(2, l);
-            st = launch_attention(e, bk, l, &kt, Pk);
-            if (!pdl_saved) e->c.flags &= ~(uint32_t)CVY_ENGINE_NO_PDL;
-            if (st != CVY_OK) return st;
-            if ((st = ck(cudaEventRecord(e->ov_ev[2 + k], sk[k]), "attention done")) != CVY_OK) return st;
-            e->cur_prio = gprio;
-            for (int q = 1; q < 4; ++q) {
-                kt.begin(3 + q, l);
-                if ((st = launch_gemm(e, bk, hp[q], Pk)) != CVY_OK) return st;
-                kt.end();
-            }
-            *launches += 5;
-        }
-    }
-    if ((st = ck(cudaEventRecord(e->ov_ev[0], e->stream_b), "overlap join")) != CVY_OK) return st;
-    if ((st = ck(cudaStreamWaitEvent(e->stream, e->ov_ev[0], 0), "overlap join wait")) != CVY_OK) return st;
-    return CVY_OK;
-}
-
 cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
     cvy_status st;
     uint32_t launches = 0;
@@ -1702,23 +1540,6 @@ cvy_status enqueue_step_kernels(cvy_engine* e, Bucket& bk) {
         if ((st = launch_k(e, f, dim3(Bp), dim3(128), 0, args, true)) != CVY_OK) return st;
         kt.end();
         launches++;
-    }
-    if (bk.ov) {
-        st = enqueue_overlap_layers(e, bk, kt, &launches);
-        e->cur = e->stream;
-        e->cur_prio = 0;
-        if (st != CVY_OK) return st;
-        // the LM head follows the join (a full edge from chain 1): no programmatic edge
-        const uint32_t saved = e->c.flags;
-        e->c.flags |= CVY_ENGINE_NO_PDL;
-        kt.begin(7, 0);
-        st = launch_gemm(e, bk, bk.plans.back());
-        e->c.flags = saved;
-        if (st != CVY_OK) return st;
-        kt.end();
-        launches++;
-        bk.launches = launches;
-        return CVY_OK;
     }
     size_t pi = 0;
     for (int l = 0; l < m.n_layers; ++l) {
@@ -1883,7 +1704,6 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
             e->capturing_spans = !e->timing && e->spans_on;
             if (e->capturing_spans) {  // kernel parameters are copied at capture: spans only in this variant
                 bk->P.spans = e->d_spans;
-                for (auto& ph : bk->PH) ph.spans = e->d_spans;
             }
             st = check_cuda(e, cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
             if (st != CVY_OK) return st;
@@ -1892,7 +1712,6 @@ cvy_status cvy_step(cvy_engine* e, cvy_step_info* last_completed) {
             e->capturing_timed = false;
             e->capturing_spans = false;
             bk->P.spans = nullptr;
-            for (auto& ph : bk->PH) ph.spans = nullptr;
             if (st2 != CVY_OK) {
                 e->dead = true;
                 return st2;
