@@ -200,6 +200,10 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         int whole = 1;
         if (const char* v = getenv("CVY_GEMM_WHOLE")) whole = atoi(v);
         if (whole && g.nbt > 1 && g.tiles * g.nbt <= num_sms) *grid = g.tiles;
+        // A/B knob: exactly k whole tiles per CTA (no shared tile): tile i's epilogue overlaps
+        // tile i+1's main loop through the double-buffered TMEM accumulator
+        if (const char* v = getenv(streamk ? "CVY_GU_TPC" : "CVY_GEMM_TPC"))
+            if (atoi(v) > 0 && g.tiles % atoi(v) == 0) *grid = g.tiles / atoi(v);
     }
     return true;
 }
@@ -1236,6 +1240,8 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         // measurement knob (wrong results): the gate/up epilogue's debug bits (GemmTC::dbg)
         if (const char* dg = getenv("CVY_GEMM_DBG_GU"))
             if (epi.kind == EPI_SWIGLU) g.dbg = atoi(dg);
+        if (const char* dg = getenv("CVY_GEMM_DBG_ALL"))  // every projection but the LM head
+            if (epi.kind != EPI_LMHEAD) g.dbg = atoi(dg);
         g.x_plane_rows = (int32_t)xcap;
         g.wtiled = e->w_tiled && (Wbase == e->w.wqkv || Wbase == e->w.wo || Wbase == e->w.wgu || Wbase == e->w.wd ||
                                   (Wbase == e->w.lm_head && lm_head_tiled(&e->m)));

@@ -379,12 +379,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
                         float v[32];
-                        tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         if (MERGE) {
                             float w[32];
-                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), w);
+                            tmem_ld32x2(tacc + (uint32_t)(s * G.cols_per_sub + cb),
+                                        tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), v, w);
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
+                        } else {
+                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         }
 #pragma unroll
                         for (int h = 0; h < 2; ++h) {
@@ -405,12 +407,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
                         float v[32];
-                        tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         if (MERGE) {
                             float w[32];
-                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), w);
+                            tmem_ld32x2(tacc + (uint32_t)(s * G.cols_per_sub + cb),
+                                        tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), v, w);
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
+                        } else {
+                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         }
                         if (!(G.dbg & 8))
                             epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, et);
@@ -427,12 +431,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
                         float v[32];
-                        tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         if (MERGE) {
                             float w[32];
-                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), w);
+                            tmem_ld32x2(tacc + (uint32_t)(s * G.cols_per_sub + cb),
+                                        tacc + (uint32_t)(s * G.cols_per_sub + Bp + cb), v, w);
 #pragma unroll
                             for (int i = 0; i < 32; ++i) v[i] += w[i];
+                        } else {
+                            tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         }
                         float* dst = acc + (size_t)(s * 128 + et) * Bp + cb;
 #pragma unroll
