@@ -104,7 +104,7 @@ bool make_tmap_kv3(CUtensorMap* out, const void* base, uint64_t rows) {
 //   Bp 160..256: 1 sub-tile, planes as two MMAs into one accumulator (N = Bp)
 //   Bp 512: 1 sub-tile, 2 batch halves of N = 256, 32-element K stages (64B swizzle)
 bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why,
-                 bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0) {
+                 bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0, int epi_groups = 1) {
     g.N = N;
     g.K = K;
     // batches above 128 columns run as nbt tiles of 128 on grid.y, each with the merged
@@ -159,6 +159,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     g.kblocks = K / g.bk;
     const uint32_t stage = GemmSmem::stage_bytes(g.nsub, Bq, 2, g.bk);
     const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
+    (void)epi_groups;  // the second epilogue group borrows the idle ring (gemm_sm100.cuh)
     // shared-memory budget per CTA (A/B knob CVY_GEMM_SMEM: a smaller ring lets the next
     // kernel's CTA co-reside and start its weight stream under this kernel's epilogue tail)
     uint32_t budget = 232448;
@@ -1228,7 +1229,8 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         // gate/up: optionally stream-K over every SM instead of 112 whole 256-row tiles (A/B knob)
         const bool gu_sk = epi.kind == EPI_SWIGLU && getenv("CVY_GU_STREAMK") && atoi(getenv("CVY_GU_STREAMK")) != 0;
         const int gu_nsub = (epi.kind == EPI_SWIGLU && getenv("CVY_GU_NSUB")) ? atoi(getenv("CVY_GU_NSUB")) : 0;
-        if (!gemm_config(g, N, K, Bp, sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub))
+        if (!gemm_config(g, N, K, Bp, sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub,
+                         gemm_epi_groups(epi.kind)))
             return false;
         g.w_row0 = layer * N;
         if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD && xcap == (int)e->slots.size()) {
@@ -1338,7 +1340,8 @@ cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp, StepParams* Pq =
     if (e->bf16) {
         void* args[] = {&gp.tmW, &gp.tmX, Pq ? Pq : &bk.P, &gp.g, &gp.tmN};
         return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind),
-                        dim3(gp.grid, gp.g.nbt), dim3(kGemmThreads), gp.smem, args, true, gp.g.split > 1 ? gp.g.split : 1);
+                        dim3(gp.grid, gp.g.nbt), dim3(gemm_launch_threads(gp.g.epi.kind, gp.g.split)), gp.smem, args, true,
+                        gp.g.split > 1 ? gp.g.split : 1);
     }
     const float* W = (const float*)gp.W;
     const float* X = (const float*)gp.X;

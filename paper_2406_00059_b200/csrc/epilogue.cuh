@@ -15,7 +15,9 @@ constexpr int kEpiThreads = 128;
 constexpr int kEsmLd = 33;  // padded row of the [128][33] exchange buffer
 constexpr uint32_t kEpiBar = 1;
 
-CVY_DEV void epi_sync() { named_bar_sync(kEpiBar, kEpiThreads); }
+// 128-thread barrier of this thread's epilogue group: threads 0..127 (barrier 1), or the second
+// group of the gate/up GEMM, threads 192..319 (barrier 3); see gemm_sm100.cuh
+CVY_DEV void epi_sync() { named_bar_sync(threadIdx.x >= 192 ? 3u : kEpiBar, kEpiThreads); }
 
 // Per-column (= per slot) metadata the epilogues need, gathered once per CTA into shared
 // memory so the per-element epilogue never chases global pointers:

@@ -75,6 +75,14 @@ CVY_DEV unsigned long long gtimer() {
 }
 
 constexpr int kGemmThreads = 192;
+// The gate/up GEMM runs its (latency-bound) SwiGLU epilogue on two groups of 4 warps (warps 0-3
+// and 6-9 both cover the 4 TMEM lane quadrants), alternating 32-column chunks.
+__host__ __device__ constexpr int gemm_epi_groups(int epi) { return epi == EPI_SWIGLU ? 2 : 1; }
+__host__ __device__ constexpr int gemm_threads(int epi) { return gemm_epi_groups(epi) == 2 ? 320 : kGemmThreads; }
+// threads a launch uses: the second epilogue group only for whole single-tile CTAs (split == 1)
+__host__ __device__ constexpr int gemm_launch_threads(int epi, int split) {
+    return (gemm_epi_groups(epi) == 2 && split == 1) ? 320 : kGemmThreads;
+}
 constexpr int kTraceStride = 16;
 
 // shared-memory carve-up (host and device agree); rows are bk*2 bytes (one swizzle atom)
@@ -149,7 +157,7 @@ CVY_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
 CVY_DEV uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
 
 template <typename T, int NSUB, bool MERGE, int BK, int EPI>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(gemm_threads(EPI), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G,
                    const __grid_constant__ CUtensorMap tmN) {
@@ -165,9 +173,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const uint32_t XB = (uint32_t)Bp * ROW;           // one activation plane per stage
     const uint32_t stage_bytes = WB + 2u * XB;
     uint8_t* fixed = smem + (size_t)G.stages * stage_bytes;
-    float* esm = reinterpret_cast<float*>(fixed);
+    constexpr int EG = gemm_epi_groups(EPI);
+    float* esm0 = reinterpret_cast<float*>(fixed);
     EpiMeta meta;
-    meta.kvoff = reinterpret_cast<long long*>(esm + 128 * kEsmLd + 4);
+    meta.kvoff = reinterpret_cast<long long*>(esm0 + 128 * kEsmLd + 4);
     meta.scale = reinterpret_cast<float*>(meta.kvoff + P.Bp);
     meta.pos = reinterpret_cast<int*>(meta.scale + P.Bp);
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta.pos + P.Bp + 2);
@@ -178,6 +187,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int* flags = reinterpret_cast<int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // epilogue group of this warp (0: warps 0-3, 1: warps 6-9).  The second group works only when
+    // the CTA owns exactly one whole tile (split == 1): its epilogue starts after the tile's last
+    // MMA, so the pipeline ring is idle and holds group 1's exchange buffer (no shared memory
+    // taken from the ring's stages)
+    const int egroup = warp >= 6 ? 1 : 0;
+    const int n_egroups = (EG == 2 && G.split == 1 && blockDim.x >= 320) ? 2 : 1;
+    float* esm = egroup ? reinterpret_cast<float*>(smem) : esm0;
     const long long T_iters = (long long)G.tiles * G.kblocks;
     const int Gc = gridDim.x;
     long long it0, it1;
@@ -202,7 +218,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull_bar[s], 1);
-            mbar_init(&tempty_bar[s], kEpiThreads);
+            mbar_init(&tempty_bar[s], kEpiThreads * n_egroups);
         }
         fence_mbar_init();
     }
@@ -338,9 +354,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         }
     } else {
-        // ===================== epilogue (warps 0-3) =====================
-        const int et = threadIdx.x;  // 0..127 == TMEM lane == tile row
-        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        // ===================== epilogue (warps 0-3, and 6-9 for the gate/up GEMM) =====================
+        const int et = (warp & 3) * 32 + lane;  // 0..127 == TMEM lane == tile row
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        // both groups meet here (prepare, stream-K ticket); one group: its own barrier
+        auto grp_sync = [&]() {
+            if (n_egroups == 2) named_bar_sync(4, 2 * kEpiThreads); else epi_sync();
+        };
+        if (egroup >= n_egroups) it0 = it1;  // second group idle in split-K mode
         const int rows = NSUB * 128;
         bool prepared = false;
         int as = 0;
@@ -354,13 +375,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int c_last = G.split > 0 ? 0 : cta_of_iter(te - 1, T_iters, Gc);
             if (!prepared) {
                 pdl_wait();
-                epilogue_prepare(P, G.epi, meta, et);
-                epi_sync();
+                if (egroup == 0) epilogue_prepare(P, G.epi, meta, et);
+                grp_sync();
                 prepared = true;
             }
             mbar_wait(&tfull_bar[as], aphase);
             tc_fence_after();
-            if (tr && et == 0) tr[2 + (it >= it1 ? 1 : 0)] = gtimer();  // [2] first / [3] last segment's MMA done
+            if (tr && et == 0 && egroup == 0) tr[2 + (it >= it1 ? 1 : 0)] = gtimer();  // [2] first / [3] last segment's MMA done
             if (G.dbg & 1) {
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
@@ -403,9 +424,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
             } else if (c_first == c_last) {
-                // sole contributor: epilogue straight from TMEM (hi + lo planes summed)
+                // sole contributor: epilogue straight from TMEM (hi + lo planes summed); with two
+                // epilogue groups, group g takes the chunks ci = g, g + 2, ...
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
+                        if (n_egroups == 2 && (((s * Bp + cb) >> 5) & 1) != egroup) continue;
                         float v[32];
                         if (MERGE) {
                             float w[32];
@@ -430,6 +453,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 int32_t* ticket = G.tile_cnt + (size_t)tile * G.nbt + blockIdx.y;
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
+                        if (n_egroups == 2 && (((s * Bp + cb) >> 5) & 1) != egroup) continue;
                         float v[32];
                         if (MERGE) {
                             float w[32];
@@ -447,13 +471,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 tc_fence_before();
                 mbar_arrive(&tempty_bar[as]);
                 __threadfence();
-                epi_sync();
-                if (et == 0) flags[0] = (atomicAdd(ticket, 1) == c_last - c_first) && !(G.dbg & 4);
-                epi_sync();
+                grp_sync();
+                if (et == 0 && egroup == 0) flags[0] = (atomicAdd(ticket, 1) == c_last - c_first) && !(G.dbg & 4);
+                grp_sync();
                 if (flags[0]) {
                     __threadfence();
                     for (int s = 0; s < NSUB; ++s)
                         for (int cb = 0; cb < Bp; cb += 32) {
+                            if (n_egroups == 2 && (((s * Bp + cb) >> 5) & 1) != egroup) continue;
                             float v[32];
                             float4* src = reinterpret_cast<float4*>(acc + (size_t)(s * 128 + et) * Bp + cb);
 #pragma unroll
@@ -469,7 +494,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             if (!(G.dbg & 8))
                                 epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, et);
                         }
-                    if (et == 0) *ticket = 0;
+                    // both groups have read the accumulator before the ticket is re-armed
+                    grp_sync();
+                    if (et == 0 && egroup == 0) *ticket = 0;
                     did_epi = true;
                 }
             }
