@@ -460,7 +460,8 @@ typedef struct {
 cvy_status cvy_runtime_create(cvy_engine* e, const cvy_runtime_config* cfg, cvy_runtime** out);
 /* Runs every request to completion (copies the descriptors; blocks the calling thread, which
  * drives cvy_step).  E_INVAL bad descriptors, E_FULL a request could not be admitted even
- * with the engine idle, E_STATE timeout or an engine error (see cvy_last_error).  May be
+ * with the engine idle (a full engine otherwise queues the request until a slot frees), E_STATE
+ * timeout or an engine error (see cvy_last_error).  May be
  * called again: each call replaces the previous logs. */
 cvy_status cvy_runtime_run(cvy_runtime* rt, const cvy_rt_request* reqs, uint32_t n, double timeout_s);
 cvy_status cvy_runtime_request_log(cvy_runtime* rt, uint32_t request, cvy_rt_request_log* out);

@@ -135,13 +135,16 @@ struct cvy_runtime {
         return CVY_OK;
     }
 
-    // admit waiting requests that have arrived, in arrival order, within max_inflight
+    // admit waiting requests that have arrived, in arrival order, within max_inflight; a full
+    // engine (CVY_E_FULL: no free slot or pages) keeps the request at the head of the queue until
+    // a finished request is released; any other error fails the run
     void admit(double t) {  // caller holds mu
         while (!waiting.empty() && reqs[waiting.front()].t_arrival <= t &&
                (cfg.max_inflight == 0 || inflight < cfg.max_inflight)) {
             const uint32_t k = waiting.front();
-            waiting.pop_front();
             cvy_status s = submit(k);
+            if (s == CVY_E_FULL && inflight > 0) break;
+            waiting.pop_front();
             if (s != CVY_OK) {
                 err = std::string("submit: ") + cvy_last_error();
                 reqs[k].done = true;
@@ -156,7 +159,7 @@ struct cvy_runtime {
         r.t_done = t;
         active--;
         inflight--;
-        if (cfg.max_inflight > 0) {
+        if (cfg.max_inflight > 0 || !waiting.empty()) {
             // abort-and-refill (NEXT-3): the slot and its pages go back now (applied at the next
             // step boundary) and a waiting request takes them
             if (cvy_release_request(e, r.rid) == CVY_OK) r.released = true;

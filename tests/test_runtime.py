@@ -233,6 +233,27 @@ def test_native_runtime_poisson_arrivals():
     eng.close()
 
 
+@pytest.mark.gpu
+def test_native_runtime_queues_when_engine_full():
+    """More requests than engine slots and no max_inflight: the native runtime keeps the ones
+    the engine refuses (CVY_E_FULL) queued in arrival order and admits them as finished requests
+    release their slots; every request completes."""
+    from inputs.configs import MISTRAL_7B, slice_of
+    from inputs.tool_workloads import TOOLS, build
+    from inputs.vocab import synthetic_vocab
+    from paper_2406_00059_b200.engine import DeviceModel, Engine
+    from paper_2406_00059_b200.runtime import NativeRuntime
+    dm = DeviceModel(slice_of(MISTRAL_7B, L=2, name="7b-L2"), "bf16", 4 * 40, seed=1002)
+    eng = Engine(dm, synthetic_vocab(32000), max_slots=4, max_pages_per_slot=40)
+    ids = {n: eng.register_tool(n, getattr(capi, k), d) for n, (k, d) in TOOLS.items()}
+    _, specs = build("codegen", 10, ids)
+    logs = NativeRuntime(eng, capi.MODE_PARTIAL).run(specs)
+    assert len(logs) == 10 and all(lg.t_done > 0 for lg in logs)
+    starts = sorted(lg.round_start[0] for lg in logs)
+    assert starts[4] > min(lg.t_done for lg in logs) - 1e-6  # the 5th waited for a slot
+    eng.close()
+
+
 # ------------------------------------------------------------------ NEXT-4: Fig. 6 sweep
 def test_sweep_builder_tool_time_is_r_times_decode_time():
     """build_sweep assigns line costs so a round's tool time is r x its decode time at the
