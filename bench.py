@@ -733,9 +733,14 @@ def main():
         bs = {w: (args.latency_batch or base[w]) for w in ws}
         from paper_2406_00059_b200 import capi
         fl = capi.ENGINE_CHUNKED_PREFILL if args.chunked_prefill else 0
-        print(json.dumps({"latency": run_latency(ws, bs, verbose=True, inflight=args.latency_inflight or None,
-                                                 flags=fl), "chunked_prefill": bool(args.chunked_prefill)}),
-              flush=True)
+        res = run_latency(ws, bs, verbose=True, inflight=args.latency_inflight or None, flags=fl,
+                          reps=args.latency_reps)
+        for row in res.values():  # per-request latency lists stay out of the summary line
+            for runs in row["runs"].values():
+                for r in runs:
+                    r.pop("lat_ms", None)
+        print(json.dumps({"latency": res, "chunked_prefill": bool(args.chunked_prefill), "runtime": "native",
+                          "protocol": "all requests at t=0, modes interleaved per repetition"}), flush=True)
         return
     if args.impl == "reference":
         run_reference(args)

@@ -401,7 +401,8 @@ typedef void (*cvy_plan_fn)(void* user, uint32_t request, uint32_t round, uint32
 
 typedef struct {
     cvy_exec_mode mode;
-    uint32_t n_workers;     /* executor threads (>= 1)                                  */
+    uint32_t n_workers;     /* executor threads (1..4096): size it to the concurrent tool
+                               calls the workload issues, or tool capacity binds          */
     uint32_t max_inflight;  /* 0: submit every request at t = 0                         */
     cvy_plan_fn plan;       /* required                                                 */
     void* plan_user;

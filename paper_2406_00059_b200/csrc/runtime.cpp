@@ -404,8 +404,8 @@ struct cvy_runtime {
 cvy_status cvy_runtime_create(cvy_engine* e, const cvy_runtime_config* cfg, cvy_runtime** out) {
     if (!out) return cvy_internal_fail(CVY_E_INVAL, "null out");
     *out = nullptr;
-    if (!e || !cfg || !cfg->plan || cfg->n_workers < 1 || cfg->n_workers > 1024)
-        return cvy_internal_fail(CVY_E_INVAL, "runtime: engine, plan callback and 1..1024 workers required");
+    if (!e || !cfg || !cfg->plan || cfg->n_workers < 1 || cfg->n_workers > 4096)
+        return cvy_internal_fail(CVY_E_INVAL, "runtime: engine, plan callback and 1..4096 workers required");
     if (cfg->mode != CVY_MODE_PARTIAL && cfg->mode != CVY_MODE_SEQUENTIAL)
         return cvy_internal_fail(CVY_E_INVAL, "runtime: bad mode");
     cvy_runtime* rt = new cvy_runtime();

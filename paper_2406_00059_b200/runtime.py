@@ -305,7 +305,7 @@ class NativeRuntime:
     per polled piece.  run() returns RequestLog objects like Runtime.run, so summarize /
     round_timelines / timeline.py work unchanged."""
 
-    def __init__(self, eng, mode: int, n_workers: int = 64, poll_sleep_us: int = 20):
+    def __init__(self, eng, mode: int, n_workers: int | None = None, poll_sleep_us: int = 20):
         self.eng = eng
         self.mode = mode
         self.n_workers = n_workers
@@ -345,7 +345,10 @@ class NativeRuntime:
                 out.contents.skip = 1
 
         cb = capi.PLAN_FN(plan_cb)
-        cfg = capi.RuntimeConfig(self.mode, self.n_workers, max_inflight or 0, cb, None, self.poll_sleep_us)
+        # executors: enough that tool capacity never binds (the paper's tools -- interpreter, web
+        # search, validator -- run every call at once; the O-3 schedule assumes parallel instances)
+        workers = self.n_workers or min(2048, max(64, 4 * len(specs)))
+        cfg = capi.RuntimeConfig(self.mode, workers, max_inflight or 0, cb, None, self.poll_sleep_us)
         h = ctypes.c_void_p()
         check(L.cvy_runtime_create(self.eng.h, ctypes.byref(cfg), ctypes.byref(h)))
         keep = []
