@@ -1227,8 +1227,16 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
     g.epi = epi;
     if (e->bf16) {
         // gate/up: optionally stream-K over every SM instead of 112 whole 256-row tiles (A/B knob)
-        const bool gu_sk = epi.kind == EPI_SWIGLU && getenv("CVY_GU_STREAMK") && atoi(getenv("CVY_GU_STREAMK")) != 0;
-        const int gu_nsub = (epi.kind == EPI_SWIGLU && getenv("CVY_GU_NSUB")) ? atoi(getenv("CVY_GU_NSUB")) : 0;
+        bool gu_sk = epi.kind == EPI_SWIGLU && getenv("CVY_GU_STREAMK") && atoi(getenv("CVY_GU_STREAMK")) != 0;
+        int gu_nsub = (epi.kind == EPI_SWIGLU && getenv("CVY_GU_NSUB")) ? atoi(getenv("CVY_GU_NSUB")) : 0;
+        // A/B knob: stream-K for the epilogue kinds in the bit mask CVY_SK_KINDS (1 << EpiKind),
+        // with CVY_SK_NSUB 128-row sub-tiles per tile
+        if (const char* v = getenv("CVY_SK_KINDS"))
+            if (Bp > 128 && ((atoi(v) >> epi.kind) & 1) && epi.kind != EPI_LMHEAD &&
+                K <= (getenv("CVY_SK_MAXK") ? atoi(getenv("CVY_SK_MAXK")) : 1 << 30)) {
+                gu_sk = true;
+                if (const char* ns = getenv("CVY_SK_NSUB")) gu_nsub = atoi(ns);
+            }
         if (!gemm_config(g, N, K, Bp, sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub,
                          gemm_epi_groups(epi.kind)))
             return false;
