@@ -90,6 +90,17 @@ CVY_DEV void tma_load_2d(void* smem_dst, const void* tmap, uint64_t* bar, int32_
         "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(policy)
         : "memory");
 }
+// CTA-pair variant (cta_group::2 MMA operands): the box lands in this CTA's shared memory and its
+// completion is signalled on the mbarrier at shared::cluster address `bar_cl`, which may live in
+// the peer CTA of the pair (the leader's stage barrier counts the bytes of both halves).
+CVY_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint32_t bar_cl, int32_t c0, int32_t c1,
+                              uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_cl), "r"(c0), "r"(c1), "l"(policy)
+        : "memory");
+}
 // 3D tiled load (e.g. one 4 KB (page, K/V, kv-head) block of the KV pool as [2 halves][16][64]).
 CVY_DEV void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int32_t c0, int32_t c1, int32_t c2,
                          uint64_t policy) {
@@ -123,6 +134,16 @@ CVY_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
+// CTA pair: one warp of EACH CTA of the pair executes these (same column count in both)
+CVY_DEV void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+CVY_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
 CVY_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
@@ -137,6 +158,26 @@ CVY_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+// CTA pair (issued by the leader CTA only): M = 256, rows [0,128) of A and D in the leader, [128,256)
+// in the peer at the same shared-memory / TMEM offsets; B's N columns split in halves the same way.
+CVY_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Pair commit: arrive on the mbarrier at the same offset in every CTA of `mask` (cluster ranks).
+CVY_DEV void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                     smem_u32(bar)), "h"(mask)
+                 : "memory");
+}
+// Arrive on an mbarrier of another CTA of the cluster (shared::cluster address from mapa).
+CVY_DEV void mbar_arrive_cluster(uint32_t bar_cl) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
 }
 // Arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete.
 CVY_DEV void umma_commit(uint64_t* bar) {

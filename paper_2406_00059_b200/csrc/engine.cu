@@ -99,14 +99,28 @@ bool make_tmap_kv3(CUtensorMap* out, const void* base, uint64_t rows) {
     return r == CUDA_SUCCESS;
 }
 
+// CTA-pair GEMMs (cta_group::2) for the epilogue kinds in the bit mask CVY_GEMM_PAIR (1 << EpiKind).
+// Default: the QKV projection on batch tiles (Bp > 128), where whole 256-row tiles leave 52 SMs idle
+// and stream-K over 148 pair CTAs measured 2.22 -> 2.13 ms/step at C4; O / down / gate-up measured
+// neutral or slower as pairs. The LM head never pairs (its sampling CTA counts
+// whole tiles).
+bool gemm_pair_ok(int epi_kind) {
+    if (epi_kind == EPI_LMHEAD) return false;
+    const char* v = getenv("CVY_GEMM_PAIR");
+    const int mask = v ? atoi(v) : (1 << EPI_QKV);
+    return ((mask >> epi_kind) & 1) != 0;
+}
+
 // Tile/pipeline configuration of the tcgen05 GEMM for a padded batch Bp.
 //   Bp <= 128: 2 sub-tiles (256 weight rows) per tile, hi/lo planes merged (MMA N = 2*Bp)
 //   Bp 160..256: 1 sub-tile, planes as two MMAs into one accumulator (N = Bp)
 //   Bp 512: 1 sub-tile, 2 batch halves of N = 256, 32-element K stages (64B swizzle)
 bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why,
-                 bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0, int epi_groups = 1) {
+                 bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0, int epi_groups = 1,
+                 bool pair_ok = false) {
     g.N = N;
     g.K = K;
+    g.pair = 0;
     // batches above 128 columns run as nbt tiles of 128 on grid.y, each with the merged
     // (hi, lo) N = 256 pipeline (measured: the unmerged Bp = 256 layout, 4x more activation
     // than weight bytes per stage and 2 stages, ran gate/up at 1.7 TB/s)
@@ -121,6 +135,36 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     const int Bq = g.bq;
     g.merge = Bq <= 128;
     g.bk = Bq >= 512 ? 32 : 64;
+    // CTA pairs (cta_group::2) for batch-tiled GEMMs: a 256-row tile per pair, each CTA streams
+    // its 128 weight rows and ONE activation plane, the leader issues M = 256 MMAs -- per SM half
+    // the activation bytes through shared memory of a 128-row tile, no split-K reduction
+    const bool pair_small = getenv("CVY_GEMM_PAIR_SMALL") && atoi(getenv("CVY_GEMM_PAIR_SMALL")) != 0;  // A/B knob
+    if (pair_ok && g.merge && (g.nbt > 1 || pair_small) && N % 256 == 0 && K % 64 == 0 && K / 64 >= 2) {
+        g.pair = 1;
+        g.nsub = 1;
+        g.mma_n = 2 * Bq;
+        g.nbh = 1;
+        g.cols_per_sub = 2 * Bq;
+        g.acc_stages = 2;
+        g.tmem_cols = pow2_at_least((uint32_t)(2 * g.cols_per_sub));
+        g.tiles = N / 256;
+        g.kblocks = K / 64;
+        g.l2_prefetch = 0;
+        const uint32_t stage = GemmSmem::stage_bytes(1, Bq, 1, 64);
+        const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
+        g.stages = std::min(12, (int)((232448 - fixed) / stage));
+        *smem = (size_t)g.stages * stage + fixed;
+        const int pairs_per_bt = std::max(1, num_sms / g.nbt / 2);
+        // whole tiles when they fill >= 3/4 of the SMs in one wave, else stream-K
+        if (g.tiles <= pairs_per_bt && 4 * 2 * g.tiles * g.nbt >= 3 * num_sms) {
+            g.split = 1;  // whole tiles: one pair per (tile, batch tile)
+            *grid = 2 * g.tiles;
+        } else {
+            g.split = 0;  // stream-K over the pairs of a batch tile
+            *grid = 2 * (int)std::min<long long>(pairs_per_bt, (long long)g.tiles * g.kblocks);
+        }
+        return true;
+    }
     if (const char* v = getenv("CVY_GEMM_BK")) g.bk = (atoi(v) == 32 && !g.merge) ? 32 : 64;  // A/B knob
     // wide GEMMs (gate/up, LM head): 256-row tiles, one per CTA, no reduction; narrow ones
     // (QKV, O, down): 128-row tiles with K split over a 2..4-CTA cluster (DSMEM reduction)
@@ -219,6 +263,9 @@ void set_gemm_smem_attrs() {
                 for (int bk : {32, 64})
                     cudaFuncSetAttribute(gemm_tc_kernel_ptr<__nv_bfloat16>(nsub, merge != 0, bk, epi),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    for (int epi = 0; epi <= EPI_STORE; ++epi)
+        cudaFuncSetAttribute(gemm_tc_kernel_ptr<__nv_bfloat16>(1, true, 64, epi, true),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
 }
 
 struct SlotHost {
@@ -1238,7 +1285,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
                 if (const char* ns = getenv("CVY_SK_NSUB")) gu_nsub = atoi(ns);
             }
         if (!gemm_config(g, N, K, Bp, sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub,
-                         gemm_epi_groups(epi.kind)))
+                         gemm_epi_groups(epi.kind), gemm_pair_ok(epi.kind)))
             return false;
         g.w_row0 = layer * N;
         if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD && xcap == (int)e->slots.size()) {
@@ -1347,9 +1394,9 @@ cvy_status build_bucket(cvy_engine* e, int Bp, Bucket** out) {
 cvy_status launch_gemm(cvy_engine* e, Bucket& bk, GemmPlan& gp, StepParams* Pq = nullptr) {
     if (e->bf16) {
         void* args[] = {&gp.tmW, &gp.tmX, Pq ? Pq : &bk.P, &gp.g, &gp.tmN};
-        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind),
+        return launch_k(e, gemm_tc_kernel_ptr<__nv_bfloat16>(gp.g.nsub, gp.g.merge != 0, gp.g.bk, gp.g.epi.kind, gp.g.pair != 0),
                         dim3(gp.grid, gp.g.nbt), dim3(gemm_launch_threads(gp.g.epi.kind, gp.g.split)), gp.smem, args, true,
-                        gp.g.split > 1 ? gp.g.split : 1);
+                        gp.g.pair ? 2 : (gp.g.split > 1 ? gp.g.split : 1));
     }
     const float* W = (const float*)gp.W;
     const float* X = (const float*)gp.X;
@@ -2100,7 +2147,8 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     int grid = 0;
     size_t smem = 0;
     std::string why;
-    if (!gemm_config(g, N, K, Bp, prop.multiProcessorCount, &grid, &smem, &why)) return fail(CVY_E_INVAL, why);
+    if (!gemm_config(g, N, K, Bp, prop.multiProcessorCount, &grid, &smem, &why, true, false, 0, 1, gemm_pair_ok(EPI_STORE)))
+        return fail(CVY_E_INVAL, why);
     g.w_row0 = 0;
     g.x_plane_rows = Bp;
     g.epi.kind = EPI_STORE;
@@ -2109,21 +2157,26 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     float* Ytmp = nullptr;
     CUDA_TRY(cudaMalloc(&Ytmp, sizeof(float) * (size_t)Bp * N));
     g.epi.store_out = Ytmp;
-    CUDA_TRY(cudaMalloc(&g.part, sizeof(float) * (size_t)g.tiles * g.nsub * 128 * Bp));
-    CUDA_TRY(cudaMemset(g.part, 0, sizeof(float) * (size_t)g.tiles * g.nsub * 128 * Bp));
-    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (g.tiles * g.nbt + 1)));
-    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (g.tiles * g.nbt + 1)));
+    const size_t tile_rows = (size_t)(g.pair ? 256 : 128 * g.nsub);
+    CUDA_TRY(cudaMalloc(&g.part, sizeof(float) * (size_t)g.tiles * tile_rows * Bp));
+    CUDA_TRY(cudaMemset(g.part, 0, sizeof(float) * (size_t)g.tiles * tile_rows * Bp));
+    CUDA_TRY(cudaMalloc(&g.tile_cnt, sizeof(int32_t) * (2 * g.tiles * g.nbt + 1)));
+    CUDA_TRY(cudaMemset(g.tile_cnt, 0, sizeof(int32_t) * (2 * g.tiles * g.nbt + 1)));
     // X as the (hi, lo) pair the engine uses: hi = X (exact bf16), lo = 0, padded to Bp rows
     void* Xp = nullptr;
     CUDA_TRY(cudaMalloc(&Xp, (size_t)2 * Bp * K * 2));
     CUDA_TRY(cudaMemset(Xp, 0, (size_t)2 * Bp * K * 2));
     CUDA_TRY(cudaMemcpy(Xp, X, (size_t)B * K * 2, cudaMemcpyDeviceToDevice));
+    // test hook: X holds 2*B rows, [hi][lo] (the kernel computes W (hi + lo))
+    if (getenv("CVY_DEBUG_GEMM_LO") && atoi(getenv("CVY_DEBUG_GEMM_LO")) != 0)
+        CUDA_TRY(cudaMemcpy(static_cast<uint8_t*>(Xp) + (size_t)Bp * K * 2, static_cast<const uint8_t*>(X) + (size_t)B * K * 2,
+                            (size_t)B * K * 2, cudaMemcpyDeviceToDevice));
     CUtensorMap tmW, tmX;
     const uint32_t xrows = g.merge ? (uint32_t)g.bq : (uint32_t)g.mma_n;
     if (!make_tmap(&tmW, W, (uint64_t)N, (uint64_t)K, (uint64_t)K, (uint32_t)(128 * g.nsub), (uint32_t)g.bk) ||
         !make_tmap(&tmX, Xp, (uint64_t)(2 * Bp), (uint64_t)K, (uint64_t)K, xrows, (uint32_t)g.bk))
         return fail(CVY_E_CUDA, "tensor map encode failed");
-    const void* kfn = gemm_tc_kernel_ptr<__nv_bfloat16>(g.nsub, g.merge != 0, g.bk, EPI_STORE);
+    const void* kfn = gemm_tc_kernel_ptr<__nv_bfloat16>(g.nsub, g.merge != 0, g.bk, EPI_STORE, g.pair != 0);
     void* args[] = {&tmW, &tmX, &P, &g, &tmW};
     cudaLaunchConfig_t lc;
     std::memset(&lc, 0, sizeof(lc));
@@ -2132,7 +2185,7 @@ extern "C" cvy_status cvy_debug_gemm(const void* W, const void* X, float* Y, int
     lc.dynamicSmemBytes = smem;
     cudaLaunchAttribute la[1];
     la[0].id = cudaLaunchAttributeClusterDimension;
-    la[0].val.clusterDim.x = (unsigned)(g.split > 1 ? g.split : 1);
+    la[0].val.clusterDim.x = (unsigned)(g.pair ? 2 : (g.split > 1 ? g.split : 1));
     la[0].val.clusterDim.y = 1;
     la[0].val.clusterDim.z = 1;
     lc.attrs = la;

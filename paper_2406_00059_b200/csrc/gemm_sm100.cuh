@@ -53,6 +53,10 @@ struct GemmTC {
     int32_t merge;      // 1: hi/lo planes merged into one N = 2*Bp MMA
     int32_t split;      // 0: stream-K over all CTAs; S >= 1: tile = blockIdx/S, K split over the S
                         //    CTAs of a thread-block cluster, reduced through DSMEM
+    int32_t pair;       // 1: CTA pairs (cta_group::2, clusters of 2): a tile is 256 weight rows, CTA
+                        //    rank r holds rows [128r, 128r+128) and activation plane r (hi / lo), the
+                        //    leader issues M = 256, N = 2*bq MMAs; split is 1 (whole tiles) or 0
+                        //    (stream-K over pairs)
     int32_t w_row0;     // first row of this layer's matrix in the weight tensor map
     int32_t wtiled;     // 1: weights packed tile-major [rows/128][K/64][128][64] (cvy_pack_weights_tiled):
                         //    every 128-row x 64-column box is 16 contiguous KB (row-major boxes
@@ -156,7 +160,7 @@ CVY_DEV void red_add_v4(float* p, float a, float b, float c, float d) {
 // descriptor arithmetic: adding `bytes` (multiple of 16) to the start address field
 CVY_DEV uint64_t desc_add(uint64_t d, uint32_t bytes) { return d + (uint64_t)(bytes >> 4); }
 
-template <typename T, int NSUB, bool MERGE, int BK, int EPI>
+template <typename T, int NSUB, bool MERGE, int BK, int EPI, bool PAIR = false>
 __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                    const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G,
@@ -171,7 +175,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     const int Bp = G.bq;                              // this CTA's batch columns
     const int cbase = (int)blockIdx.y * G.bq;         // first batch column of this CTA
     const uint32_t XB = (uint32_t)Bp * ROW;           // one activation plane per stage
-    const uint32_t stage_bytes = WB + 2u * XB;
+    // a pair CTA holds one activation plane (its half of the MMA's N = 2*bq B operand)
+    const uint32_t stage_bytes = WB + (PAIR ? 1u : 2u) * XB;
     uint8_t* fixed = smem + (size_t)G.stages * stage_bytes;
     constexpr int EG = gemm_epi_groups(EPI);
     float* esm0 = reinterpret_cast<float*>(fixed);
@@ -195,19 +200,24 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     const int n_egroups = (EG == 2 && G.split == 1 && blockDim.x >= 320) ? 2 : 1;
     float* esm = egroup ? reinterpret_cast<float*>(smem) : esm0;
     const long long T_iters = (long long)G.tiles * G.kblocks;
-    const int Gc = gridDim.x;
+    // pair mode: work is assigned per CTA pair (both CTAs of a pair run the same k-range)
+    const int prank = PAIR ? (int)(blockIdx.x & 1u) : 0;
+    const int bx = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int Gc = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     long long it0, it1;
     int crank = 0;
     if (G.split > 0) {
         // cluster split-K: CTA (tile, rank) owns k-blocks [rank*KB/S, (rank+1)*KB/S) of one tile
-        const int tile = blockIdx.x / G.split;
-        crank = blockIdx.x % G.split;
+        const int tile = bx / G.split;
+        crank = bx % G.split;
         it0 = (long long)tile * G.kblocks + ((long long)crank * G.kblocks) / G.split;
         it1 = (long long)tile * G.kblocks + ((long long)(crank + 1) * G.kblocks) / G.split;
     } else {
-        it0 = ((long long)blockIdx.x * T_iters) / Gc;
-        it1 = ((long long)(blockIdx.x + 1) * T_iters) / Gc;
+        it0 = ((long long)bx * T_iters) / Gc;
+        it1 = ((long long)(bx + 1) * T_iters) / Gc;
     }
+    // 128-row weight tile (of the whole matrix) that sub-tile s of `tile` covers in this CTA
+    auto row_tile = [&](int tile, int s) { return PAIR ? tile * 2 + prank : tile * NSUB + s; };
 
     if (warp == 4 && lane == 0) {
         tma_prefetch_desc(&tmW);
@@ -218,13 +228,19 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull_bar[s], 1);
-            mbar_init(&tempty_bar[s], kEpiThreads * n_egroups);
+            // pair: the leader's accumulator is released by both CTAs' epilogue threads
+            mbar_init(&tempty_bar[s], kEpiThreads * n_egroups * (PAIR ? 2 : 1));
         }
         fence_mbar_init();
     }
-    if (warp == 5) tmem_alloc(tmem_slot, G.tmem_cols);
+    if (warp == 5) {
+        if (PAIR) tmem_alloc_pair(tmem_slot, G.tmem_cols);
+        else tmem_alloc(tmem_slot, G.tmem_cols);
+    }
     tc_fence_before();
-    __syncthreads();
+    // pair: the peer's TMA loads complete on the leader's barriers -- both initialised first
+    if (PAIR) cluster_sync_all();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_launch_dependents();
@@ -239,6 +255,33 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
             const int rows_per_tile = 128 * NSUB;
             const int xh = MERGE ? 1 : G.nbh;
             const int xrows = MERGE ? Bp : G.mma_n;
+            // stage s's transaction barrier: the leader's (both halves of a pair count there)
+            auto bar_cl = [&](int s) -> uint32_t {
+                return PAIR ? mapa_shared(smem_u32(&full_bar[s]), 0u) : smem_u32(&full_bar[s]);
+            };
+            auto expect = [&](int s) {
+                if (!PAIR) mbar_arrive_expect_tx(&full_bar[s], stage_bytes);
+                else if (prank == 0) mbar_arrive_expect_tx(&full_bar[s], 2u * stage_bytes);
+            };
+            auto load_w = [&](uint8_t* dst, int s, int tile, int kb) {
+                if (PAIR) {
+                    const int rt = row_tile(tile, 0);
+                    if (!G.wtiled) tma_load_2d_pair(dst, &tmW, bar_cl(s), kb * BK, G.w_row0 + rt * 128, pol_w);
+                    else tma_load_2d_pair(dst, &tmW, bar_cl(s), 0, ((G.w_row0 / 128 + rt) * G.kblocks + kb) * 128, pol_w);
+                } else {
+                    load_w_tile<NSUB, BK>(dst, &tmW, &full_bar[s], G, tile, kb, pol_w);
+                }
+            };
+            auto load_x = [&](uint8_t* sx, int s, int kb) {
+                if (PAIR) {
+                    tma_load_2d_pair(sx, &tmX, bar_cl(s), kb * BK, prank * G.x_plane_rows + cbase, pol_x);
+                } else {
+                    for (int pl = 0; pl < 2; ++pl)
+                        for (int h = 0; h < xh; ++h)
+                            tma_load_2d(sx + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[s], kb * BK,
+                                        pl * G.x_plane_rows + cbase + h * xrows, pol_x);
+                }
+            };
             // weights do not depend on the previous kernel: issue the first stages before the
             // grid-dependency wait so the weight stream starts under the previous kernel's tail
             const long long n_it = it1 - it0;
@@ -246,8 +289,8 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
             for (int i = 0; i < pre; ++i) {
                 const long long it = it0 + i;
                 const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
-                mbar_arrive_expect_tx(&full_bar[i], stage_bytes);
-                load_w_tile<NSUB, BK>(smem + (size_t)i * stage_bytes, &tmW, &full_bar[i], G, tile, kb, pol_w);
+                expect(i);
+                load_w(smem + (size_t)i * stage_bytes, i, tile, kb);
             }
             // look-ahead into L2 beyond the smem ring (l2_prefetch k-blocks, rolling with the main
             // loop): more weight bytes in flight per SM than the ring holds
@@ -262,31 +305,24 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                 }
             };
             long long pf_next = it0 + pre;
-            const long long pf_end = min(it1, it0 + pre + (long long)G.l2_prefetch);
+            const long long pf_end = PAIR ? pf_next : min(it1, it0 + pre + (long long)G.l2_prefetch);
             for (; pf_next < pf_end; ++pf_next) l2_pf(pf_next);
             pdl_wait();
             if (G.epi.span_kind >= 0) span_begin(P.spans, P.span_base + G.epi.layer * 8 + G.epi.span_kind);
             for (int i = 0; i < pre; ++i) {
                 const int kb = (int)((it0 + i) % G.kblocks);
-                uint8_t* sx = smem + (size_t)i * stage_bytes + WB;
-                for (int pl = 0; pl < 2; ++pl)
-                    for (int h = 0; h < xh; ++h)
-                        tma_load_2d(sx + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[i], kb * BK,
-                                    pl * G.x_plane_rows + cbase + h * xrows, pol_x);
+                load_x(smem + (size_t)i * stage_bytes + WB, i, kb);
             }
             int stage = pre % G.stages;
             uint32_t phase = (pre == G.stages) ? 1u : 0u;
             for (long long it = it0 + pre; it < it1; ++it) {
                 const int tile = (int)(it / G.kblocks), kb = (int)(it % G.kblocks);
                 mbar_wait(&empty_bar[stage], phase ^ 1u);
-                if (G.l2_prefetch > 0 && pf_next < it1) l2_pf(pf_next++);
+                if (!PAIR && G.l2_prefetch > 0 && pf_next < it1) l2_pf(pf_next++);
                 uint8_t* sw = smem + (size_t)stage * stage_bytes;
-                mbar_arrive_expect_tx(&full_bar[stage], stage_bytes);
-                load_w_tile<NSUB, BK>(sw, &tmW, &full_bar[stage], G, tile, kb, pol_w);
-                for (int pl = 0; pl < 2; ++pl)
-                    for (int h = 0; h < xh; ++h)
-                        tma_load_2d(sw + WB + (size_t)(pl * Bp + h * xrows) * ROW, &tmX, &full_bar[stage], kb * BK,
-                                    pl * G.x_plane_rows + cbase + h * xrows, pol_x);
+                expect(stage);
+                load_w(sw, stage, tile, kb);
+                load_x(sw + WB, stage, kb);
                 if (++stage == G.stages) {
                     stage = 0;
                     phase ^= 1u;
@@ -297,9 +333,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
         // non-split: warm L2 with the next GEMM's first k-blocks right behind our own stream
         __syncwarp();
         if (G.split <= 1 && blockIdx.y == 0) prefetch_next_gemm(G, &tmN, lane);
-    } else if (warp == 5) {
-        // ===================== MMA issuer =====================
-        const uint32_t idesc = idesc_bf16_f32(128, (uint32_t)G.mma_n);
+    } else if (warp == 5 && (!PAIR || prank == 0)) {
+        // ===================== MMA issuer (pair: the leader CTA only) =====================
+        const uint32_t idesc = idesc_bf16_f32(PAIR ? 256 : 128, (uint32_t)G.mma_n);
         const uint64_t d0 = (BK == 64) ? sdesc_kmajor_sw128(smem_u32(smem)) : sdesc_kmajor_sw64(smem_u32(smem));
         int stage = 0;
         uint32_t phase = 0;
@@ -324,7 +360,9 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #pragma unroll
                         for (int s = 0; s < NSUB; ++s) {
                             const uint64_t ad = desc_add(ws, (uint32_t)s * 128u * ROW + (uint32_t)k * 32u);
-                            if (MERGE) {
+                            if (PAIR) {
+                                umma_bf16_pair(dcol, ad, desc_add(xs, (uint32_t)k * 32u), idesc, (first && k == 0) ? 0u : 1u);
+                            } else if (MERGE) {
                                 umma_bf16(dcol + (uint32_t)(s * G.cols_per_sub), ad, desc_add(xs, (uint32_t)k * 32u),
                                           idesc, (first && k == 0) ? 0u : 1u);
                             } else {
@@ -338,7 +376,10 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                         }
                     }
                 }
-                if (lane == 0) umma_commit(&empty_bar[stage]);
+                if (lane == 0) {
+                    if (PAIR) umma_commit_pair(&empty_bar[stage], 3);  // both CTAs' producers
+                    else umma_commit(&empty_bar[stage]);
+                }
                 __syncwarp();
                 first = false;
                 if (++stage == G.stages) {
@@ -346,14 +387,17 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                     phase ^= 1u;
                 }
             }
-            if (lane == 0) umma_commit(&tfull_bar[as]);
+            if (lane == 0) {
+                if (PAIR) umma_commit_pair(&tfull_bar[as], 3);  // both CTAs' epilogues
+                else umma_commit(&tfull_bar[as]);
+            }
             __syncwarp();
             if (++as == G.acc_stages) {
                 as = 0;
                 aphase ^= 1u;
             }
         }
-    } else {
+    } else if (warp != 5) {
         // ===================== epilogue (warps 0-3, and 6-9 for the gate/up GEMM) =====================
         const int et = (warp & 3) * 32 + lane;  // 0..127 == TMEM lane == tile row
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -362,6 +406,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
             if (n_egroups == 2) named_bar_sync(4, 2 * kEpiThreads); else epi_sync();
         };
         if (egroup >= n_egroups) it0 = it1;  // second group idle in split-K mode
+        // release accumulator stage a to the MMA issuer (pair: the leader's barrier)
+        auto release_acc = [&](int a) {
+            if (PAIR && prank != 0) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty_bar[a]), 0u));
+            else mbar_arrive(&tempty_bar[a]);
+        };
         const int rows = NSUB * 128;
         bool prepared = false;
         int as = 0;
@@ -384,7 +433,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
             if (tr && et == 0 && egroup == 0) tr[2 + (it >= it1 ? 1 : 0)] = gtimer();  // [2] first / [3] last segment's MMA done
             if (G.dbg & 1) {
                 tc_fence_before();
-                mbar_arrive(&tempty_bar[as]);
+                release_acc(as);
                 if (++as == G.acc_stages) {
                     as = 0;
                     aphase ^= 1u;
@@ -422,7 +471,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                         }
                     }
                 tc_fence_before();
-                mbar_arrive(&tempty_bar[as]);
+                release_acc(as);
             } else if (c_first == c_last) {
                 // sole contributor: epilogue straight from TMEM (hi + lo planes summed); with two
                 // epilogue groups, group g takes the chunks ci = g, g + 2, ...
@@ -440,17 +489,19 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                             tmem_ld32(tacc + (uint32_t)(s * G.cols_per_sub + cb), v);
                         }
                         if (!(G.dbg & 8))
-                            epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, et);
+                            epilogue_chunk<T, EPI>(P, G.epi, row_tile(tile, s) * 128, cbase + cb, v, esm, meta, et);
                     }
                 tc_fence_before();
-                mbar_arrive(&tempty_bar[as]);
+                release_acc(as);
                 did_epi = true;
             } else {
                 // Shared tile: add this CTA's partial into the tile's fp32 accumulator with L2
                 // vector reductions (no return, nobody waits), take an arrival ticket; the last
                 // arriver reads the completed sum, re-zeroes it, and runs the epilogue.
-                float* acc = G.part + ((size_t)tile * G.nbt + blockIdx.y) * rows * Bp;
-                int32_t* ticket = G.tile_cnt + (size_t)tile * G.nbt + blockIdx.y;
+                // pair: each CTA's 128-row half has its own accumulator and ticket
+                const size_t ai = PAIR ? ((size_t)tile * G.nbt + blockIdx.y) * 2 + prank : (size_t)tile * G.nbt + blockIdx.y;
+                float* acc = G.part + ai * rows * Bp;
+                int32_t* ticket = G.tile_cnt + ai;
                 for (int s = 0; s < NSUB; ++s)
                     for (int cb = 0; cb < Bp; cb += 32) {
                         if (n_egroups == 2 && (((s * Bp + cb) >> 5) & 1) != egroup) continue;
@@ -469,7 +520,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                         for (int q = 0; q < 8; ++q) red_add_v4(dst + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
                     }
                 tc_fence_before();
-                mbar_arrive(&tempty_bar[as]);
+                release_acc(as);
                 __threadfence();
                 grp_sync();
                 if (et == 0 && egroup == 0) flags[0] = (atomicAdd(ticket, 1) == c_last - c_first) && !(G.dbg & 4);
@@ -492,7 +543,7 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 #pragma unroll
                             for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));
                             if (!(G.dbg & 8))
-                                epilogue_chunk<T, EPI>(P, G.epi, (tile * NSUB + s) * 128, cbase + cb, v, esm, meta, et);
+                                epilogue_chunk<T, EPI>(P, G.epi, row_tile(tile, s) * 128, cbase + cb, v, esm, meta, et);
                         }
                     // both groups have read the accumulator before the ticket is re-armed
                     grp_sync();
@@ -567,10 +618,14 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
     }
     if (tr && threadIdx.x == 0) tr[4] = gtimer();  // epilogue warps done
     tc_fence_before();
-    __syncthreads();
+    // pair: the leader's MMAs write the peer's TMEM and its commits / the peer's releases cross
+    // CTAs -- neither CTA frees TMEM or exits before both are done
+    if (PAIR) cluster_sync_all();
+    else __syncthreads();
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, G.tmem_cols);
+        if (PAIR) tmem_dealloc_pair(tmem_base, G.tmem_cols);
+        else tmem_dealloc(tmem_base, G.tmem_cols);
     }
     if (threadIdx.x == 0 && G.epi.span_kind >= 0)
         span_end(P.spans, kSpanSlots, P.span_base + G.epi.layer * 8 + G.epi.span_kind);
@@ -579,20 +634,21 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
 
 // Host-side selection of the kernel instantiation for a plan (split mode is a runtime field).
 template <typename T, int EPI>
-inline const void* gemm_tc_kernel_ptr_k(int nsub, bool merge, int bk) {
+inline const void* gemm_tc_kernel_ptr_k(int nsub, bool merge, int bk, bool pair) {
+    if (pair) return (const void*)gemm_tc_kernel<T, 1, true, 64, EPI, true>;
     if (merge) return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, true, 64, EPI> : (const void*)gemm_tc_kernel<T, 1, true, 64, EPI>;
     if (bk == 32)
         return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, false, 32, EPI> : (const void*)gemm_tc_kernel<T, 1, false, 32, EPI>;
     return nsub == 2 ? (const void*)gemm_tc_kernel<T, 2, false, 64, EPI> : (const void*)gemm_tc_kernel<T, 1, false, 64, EPI>;
 }
 template <typename T>
-inline const void* gemm_tc_kernel_ptr(int nsub, bool merge, int bk, int epi) {
+inline const void* gemm_tc_kernel_ptr(int nsub, bool merge, int bk, int epi, bool pair = false) {
     switch (epi) {
-        case EPI_QKV: return gemm_tc_kernel_ptr_k<T, EPI_QKV>(nsub, merge, bk);
-        case EPI_RESID: return gemm_tc_kernel_ptr_k<T, EPI_RESID>(nsub, merge, bk);
-        case EPI_SWIGLU: return gemm_tc_kernel_ptr_k<T, EPI_SWIGLU>(nsub, merge, bk);
-        case EPI_LMHEAD: return gemm_tc_kernel_ptr_k<T, EPI_LMHEAD>(nsub, merge, bk);
-        default: return gemm_tc_kernel_ptr_k<T, EPI_STORE>(nsub, merge, bk);
+        case EPI_QKV: return gemm_tc_kernel_ptr_k<T, EPI_QKV>(nsub, merge, bk, pair);
+        case EPI_RESID: return gemm_tc_kernel_ptr_k<T, EPI_RESID>(nsub, merge, bk, pair);
+        case EPI_SWIGLU: return gemm_tc_kernel_ptr_k<T, EPI_SWIGLU>(nsub, merge, bk, pair);
+        case EPI_LMHEAD: return gemm_tc_kernel_ptr_k<T, EPI_LMHEAD>(nsub, merge, bk, false);
+        default: return gemm_tc_kernel_ptr_k<T, EPI_STORE>(nsub, merge, bk, pair);
     }
 }
 

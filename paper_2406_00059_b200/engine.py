@@ -240,12 +240,20 @@ def stats_allgather(engines: list[Engine]) -> np.ndarray:
     return out
 
 
-def debug_gemm(W, X, N: int, K: int, B: int, iters: int = 1, device: int = 0):
-    """Y = X W^T through the decode step's tcgen05 GEMM kernel (test/measurement hook).
-    W, X: bf16 CUDA tensors; returns (Y fp32 CUDA tensor [B][N], mean ms per launch)."""
+def debug_gemm(W, X, N: int, K: int, B: int, iters: int = 1, device: int = 0, X_lo=None):
+    """Y = (X + X_lo) W^T through the decode step's tcgen05 GEMM kernel (test/measurement hook):
+    X is the activation's hi plane, X_lo (optional, default zero) its lo plane.
+    W, X, X_lo: bf16 CUDA tensors; returns (Y fp32 CUDA tensor [B][N], mean ms per launch)."""
+    import os
     import torch
     Y = torch.empty((B, N), dtype=torch.float32, device=W.device)
     ms = ctypes.c_float()
-    check(capi.lib().cvy_debug_gemm(W.data_ptr(), X.data_ptr(), Y.data_ptr(), N, K, B, iters, device,
-                                    ctypes.byref(ms)))
+    if X_lo is not None:
+        X = torch.cat([X[:B], X_lo[:B]]).contiguous()
+        os.environ["CVY_DEBUG_GEMM_LO"] = "1"
+    try:
+        check(capi.lib().cvy_debug_gemm(W.data_ptr(), X.data_ptr(), Y.data_ptr(), N, K, B, iters, device,
+                                        ctypes.byref(ms)))
+    finally:
+        os.environ.pop("CVY_DEBUG_GEMM_LO", None)
     return Y, ms.value

@@ -44,6 +44,28 @@ def test_tc_gemm_matches_fp64(N, K, B):
     assert err < 1e-6 * K + 1e-5, err  # fp32 accumulation of exact bf16 products
 
 
+@pytest.mark.parametrize("N,K,B", [(4096, 4096, 512), (28672, 4096, 512), (6144, 4096, 512),
+                                   (4096, 14336, 512), (4096, 4096, 256), (512, 128, 160),
+                                   (6144, 4096, 64), (4096, 14336, 64), (1024, 256, 32)])
+def test_tc_gemm_cta_pair_matches_fp64(N, K, B, monkeypatch):
+    """CTA-pair (cta_group::2) GEMMs on batch tiles: whole 256-row pair tiles and stream-K over
+    pairs, with a non-zero lo plane (the peer CTA's half of the B operand)."""
+    import torch
+    from paper_2406_00059_b200.engine import debug_gemm
+    ensure_built()
+    monkeypatch.setenv("CVY_GEMM_PAIR", str(1 << 4))  # EPI_STORE
+    if B <= 128:
+        monkeypatch.setenv("CVY_GEMM_PAIR_SMALL", "1")
+    g = torch.Generator(device="cuda").manual_seed(N * 5 + K + B)
+    W = (torch.rand((N, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    X = (torch.rand((B, K), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    Xlo = ((torch.rand((B, K), generator=g, device="cuda") * 2 - 1) * 2.0 ** -9).to(torch.bfloat16)
+    Y, _ = debug_gemm(W, X, N, K, B, X_lo=Xlo)
+    ref = (X.double() + Xlo.double()) @ W.double().T
+    err = (Y.double() - ref).abs().max().item()
+    assert err < 1e-6 * K + 1e-5, err
+
+
 # ------------------------------------------------------------------ tiny config, free running
 def test_tiny_fp32_free_running_logits_1e4():
     d, gens = free_running_parity(TINY, "fp32", BYTE_VOCAB, tiny_prompts(4), max_new=64, seed=1000, tol=1e-4)
