@@ -1279,7 +1279,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
         // A/B knob: stream-K for the epilogue kinds in the bit mask CVY_SK_KINDS (1 << EpiKind),
         // with CVY_SK_NSUB 128-row sub-tiles per tile
         if (const char* v = getenv("CVY_SK_KINDS"))
-            if (Bp > 128 && ((atoi(v) >> epi.kind) & 1) && epi.kind != EPI_LMHEAD &&
+            if (Bp > 128 && ((atoi(v) >> epi.kind) & 1) &&
                 K <= (getenv("CVY_SK_MAXK") ? atoi(getenv("CVY_SK_MAXK")) : 1 << 30)) {
                 gu_sk = true;
                 if (const char* ns = getenv("CVY_SK_NSUB")) gu_nsub = atoi(ns);
