@@ -189,8 +189,11 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
         const uint32_t ph = (uint32_t)(t / STAGES) & 1u;
         const int wp = PPS == 4 ? warp : (warp & 1);    // this warp's page within the stage
         const int pidx = t * PPS + wp;                  // this warp's page in the split
+        // every consumer of the stage waits for its data, even one with no page in it (the last
+        // stage of an odd page count): its empty-barrier arrival must not count toward the
+        // slot's PREVIOUS phase while the other warp is still reading that phase's pages
+        mbar_wait(&full_bar[st], ph);
         if (pidx < n_pages) {
-            mbar_wait(&full_bar[st], ph);
             const uint32_t kbase = smem_u32(stages + (size_t)st * STAGE + (size_t)(wp * 2) * BLK);
             const uint32_t vbase = kbase + BLK;
             // ---- S^T = K . [q_hi|q_lo]^T

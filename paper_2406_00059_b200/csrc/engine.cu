@@ -100,14 +100,15 @@ bool make_tmap_kv3(CUtensorMap* out, const void* base, uint64_t rows) {
 }
 
 // CTA-pair GEMMs (cta_group::2) for the epilogue kinds in the bit mask CVY_GEMM_PAIR (1 << EpiKind).
-// Default: the QKV projection on batch tiles (Bp > 128), where whole 256-row tiles leave 52 SMs idle
-// and stream-K over 148 pair CTAs measured 2.22 -> 2.13 ms/step at C4; O / down / gate-up measured
-// neutral or slower as pairs. The LM head never pairs (its sampling CTA counts
-// whole tiles).
+// Default on batch tiles (Bp > 128): QKV (whole 256-row tiles left 52 SMs idle; stream-K over 144
+// pair CTAs) and gate/up (a single-CTA 256-row tile fills all 512 TMEM columns, so its epilogue
+// stalled the MMAs; a pair CTA's 128 rows double-buffer the accumulator): C4 QKV 2.22 -> 2.03,
+// gate/up 6.8 -> 5.9 ms/step. O / down (2-CTA cluster split-K) measured neutral as pairs
+// (DESIGN.md §7.3). The LM head never pairs (its sampling CTA counts whole tiles).
 bool gemm_pair_ok(int epi_kind) {
     if (epi_kind == EPI_LMHEAD) return false;
     const char* v = getenv("CVY_GEMM_PAIR");
-    const int mask = v ? atoi(v) : (1 << EPI_QKV);
+    const int mask = v ? atoi(v) : ((1 << EPI_QKV) | (1 << EPI_SWIGLU));
     return ((mask >> epi_kind) & 1) != 0;
 }
 
@@ -139,7 +140,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     // its 128 weight rows and ONE activation plane, the leader issues M = 256 MMAs -- per SM half
     // the activation bytes through shared memory of a 128-row tile, no split-K reduction
     const bool pair_small = getenv("CVY_GEMM_PAIR_SMALL") && atoi(getenv("CVY_GEMM_PAIR_SMALL")) != 0;  // A/B knob
-    if (pair_ok && g.merge && (g.nbt > 1 || pair_small) && N % 256 == 0 && K % 64 == 0 && K / 64 >= 2) {
+    if (pair_ok && g.merge && (g.nbt > 1 || pair_small) && N % 256 == 0 && K % 128 == 0 && K / 128 >= 2) {
         g.pair = 1;
         g.nsub = 1;
         g.mma_n = 2 * Bq;
@@ -148,9 +149,9 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         g.acc_stages = 2;
         g.tmem_cols = pow2_at_least((uint32_t)(2 * g.cols_per_sub));
         g.tiles = N / 256;
-        g.kblocks = K / 64;
+        g.kblocks = K / 128;  // pipeline stages of two 64-column k-blocks (gemm_sm100.cuh KB2)
         g.l2_prefetch = 0;
-        const uint32_t stage = GemmSmem::stage_bytes(1, Bq, 1, 64);
+        const uint32_t stage = 2 * GemmSmem::stage_bytes(1, Bq, 1, 64);
         const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
         g.stages = std::min(12, (int)((232448 - fixed) / stage));
         *smem = (size_t)g.stages * stage + fixed;
@@ -220,7 +221,9 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     if (g.merge && !getenv("CVY_GEMM_STREAMK") && !streamk && (g.nbt == 1 || !allow_kernel_split || bt_split)) {
         int S = 1;
         // the LM head counts completed tiles to elect the sampling CTA: whole tiles only
-        while (allow_kernel_split && S < kMaxSplit && g.tiles * g.nbt * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
+        int smax = kMaxSplit;
+        if (const char* v = getenv("CVY_GEMM_MAXSPLIT")) smax = std::max(1, std::min(kMaxSplit, atoi(v)));  // A/B knob
+        while (allow_kernel_split && S < smax && g.tiles * g.nbt * (S + 1) <= num_sms && S + 1 <= g.kblocks) ++S;
         if (S == 3 && !getenv("CVY_GEMM_ALLOW_S3")) S = 2;  // clusters of 3 do not pack onto the GPCs (measured: second wave)
         if ((bt_split ? g.tiles * g.nbt : g.tiles) <= num_sms) g.split = S;
         // the DSMEM staging of the partial must fit in the pipeline smem
@@ -1988,6 +1991,21 @@ cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap,
         case 3: src = e->d_o; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
         case 4: src = e->d_h; n = (e->bf16 ? 2 : 1) * B * e->act_ld * es; break;
         case 5: src = e->d_ssq; n = (size_t)(e->m.d_model / 128) * B * 4; break;
+        case 6: src = e->d_page_table; n = B * e->c.max_pages_per_slot * 4; break;
+        case 7:
+            if (!e->d_prow) return fail(CVY_E_STATE, "no chunked prefill");
+            src = e->d_prow;
+            n = (size_t)3 * kPrefillRows * 4;
+            break;
+        case 8: case 9: case 12 + 8: case 13 + 8: case 14 + 8:  // last prefill pass: x, q, o, h, act
+            if (!e->d_px) return fail(CVY_E_STATE, "no chunked prefill");
+            if (which == 8) { src = e->d_px; n = sizeof(float) * kPrefillRows * e->m.d_model; }
+            else if (which == 9) { src = e->d_pq; n = sizeof(float) * kPrefillRows * e->m.n_heads * e->m.head_dim; }
+            else {
+                src = which == 20 ? e->d_po : which == 21 ? e->d_ph : e->d_pact;
+                n = 2 * es * kPrefillRows * e->act_ld;
+            }
+            break;
         case 10: case 11: case 12: case 13:
             if (!e->d_trace) return fail(CVY_E_STATE, "set CVY_GEMM_TRACE_LAYER before engine create");
             src = e->d_trace + (size_t)(which - 10) * kTraceStride * e->num_sms;

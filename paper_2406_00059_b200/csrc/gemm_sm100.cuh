@@ -166,15 +166,18 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                    const __grid_constant__ StepParams P, const __grid_constant__ GemmTC G,
                    const __grid_constant__ CUtensorMap tmN) {
     constexpr uint32_t ROW = BK * 2;                  // bytes per smem row
-    constexpr uint32_t WB = NSUB * 128u * ROW;        // weight bytes per stage
-    constexpr int KSTEPS = BK / 16;
+    // a pair stage holds two BK-column k-blocks (8 MMAs per barrier round trip, as a 256-row
+    // single-CTA stage); G.kblocks counts stages
+    constexpr int KB2 = PAIR ? 2 : 1;
+    constexpr uint32_t WB = NSUB * 128u * ROW * KB2;  // weight bytes per stage
+    constexpr int KSTEPS = BK / 16 * KB2;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // aligned by an offset from smem_raw (not a uintptr round trip), so the compiler keeps the
     // shared state space and the epilogue's exchange / metadata accesses compile to LDS / STS
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int Bp = G.bq;                              // this CTA's batch columns
     const int cbase = (int)blockIdx.y * G.bq;         // first batch column of this CTA
-    const uint32_t XB = (uint32_t)Bp * ROW;           // one activation plane per stage
+    const uint32_t XB = (uint32_t)Bp * ROW * KB2;     // one activation plane per stage
     // a pair CTA holds one activation plane (its half of the MMA's N = 2*bq B operand)
     const uint32_t stage_bytes = WB + (PAIR ? 1u : 2u) * XB;
     uint8_t* fixed = smem + (size_t)G.stages * stage_bytes;
@@ -266,15 +269,23 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
             auto load_w = [&](uint8_t* dst, int s, int tile, int kb) {
                 if (PAIR) {
                     const int rt = row_tile(tile, 0);
-                    if (!G.wtiled) tma_load_2d_pair(dst, &tmW, bar_cl(s), kb * BK, G.w_row0 + rt * 128, pol_w);
-                    else tma_load_2d_pair(dst, &tmW, bar_cl(s), 0, ((G.w_row0 / 128 + rt) * G.kblocks + kb) * 128, pol_w);
+#pragma unroll
+                    for (int j = 0; j < KB2; ++j) {
+                        const int kc = kb * KB2 + j;  // BK-column k-block
+                        uint8_t* d = dst + j * 128 * ROW;
+                        if (!G.wtiled) tma_load_2d_pair(d, &tmW, bar_cl(s), kc * BK, G.w_row0 + rt * 128, pol_w);
+                        else tma_load_2d_pair(d, &tmW, bar_cl(s), 0, ((G.w_row0 / 128 + rt) * G.kblocks * KB2 + kc) * 128, pol_w);
+                    }
                 } else {
                     load_w_tile<NSUB, BK>(dst, &tmW, &full_bar[s], G, tile, kb, pol_w);
                 }
             };
             auto load_x = [&](uint8_t* sx, int s, int kb) {
                 if (PAIR) {
-                    tma_load_2d_pair(sx, &tmX, bar_cl(s), kb * BK, prank * G.x_plane_rows + cbase, pol_x);
+#pragma unroll
+                    for (int j = 0; j < KB2; ++j)
+                        tma_load_2d_pair(sx + (size_t)j * Bp * ROW, &tmX, bar_cl(s), (kb * KB2 + j) * BK,
+                                         prank * G.x_plane_rows + cbase, pol_x);
                 } else {
                     for (int pl = 0; pl < 2; ++pl)
                         for (int h = 0; h < xh; ++h)
@@ -361,7 +372,11 @@ __global__ void __launch_bounds__(gemm_threads(EPI), 1)
                         for (int s = 0; s < NSUB; ++s) {
                             const uint64_t ad = desc_add(ws, (uint32_t)s * 128u * ROW + (uint32_t)k * 32u);
                             if (PAIR) {
-                                umma_bf16_pair(dcol, ad, desc_add(xs, (uint32_t)k * 32u), idesc, (first && k == 0) ? 0u : 1u);
+                                // k-step k: k-block k / 4 of the stage, 16-column step k % 4
+                                const uint32_t j = (uint32_t)k / (BK / 16), kk = (uint32_t)k % (BK / 16);
+                                umma_bf16_pair(dcol, desc_add(ws, j * 128u * ROW + kk * 32u),
+                                               desc_add(xs, j * (uint32_t)Bp * ROW + kk * 32u), idesc,
+                                               (first && k == 0) ? 0u : 1u);
                             } else if (MERGE) {
                                 umma_bf16(dcol + (uint32_t)(s * G.cols_per_sub), ad, desc_add(xs, (uint32_t)k * 32u),
                                           idesc, (first && k == 0) ? 0u : 1u);

@@ -45,8 +45,9 @@ def test_tc_gemm_matches_fp64(N, K, B):
 
 
 @pytest.mark.parametrize("N,K,B", [(4096, 4096, 512), (28672, 4096, 512), (6144, 4096, 512),
-                                   (4096, 14336, 512), (4096, 4096, 256), (512, 128, 160),
-                                   (6144, 4096, 64), (4096, 14336, 64), (1024, 256, 32)])
+                                   (4096, 14336, 512), (4096, 4096, 256), (512, 256, 160),
+                                   (6144, 4096, 64), (4096, 14336, 64), (1024, 256, 32),
+                                   (28672, 4096, 256), (6144, 4096, 384), (28672, 4096, 384), (14336, 4096, 200)])
 def test_tc_gemm_cta_pair_matches_fp64(N, K, B, monkeypatch):
     """CTA-pair (cta_group::2) GEMMs on batch tiles: whole 256-row pair tiles and stream-K over
     pairs, with a non-zero lo plane (the peer CTA's half of the B operand)."""
@@ -801,3 +802,33 @@ def test_multi_tool_sets_bitexact(vocab_kind):
         n_tools_seen |= {r[8] for r in want if r[8] >= 0}
     assert n_tools_seen == set(ids.values())
     eng.close()
+
+
+def test_prefill_attention_is_deterministic_with_odd_page_counts():
+    """Regression: with 2 pages per stage, the warp of a pair that has no page in the last stage
+    (odd page count) used to arrive on the slot's empty barrier without waiting for the stage --
+    its arrival could complete the PREVIOUS phase while its partner was still reading, and the
+    producer overwrote that page (rows with 5 pages of keys came out wrong ~1 run in 4).  The
+    attention output of a chunked-prefill pass with such rows must be identical run to run."""
+    import ctypes
+    shape, vocab = slice_of(MISTRAL_7B, L=1, name="7b-L1"), synthetic_vocab(32000)
+    ref = None
+    for rep in range(6):
+        rng = random.Random(31)
+        flags = capi.ENGINE_DEBUG_LOGITS | capi.ENGINE_CHUNKED_PREFILL
+        dm, eng = make_engine(shape, "bf16", vocab, 5, 1010, flags=flags, max_pages_per_slot=16)
+        prompts = [[rng.randrange(3, shape.V) for _ in range(n)] for n in (1, 2, 17, 40, 65)]
+        for i, p in enumerate(prompts):
+            eng.submit_request(p, 3, synth_prefix_len=[0, 9, 0, 21, 3][i], synth_seed=40 + i)
+        eng.step()
+        eng.sync()
+        nb = ctypes.c_size_t()
+        assert capi.lib().cvy_debug_buffer(eng.h, 20, None, 0, ctypes.byref(nb)) == 0
+        o = np.zeros(nb.value, dtype=np.uint8)
+        assert capi.lib().cvy_debug_buffer(eng.h, 20, o.ctypes.data_as(ctypes.c_void_p), nb.value,
+                                           ctypes.byref(nb)) == 0
+        eng.close()
+        if ref is None:
+            ref = o
+        else:
+            assert np.array_equal(o, ref), f"attention output differs in repetition {rep}"
