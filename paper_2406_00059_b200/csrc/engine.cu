@@ -157,7 +157,8 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         *smem = (size_t)g.stages * stage + fixed;
         const int pairs_per_bt = std::max(1, num_sms / g.nbt / 2);
         // whole tiles when they fill >= 3/4 of the SMs in one wave, else stream-K
-        if (g.tiles <= pairs_per_bt && 4 * 2 * g.tiles * g.nbt >= 3 * num_sms) {
+        const bool force_sk = getenv("CVY_PAIR_STREAMK") && atoi(getenv("CVY_PAIR_STREAMK")) != 0;  // A/B knob
+        if (!force_sk && g.tiles <= pairs_per_bt && 4 * 2 * g.tiles * g.nbt >= 3 * num_sms) {
             g.split = 1;  // whole tiles: one pair per (tile, batch tile)
             *grid = 2 * g.tiles;
         } else {
