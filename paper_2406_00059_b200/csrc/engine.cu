@@ -103,12 +103,13 @@ bool make_tmap_kv3(CUtensorMap* out, const void* base, uint64_t rows) {
 // Default on batch tiles (Bp > 128): QKV (whole 256-row tiles left 52 SMs idle; stream-K over 144
 // pair CTAs) and gate/up (a single-CTA 256-row tile fills all 512 TMEM columns, so its epilogue
 // stalled the MMAs; a pair CTA's 128 rows double-buffer the accumulator): C4 QKV 2.22 -> 2.03,
-// gate/up 6.8 -> 5.9 ms/step. O / down (2-CTA cluster split-K) measured neutral as pairs
-// (DESIGN.md §7.3). The LM head never pairs (its sampling CTA counts whole tiles).
+// gate/up 6.8 -> 5.9 ms/step; O / down as whole pair tiles instead of the 2-CTA cluster split-K:
+// 1.40 -> 1.30 and 3.23 -> 3.13 ms/step (as stream-K pairs they lose, so they pair only when whole
+// tiles fill the GPU). DESIGN.md §7.3. The LM head never pairs (its sampling CTA counts whole tiles).
 bool gemm_pair_ok(int epi_kind) {
     if (epi_kind == EPI_LMHEAD) return false;
     const char* v = getenv("CVY_GEMM_PAIR");
-    const int mask = v ? atoi(v) : ((1 << EPI_QKV) | (1 << EPI_SWIGLU));
+    const int mask = v ? atoi(v) : ((1 << EPI_QKV) | (1 << EPI_RESID) | (1 << EPI_SWIGLU));
     return ((mask >> epi_kind) & 1) != 0;
 }
 
@@ -118,7 +119,7 @@ bool gemm_pair_ok(int epi_kind) {
 //   Bp 512: 1 sub-tile, 2 batch halves of N = 256, 32-element K stages (64B swizzle)
 bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t* smem, std::string* why,
                  bool allow_kernel_split = true, bool streamk = false, int nsub_override = 0, int epi_groups = 1,
-                 bool pair_ok = false) {
+                 bool pair_ok = false, bool pair_sk_ok = true) {
     g.N = N;
     g.K = K;
     g.pair = 0;
@@ -140,7 +141,12 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
     // its 128 weight rows and ONE activation plane, the leader issues M = 256 MMAs -- per SM half
     // the activation bytes through shared memory of a 128-row tile, no split-K reduction
     const bool pair_small = getenv("CVY_GEMM_PAIR_SMALL") && atoi(getenv("CVY_GEMM_PAIR_SMALL")) != 0;  // A/B knob
-    if (pair_ok && g.merge && (g.nbt > 1 || pair_small) && N % 256 == 0 && K % 128 == 0 && K / 128 >= 2) {
+    const bool force_sk = getenv("CVY_PAIR_STREAMK") && atoi(getenv("CVY_PAIR_STREAMK")) != 0;  // A/B knob
+    const int pair_tiles = N / 256, pairs_per_bt = std::max(1, num_sms / std::max(1, g.nbt) / 2);
+    // whole pair tiles when they fill >= 3/4 of the SMs in one wave, else stream-K over the pairs
+    const bool pair_whole = !force_sk && pair_tiles <= pairs_per_bt && 4 * 2 * pair_tiles * g.nbt >= 3 * num_sms;
+    if (pair_ok && (pair_whole || pair_sk_ok) && g.merge && (g.nbt > 1 || pair_small) && N % 256 == 0 &&
+        K % 128 == 0 && K / 128 >= 2) {
         g.pair = 1;
         g.nsub = 1;
         g.mma_n = 2 * Bq;
@@ -155,10 +161,7 @@ bool gemm_config(GemmTC& g, int N, int K, int Bp, int num_sms, int* grid, size_t
         const uint32_t fixed = GemmSmem::fixed_bytes(Bp) + 1024;
         g.stages = std::min(12, (int)((232448 - fixed) / stage));
         *smem = (size_t)g.stages * stage + fixed;
-        const int pairs_per_bt = std::max(1, num_sms / g.nbt / 2);
-        // whole tiles when they fill >= 3/4 of the SMs in one wave, else stream-K
-        const bool force_sk = getenv("CVY_PAIR_STREAMK") && atoi(getenv("CVY_PAIR_STREAMK")) != 0;  // A/B knob
-        if (!force_sk && g.tiles <= pairs_per_bt && 4 * 2 * g.tiles * g.nbt >= 3 * num_sms) {
+        if (pair_whole) {
             g.split = 1;  // whole tiles: one pair per (tile, batch tile)
             *grid = 2 * g.tiles;
         } else {
@@ -1289,7 +1292,7 @@ bool plan_gemm(cvy_engine* e, Bucket& bk, const void* Wbase, int N, int K, int l
                 if (const char* ns = getenv("CVY_SK_NSUB")) gu_nsub = atoi(ns);
             }
         if (!gemm_config(g, N, K, Bp, sms, &gp.grid, &gp.smem, why, epi.kind != EPI_LMHEAD, gu_sk, gu_nsub,
-                         gemm_epi_groups(epi.kind), gemm_pair_ok(epi.kind)))
+                         gemm_epi_groups(epi.kind), gemm_pair_ok(epi.kind), epi.kind != EPI_RESID))
             return false;
         g.w_row0 = layer * N;
         if (e->d_trace && layer == e->trace_layer && epi.kind != EPI_LMHEAD && xcap == (int)e->slots.size()) {
