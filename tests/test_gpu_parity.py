@@ -186,18 +186,19 @@ def test_7b_full_32_layers_bf16_b2():
     assert d < 2e-2
 
 
-def test_7b_width_large_batch_sampled():
-    """B=512 (validation-config batch) on a 1-layer 7B-width slice: every GEMM runs at Bp=512
-    (two UMMA N=256 halves); sampled requests are checked against the oracle one by one."""
+@pytest.mark.parametrize("B", [512, 200])
+def test_7b_width_large_batch_sampled(B):
+    """B=512 (validation-config batch) and B=200 (Bp=256) on a 1-layer 7B-width slice: every GEMM
+    runs on 128-column batch tiles (CTA pairs for QKV / gate-up, and O / down at 4 batch tiles);
+    sampled requests are checked against the oracle one by one."""
     shape = slice_of(MISTRAL_7B, L=1, name="7b-L1")
     vocab = synthetic_vocab(32000)
-    B = 512
     seed = 1005
     dm, eng = make_engine(shape, "bf16", vocab, B, seed, max_pages_per_slot=8)
     rng = random.Random(3)
     prompts = [[1, rng.randrange(3, 32000)] for _ in range(B)]
     rids = [eng.submit_request(p, 2, synth_prefix_len=20 + (i % 50), synth_seed=i) for i, p in enumerate(prompts)]
-    sample = [0, 1, 137, 255, 256, 300, 511]
+    sample = sorted({i for i in (0, 1, 137, 255, 256, 300, 511) if i < B} | {B - 1})
     w = oracle.Weights(shape, seed, bf16=True)
     oreqs = {}
     for i in sample:
