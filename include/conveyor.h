@@ -144,7 +144,7 @@ typedef struct {
  *   wgu        [L][2*d_ff][d]  gate/up interleaved in 64-row blocks: rows 128j..128j+63
  *                              are gate rows 64j.., rows 128j+64..128j+127 up rows 64j..
  *   wd         [L][d][d_ff]
- *   kv_pool    [L][n_pages][2 (K,V)][Hkv][16][hd]  (written by the engine)            */
+ *   kv_pool    [L][n_pages][Hkv][2 (K,V)][16][hd]  (written by the engine)            */
 typedef struct {
     const void* embed;
     const void* lm_head;

@@ -121,19 +121,18 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
             if (lane == 0) mbar_arrive_expect_tx(&full_bar[st], (uint32_t)(np * 2 * BLK));
             for (int p = 0; p < np; ++p) {
                 const int page = page_of(t * PPS + p);
-                if (lane == 0)
-                    for (int c = 0; c < 2; ++c) {
-                        const int row0 = ((((layer * P.n_pages + page) * 2 + c) * P.Hkv) + g) * 16;
-                        uint8_t* dst = stages + (size_t)st * STAGE + (size_t)(p * 2 + c) * BLK;
-                        if (HALVES == 2 && P.kv_tma3d) {
-                            // the whole 4 KB block in one box: [2 halves][16 rows][64], the same
-                            // shared-memory image as the two 2D boxes
-                            tma_load_3d(dst, &tmKV, &full_bar[st], 0, row0, 0, pol);
-                        } else {
-                            for (int h = 0; h < HALVES; ++h)
-                                tma_load_2d(dst + h * 2048, &tmKV, &full_bar[st], h * 64, row0, pol);
-                        }
+                if (lane == 0) {
+                    // the (page, kv-head) block: K rows 0-15 then V rows 16-31, contiguous in the
+                    // pool ([L][pages][Hkv][K/V][16][hd]); one box lands as [half][32 rows][64]
+                    const int row0 = ((layer * P.n_pages + page) * P.Hkv + g) * 32;
+                    uint8_t* dst = stages + (size_t)st * STAGE + (size_t)(p * 2) * BLK;
+                    if (HALVES == 2 && P.kv_tma3d) {
+                        tma_load_3d(dst, &tmKV, &full_bar[st], 0, row0, 0, pol);
+                    } else {
+                        for (int h = 0; h < HALVES; ++h)
+                            tma_load_2d(dst + h * 4096, &tmKV, &full_bar[st], h * 64, row0, pol);
                     }
+                }
             }
         };
         int t = 0;
@@ -195,7 +194,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
         mbar_wait(&full_bar[st], ph);
         if (pidx < n_pages) {
             const uint32_t kbase = smem_u32(stages + (size_t)st * STAGE + (size_t)(wp * 2) * BLK);
-            const uint32_t vbase = kbase + BLK;
+            const uint32_t vbase = kbase + 2048;  // [half][K 16 rows | V 16 rows][64]: halves 4 KB apart
             // ---- S^T = K . [q_hi|q_lo]^T
             float s[2][4];  // [key block of 8 cols? no: one n8 block]; s[0] keys grp / grp+8
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -203,7 +202,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
             for (int ks = 0; ks < KSTEPS; ++ks) {
                 const int r = (lane & 7) + ((lane >> 3) & 1) * 8;    // key row
                 const int dchunk = ks * 2 + (lane >> 4);             // 16-B chunk of dims
-                const uint32_t addr = kbase + (dchunk >> 3) * 2048 + sw128(r, dchunk & 7);
+                const uint32_t addr = kbase + (dchunk >> 3) * 4096 + sw128(r, dchunk & 7);
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4(addr, a0, a1, a2, a3);
                 mma_bf16_16816(acc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
@@ -268,7 +267,7 @@ __global__ void __launch_bounds__(kAtcThreads) attention_tc_kernel(const __grid_
                 const int mtx = lane >> 3, r = lane & 7;
                 const int key = r + (mtx >> 1) * 8;
                 const int dchunk = i * 2 + (mtx & 1);
-                const uint32_t addr = vbase + (dchunk >> 3) * 2048 + sw128(key, dchunk & 7);
+                const uint32_t addr = vbase + (dchunk >> 3) * 4096 + sw128(key, dchunk & 7);
                 uint32_t a0, a1, a2, a3;
                 ldsm_x4_t(addr, a0, a1, a2, a3);
                 mma_bf16_16816(o[i], a0, a1, a2, a3, pb0, pb1);

@@ -91,7 +91,7 @@ bool make_tmap_kv3(CUtensorMap* out, const void* base, uint64_t rows) {
     if (!fn) return false;
     cuuint64_t gdim[3] = {64, rows, 2};
     cuuint64_t gstride[2] = {256, 128};
-    cuuint32_t box[3] = {64, 16, 2};
+    cuuint32_t box[3] = {64, 32, 2};  // one (page, kv-head) K+V block: 32 rows x 2 halves
     cuuint32_t estride[3] = {1, 1, 1};
     CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), gdim, gstride, box, estride,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -772,7 +772,7 @@ cvy_status cvy_engine_create(const cvy_model_config* m, const cvy_engine_config*
         e->kv_tma3d = hd == 128;
         if (const char* v = getenv("CVY_KV_TMA3D")) e->kv_tma3d = e->kv_tma3d && atoi(v) != 0;
         if (e->kv_tma3d && !make_tmap_kv3(&e->tm_kv, w->kv_pool, rows)) e->kv_tma3d = false;
-        if (!e->kv_tma3d && !make_tmap(&e->tm_kv, w->kv_pool, rows, (uint64_t)hd, (uint64_t)hd, 16, 64)) {
+        if (!e->kv_tma3d && !make_tmap(&e->tm_kv, w->kv_pool, rows, (uint64_t)hd, (uint64_t)hd, 32, 64)) {
             cvy_engine_destroy(e);
             return fail(CVY_E_CUDA, "KV tensor map encode failed");
         }

@@ -202,7 +202,7 @@ CVY_DEV void epilogue_chunk(const StepParams& P, const EpiArgs& E, int n0, int c
                         const int g = rel / hd, e = rel % hd;
                         T* kv = reinterpret_cast<T*>(P.kv_pool) +
                                 (size_t)E.layer * P.n_pages * (size_t)(2 * P.Hkv * kPageTokens * hd) + M.kvoff[b] +
-                                (size_t)(c * P.Hkv + g) * (kPageTokens * hd) + e;
+                                (size_t)(g * 2 + c) * (kPageTokens * hd) + e;
                         store_rows<T, RP>(kv, w);
                     }
                 }

@@ -49,7 +49,7 @@ __global__ void synth_prefix_kernel(T* kv_pool, const int32_t* pages, int n_page
         uint64_t tid = (1ULL << 62) ^ (synth_seed * (uint64_t)L + (uint64_t)l);
         float v = hash_uniform_f32(0, tid, (uint64_t)idx, a);
         int page = pages[pos / kPageTokens];
-        size_t off = ((((size_t)l * n_pages_total + page) * 2 + c) * Hkv + g) * (size_t)(kPageTokens * hd) +
+        size_t off = ((((size_t)l * n_pages_total + page) * Hkv + g) * 2 + c) * (size_t)(kPageTokens * hd) +
                      (size_t)(pos % kPageTokens) * hd + e;
         kv_pool[off] = DT<T>::from_f(v);
     }
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
         float sv[kAttnMaxG];
         if (key < k_end) {
             const int page = pt[key / kPageTokens];
-            const T* krow = kv + layer_base + (size_t)page * page_stride + ((size_t)0 * P.Hkv + g) * kPageTokens * hd +
+            const T* krow = kv + layer_base + (size_t)page * page_stride + ((size_t)g * 2 + 0) * kPageTokens * hd +
                             (size_t)(key % kPageTokens) * hd;
 #pragma unroll
             for (int j = 0; j < kAttnMaxG; ++j) sv[j] = 0.f;
@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kAttnThreads) attention_kernel(const __grid_co
             for (int kk = 0; kk < kn; ++kk) {
                 const int kkey = k0 + kk;
                 const int page = pt[kkey / kPageTokens];
-                const T* vrow = kv + layer_base + (size_t)page * page_stride + ((size_t)1 * P.Hkv + g) * kPageTokens * hd +
+                const T* vrow = kv + layer_base + (size_t)page * page_stride + ((size_t)g * 2 + 1) * kPageTokens * hd +
                                 (size_t)(kkey % kPageTokens) * hd;
                 a += sc[j * kAttnThreads + kk] * DT<T>::to_f(vrow[e]);
             }

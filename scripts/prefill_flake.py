@@ -51,7 +51,7 @@ for name, extra in variants.items():
         kv = kvraw.float().cpu().numpy()
         if rep == 0:
             print("kv_pool elements", kv.size, "=", kv.size / (2 * 2 * 8 * 16 * 128), "pages x layers", flush=True)
-        kv = kv.reshape(2, -1, 2, 8, 16, 128)  # [L][pages][K/V][Hkv][16][hd]
+        kv = kv.reshape(2, -1, 8, 2, 16, 128)  # [L][pages][Hkv][K/V][16][hd]
         if rep == 0:
             nz = sorted(set((int(a), int(b)) for a, b in np.argwhere(np.abs(kv).sum(axis=(2, 3, 4, 5)) > 0)))
             print("nonzero (layer, page):", nz, flush=True)
@@ -73,7 +73,7 @@ for name, extra in variants.items():
                             owner.setdefault(int(pg), (sl, j))
                 agg = {}
                 for b in bad:
-                    l, pg, c, g, tk = (int(x) for x in b[:5])
+                    l, pg, g, c, tk = (int(x) for x in b[:5])
                     sl, j = owner.get(pg, (-1, -1))
                     key = (l, sl, j * 16 + tk if sl >= 0 else (pg, tk), "KV"[c])
                     agg.setdefault(key, set()).add(g)
