@@ -348,7 +348,10 @@ cvy_status cvy_stats_allgather(cvy_engine* const* engines, int32_t n, uint64_t* 
 /* Test hook: copy an internal device buffer of the last completed step to host memory.
  * which: 0 x (fp32 [Bmax][d]), 1 act, 2 q (fp32 [Bmax][H*hd]), 3 o, 4 h (model dtype
  * [Bmax][act_ld]), 5 ssq (fp32 [d/128][Bmax]), 6 page table (int32 [max_slots][max_pages_per_slot]),
- * 7 last chunked-prefill row table (int32 [3][512]: slot, position, token).  *bytes receives the buffer size; if dst is
+ * 7 last chunked-prefill row table (int32 [3][512]: slot, position, token); the last chunked-prefill
+ * pass's buffers (512 rows): 8 x (fp32 [512][d]), 9 q (fp32 [512][H*hd]), 20 o, 21 h, 22 act
+ * (model dtype [2 planes][512][act_ld]); 10-13 GEMM trace stamps (CVY_GEMM_TRACE_LAYER).
+ * CVY_E_STATE if the engine has no such buffer.  *bytes receives the buffer size; if dst is
  * NULL only the size is returned. */
 cvy_status cvy_debug_buffer(cvy_engine* e, int32_t which, void* dst, size_t cap, size_t* bytes);
 
