@@ -519,7 +519,7 @@ def test_tool_registration_errors():
 
 
 # ------------------------------------------------------------------ NEXT-1: chunked prefill
-@pytest.mark.parametrize("which", ["tiny", "7b-L2"])
+@pytest.mark.parametrize("which", ["tiny", "7b-L2", "7b-L2-wide"])
 def test_chunked_prefill_prompts_and_observations_match_oracle(which):
     """CVY_ENGINE_CHUNKED_PREFILL: all prompt tokens but the last (and, after a FINAL, the last
     generated token + all observation tokens but the last) run as one batched prefill pass;
@@ -536,7 +536,10 @@ def test_chunked_prefill_prompts_and_observations_match_oracle(which):
     dm, eng = make_engine(shape, "bf16", vocab, B, seed, flags=flags, max_pages_per_slot=16)
     w = oracle.Weights(shape, seed, bf16=True)
     # 1 + 16 + 39 + 150 (+ the 65-token prompt's 64) rows: a 256-row pass (unmerged stream-K GEMMs)
-    prompts = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 2, 17, 40, 151 if which == "tiny" else 65)]
+    # 7b-L2-wide: 205 prefill rows -> a 256-row pass on two batch tiles (CTA-pair stream-K QKV and
+    # gate/up, cluster split-K O / down)
+    last = {"tiny": 151, "7b-L2": 65, "7b-L2-wide": 150}[which]
+    prompts = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 2, 17, 40, last)]
     prefix = [0, 9, 0, 21, 3]
     obs = [[rng.randrange(3, V) for _ in range(n)] for n in (1, 5, 30, 2, 0)]
     oreqs, rids = [], []
